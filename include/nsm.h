@@ -1,0 +1,186 @@
+/*
+ * nsm.h -- C ABI of the B200 (sm_100a) neural-shadow-mapping inference path.
+ *
+ * The path is the per-frame inference of the reference package `shadowkit`
+ * (/root/reference/pkg/src/shadowkit): stage 1 `raster.assemble_features`
+ * (G-buffer + shadow map -> 4 input planes) and stage 2 `network.forward`
+ * (compact space-to-depth U-Net -> visibility in [0, 1]).  Every entry point
+ * below replaces one reference interface; the file:line it replaces is given
+ * beside it.  No torch / C++ types cross this boundary: plain pointers, sizes
+ * and POD structs.  Device pointers are caller-owned (e.g. torch CUDA tensors);
+ * the library never allocates per call (the plan owns its packed weights).
+ *
+ * Errors: every call returns an nsm_status; `nsm_last_error()` gives the
+ * thread-local message.  The Python host maps the codes back onto the
+ * reference's exception types:
+ *   NSM_ERR_SHAPE   -> ValueError    (network.py:169-173 messages)
+ *   NSM_ERR_FRUSTUM -> raster.FrustumError (raster.py:60-61, 251-255)
+ *   NSM_ERR_FORMAT  -> fileio.FormatError  (fileio.py:22-23, network.py:272-273)
+ *   NSM_ERR_ARG     -> ValueError
+ *   NSM_ERR_CUDA    -> RuntimeError
+ * Thread safety: a plan is immutable after nsm_plan_create and may be used
+ * from several host threads on distinct streams with distinct workspaces.
+ */
+#ifndef NSM_H
+#define NSM_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define NSM_ABI_VERSION 1
+#define NSM_MAX_FRAMES_PER_LAUNCH 8
+
+typedef enum nsm_status {
+    NSM_OK = 0,
+    NSM_ERR_ARG = 1,
+    NSM_ERR_SHAPE = 2,
+    NSM_ERR_FRUSTUM = 3,
+    NSM_ERR_FORMAT = 4,
+    NSM_ERR_CUDA = 5,
+    NSM_ERR_UNSUPPORTED = 6
+} nsm_status;
+
+typedef enum nsm_dtype {
+    NSM_F32 = 0,   /* reference precision (fp32 oracle parity, <= 1e-4)   */
+    NSM_F16 = 1,   /* fp16 operands, fp32 accumulate (<= 1e-2 / 1e-4 MSE) */
+    NSM_BF16 = 2,  /* bf16 operands, fp32 accumulate                      */
+    NSM_F64 = 3    /* G-buffer planes only (drop-in of fp64 numpy buffers) */
+} nsm_dtype;
+
+/* network.NetworkConfig (network.py:44-76). */
+typedef struct nsm_net_config {
+    int32_t layers;
+    int32_t base_channels;
+    int32_t in_channels;
+    int32_t use_space_to_depth;
+    int32_t channel_cap;
+} nsm_net_config;
+
+/* raster.EmitterView (raster.py:64-73): square frustum from the emitter
+ * centre; `height`/`width` is the shadow-map resolution. */
+typedef struct nsm_emitter_view {
+    double position[3];
+    double forward[3];
+    double up[3];
+    double right[3];
+    double tan_half;
+    int32_t height;
+    int32_t width;
+} nsm_emitter_view;
+
+/* scene.CameraPose (scene.py:102-114); forward/up already orthonormal. */
+typedef struct nsm_camera {
+    double position[3];
+    double forward[3];
+    double up[3];
+    double fov_y;
+    int32_t height;
+    int32_t width;
+} nsm_camera;
+
+/* Per-frame constants of one frame in a batch. */
+typedef struct nsm_frame {
+    nsm_camera camera;
+    nsm_emitter_view view;
+    double emitter_center[3];
+    double size_index;   /* ch2 dc offset (raster.py:276), no range check */
+    double bias;         /* acne bias b; ShadowMap.default_bias = 1e-3 * diag */
+} nsm_frame;
+
+/* raster.GBuffer (raster.py:154-170) as planar device buffers of one batch:
+ * frame f, plane element (y, x) of d is d[f * frame_stride + y * W + x];
+ * normal / position are (3, H, W) per frame at the same frame_stride * 3.
+ * z_f / c_e / c_c / coverage are optional: when NULL they are derived from
+ * the planes exactly as render_gbuffer does (raster.py:222-232) and coverage
+ * is d > 0. */
+typedef struct nsm_gbuffer {
+    nsm_dtype dtype;            /* NSM_F32 or NSM_F64 */
+    const void* d;
+    const void* normal;
+    const void* position;
+    const void* z_f;
+    const void* c_e;
+    const void* c_c;
+    const uint8_t* coverage;
+    int64_t frame_stride;       /* elements per (H, W) plane-set of one frame */
+} nsm_gbuffer;
+
+typedef struct nsm_plan nsm_plan;
+
+/* ---- plan layer: network.init_weights / load_network -> kernel layout ----
+ * Replaces the weight dict consumed by network.forward (network.py:165-195;
+ * names/shapes per network._named_params, network.py:277-285).  host_data[i]
+ * is an fp32 OIHW (weights) or (O,) (bias) array of shape dims[i][0..ndims[i]).
+ * A name set or shape that does not match cfg -> NSM_ERR_FORMAT
+ * (network.py:271-273); an invalid cfg -> NSM_ERR_ARG (network.py:52-58). */
+nsm_status nsm_plan_create(const nsm_net_config* cfg, int32_t n_tensors,
+                           const char* const* names, const float* const* host_data,
+                           const int32_t* ndims, const int32_t* const* dims,
+                           nsm_dtype act_dtype, nsm_plan** out_plan);
+void nsm_plan_destroy(nsm_plan* plan);
+nsm_status nsm_plan_info(const nsm_plan* plan, nsm_net_config* cfg, nsm_dtype* act_dtype,
+                         int64_t* n_params);
+
+/* Device workspace needed by nsm_forward / nsm_infer for a batch of n frames
+ * of h x w input pixels. */
+size_t nsm_workspace_size(const nsm_plan* plan, int32_t n, int32_t h, int32_t w);
+
+/* ---- stage 1: raster.assemble_features (raster.py:266-278) ----
+ * out_planes: (n, 4, h, w) fp32 device.  texel_idx (nullable): (n, 2, h, w)
+ * int32 (row, col) nearest texels, -1 on uncovered pixels.  first_bad: n
+ * device int64 = row-major index of the first covered pixel that projects
+ * outside the frustum, INT64_MAX if none (raster.py:251-255); the call
+ * itself does not synchronise, the host raises FrustumError after reading it.
+ * sm: (n, Hs, Ws) fp32 radial depths, +inf = miss, frame f at f * sm_stride. */
+nsm_status nsm_features(const nsm_gbuffer* g, const float* sm, int64_t sm_stride,
+                        const nsm_frame* frames, int32_t n, int32_t h, int32_t w,
+                        float* out_planes, int32_t* texel_idx, int64_t* first_bad,
+                        void* stream);
+
+/* ---- stage 2: network.forward (network.py:165-209) ----
+ * x: (n, in_channels, h, w) fp32 device, y: (n, 1, h, w) fp32 device.
+ * h, w must be divisible by 2**(layers-1) (NSM_ERR_SHAPE otherwise). */
+nsm_status nsm_forward(const nsm_plan* plan, const float* x, int32_t n, int32_t h,
+                       int32_t w, float* y, void* workspace, size_t ws_bytes, void* stream);
+
+/* ---- fused stages 1+2: the hot path ----
+ * assemble_features then forward per frame, features never written to HBM
+ * on the fp16/bf16 plans.  h need not be divisible by 2**(layers-1): rows /
+ * columns up to the next multiple are treated as uncovered (zero features,
+ * the same padding the oracle applies) and cropped from y.  y: (n, 1, h, w)
+ * of y_dtype (NSM_F32 or NSM_F16). */
+nsm_status nsm_infer(const nsm_plan* plan, const nsm_gbuffer* g, const float* sm,
+                     int64_t sm_stride, const nsm_frame* frames, int32_t n, int32_t h,
+                     int32_t w, void* y, nsm_dtype y_dtype, int64_t* first_bad,
+                     void* workspace, size_t ws_bytes, void* stream);
+
+/* ---- input producers (the step before the path) ----
+ * raster.render_gbuffer (raster.py:217-242) depth/normal/position planes and
+ * raster.render_shadowmap (raster.py:206-214) over an analytic primitive
+ * table: prims = device (n_prims, 16) fp64 rows, see scenes.primitive_table. */
+nsm_status nsm_render_gbuffer(const double* prims, int32_t n_prims, const nsm_camera* cam,
+                              float* d, float* normal, float* position, void* stream);
+nsm_status nsm_render_shadowmap(const double* prims, int32_t n_prims,
+                                const nsm_emitter_view* view, float* depth, void* stream);
+
+/* ---- tracing / launch accounting (tracing) ----
+ * nsm_launch_count: kernels launched by this library since load (graph
+ * replays not included).  nsm_profile_enable(1): record a CUDA-event pair
+ * on the launching stream around every eager (non-captured) launch;
+ * nsm_profile_report writes "name launches total_ms" lines into buf, clears
+ * the records and returns the full report length. */
+int64_t nsm_launch_count(void);
+void nsm_profile_enable(int32_t on);
+int32_t nsm_profile_report(char* buf, size_t cap);
+
+const char* nsm_last_error(void);
+int32_t nsm_abi_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* NSM_H */

@@ -1,0 +1,63 @@
+// Plan layer: the device-resident, kernel-layout form of a NetworkConfig +
+// weight dict (network.py:44-144, 277-285).
+#pragma once
+
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+
+namespace nsm {
+
+constexpr int kMaxLevels = 8;
+
+struct ConvW {
+    int cin = 0, cout = 0, k = 0;
+    const float* w32 = nullptr;   // OIHW fp32 (reference layout)
+    const float* b32 = nullptr;   // (O,) fp32
+    const void* wpk = nullptr;    // packed 16-bit tiles for the tensor-core path
+    bool present() const { return k != 0; }
+};
+
+struct Level {
+    ConvW enc3, enc1, dec3, dec1;
+};
+
+struct Plan {
+    nsm_net_config cfg{};
+    nsm_dtype act = NSM_F32;
+    int nlev = 0;                 // len(level_channels)
+    int chans[kMaxLevels] = {};
+    int first_in = 0;
+    int out_ch = 0;
+    Level lev[kMaxLevels];
+    ConvW head;
+    int64_t n_params = 0;
+    void* dev = nullptr;          // one allocation holding every tensor
+    size_t dev_bytes = 0;
+};
+
+size_t forward_f32_workspace(const Plan& p, int n, int h, int w);
+nsm_status forward_f32(const Plan& p, const float* x, int n, int h, int w, float* out, void* ws,
+                       size_t ws_bytes, cudaStream_t st);
+
+// fp16 / bf16 tensor-core path (net_f16.cu)
+bool f16_supported(const Plan& p);
+size_t infer_f16_workspace(const Plan& p, int n, int h, int w);
+nsm_status pack_f16(Plan& p, std::vector<char>& host_blob, size_t& offset_out);
+nsm_status forward_f16(const Plan& p, const float* x, int n, int h, int w, float* out, void* ws,
+                       size_t ws_bytes, cudaStream_t st);
+nsm_status infer_f16(const Plan& p, const nsm_gbuffer* g, const float* sm, int64_t sm_stride,
+                     const nsm_frame* frames, int n, int h, int w, void* y, nsm_dtype y_dtype,
+                     int64_t* first_bad, void* ws, size_t ws_bytes, cudaStream_t st);
+
+nsm_status launch_features(const nsm_gbuffer* g, const float* sm, int64_t sm_stride,
+                           const nsm_frame* frames, int32_t n, int32_t h, int32_t w, int32_t ho,
+                           int32_t wo, float* out, int32_t* tidx, int64_t* first_bad,
+                           cudaStream_t st);
+nsm_status launch_render_gbuffer(const double* prims, int32_t n_prims, const nsm_camera* cam,
+                                 float* d, float* normal, float* position, cudaStream_t st);
+nsm_status launch_render_shadowmap(const double* prims, int32_t n_prims,
+                                   const nsm_emitter_view* view, float* depth, cudaStream_t st);
+
+}  // namespace nsm
