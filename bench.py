@@ -223,6 +223,12 @@ def run_ours(args):
 
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clk:
+        # keep the GPU loaded ~1 s so nvidia-smi samples clocks under load
+        t_end = time.time() + 1.0
+        while time.time() < t_end:
+            for _ in range(20):
+                step()
+            torch.cuda.synchronize()
         barrier(world)
         torch.cuda.synchronize()
         e0.record()

@@ -100,6 +100,11 @@ __global__ void fill_i64(int64_t* p, int n, int64_t v) {
     if (i < n) p[i] = v;
 }
 
+void launch_fill_i64(int64_t* p, int n, int64_t v, cudaStream_t st) {
+    NSM_PROF("fill_i64", st);
+    fill_i64<<<(n + 127) / 128, 128, 0, st>>>(p, n, v);
+}
+
 nsm_status launch_features(const nsm_gbuffer* g, const float* sm, int64_t sm_stride,
                            const nsm_frame* frames, int32_t n, int32_t h, int32_t w,
                            int32_t ho, int32_t wo, float* out, int32_t* tidx,

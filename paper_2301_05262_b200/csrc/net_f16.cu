@@ -1,23 +1,938 @@
-// fp16 / bf16 tensor-core path (placeholder until the fused level kernels land).
+// fp16 / bf16 hot path: the U-Net of network.forward (network.py:165-209)
+// as level-fused tensor-core kernels, with the feature pass
+// (raster.assemble_features, raster.py:266-278) fused into the level-0
+// encoder so that the 4 feature planes never reach HBM.
+//
+//   enc0   features + space_to_depth + l0.enc3 + l0.enc1 + avg_pool2  (mma.sync)
+//   lv<>   l1 enc / l2 enc / l3 bottleneck / l2 dec / l1 dec          (tcgen05)
+//   dec0   up2 + l0.dec3 + l0.dec1 + head                              (mma.sync)
+//   recon  bilinear(ch0) + depth_to_space(detail) + sigmoid, crop      (CUDA cores)
+//
+// Activations live in NHWC 16-bit tensors between kernels (L2-resident for
+// a chunk of frames); inside a kernel they live in chunk-planar SMEM tiles
+// (tc.cuh) so that every 3x3 tap of the implicit GEMM is an address offset,
+// for ldmatrix rows and for UMMA descriptors alike.  Bias, ReLU, pooling,
+// upsampling, skip sums, the head and the sigmoid run in fp32 registers.
+#include <algorithm>
+#include <cmath>
+#include <vector>
+
 #include "common.cuh"
 #include "net.cuh"
+#include "prof.cuh"
+#include "tc.cuh"
 
 namespace nsm {
 
-bool f16_supported(const Plan&) { return false; }
+namespace {
 
-size_t infer_f16_workspace(const Plan&, int, int, int) { return 0; }
+// ------------------------------------------------------------------ config
+constexpr int kChunkFrames = 2;       // frames per pass through all levels (L2 residency)
+constexpr int E0_TH = 16, E0_TW = 64;  // level-0 output tile (enc0 / dec0)
+constexpr int E0_IR = E0_TH + 2, E0_IC = E0_TW + 2;
+constexpr int E0_PLANE = plane_bytes(E0_IR * E0_IC, 2);
+constexpr int E0_SMEM = 2 * E0_PLANE;
 
-nsm_status pack_f16(Plan&, std::vector<char>&, size_t&) { return NSM_OK; }
-
-nsm_status forward_f16(const Plan&, const float*, int, int, int, float*, void*, size_t,
-                       cudaStream_t) {
-    return fail(NSM_ERR_UNSUPPORTED, "16-bit kernels not built");
+// packed-weight formats (offsets into the plan's device block)
+//  "frag": mma.sync B fragments, [tap][kk][nt][lane][2] u32
+//  "umma": K-major core matrices, [tap][kk][2 chunks][N][8] elements
+size_t frag_words(int taps, int cin, int cout) {
+    return (size_t)taps * ((cin + 15) / 16) * ((cout + 7) / 8) * 64;
 }
 
-nsm_status infer_f16(const Plan&, const nsm_gbuffer*, const float*, int64_t, const nsm_frame*, int,
-                     int, int, void*, nsm_dtype, int64_t*, void*, size_t, cudaStream_t) {
-    return fail(NSM_ERR_UNSUPPORTED, "16-bit kernels not built");
+// l0.enc3 reads a tile whose channel k' = (2dy + dx) * 4 + c holds s2d
+// channel 4c + 2dy + dx (space_to_depth, autodiff.py:290-308), so each
+// full-resolution pixel writes its 4 features contiguously.
+int perm_s2d(int kp, int cin4) {
+    if (cin4 != 16) return kp;
+    return 4 * (kp % 4) + kp / 4;
+}
+
+template <typename T>
+uint16_t to_bits(float v) {
+    T h = (T)v;
+    return *reinterpret_cast<uint16_t*>(&h);
+}
+
+template <typename T>
+void pack_frag(const float* w, int cout, int cin, int k, bool s2d_perm, std::vector<uint32_t>& out) {
+    const int taps = k * k, KK = (cin + 15) / 16, NT = (cout + 7) / 8;
+    out.assign(frag_words(taps, cin, cout), 0u);
+    auto B = [&](int tap, int kk, int n) -> float {
+        if (n >= cout || kk >= cin) return 0.f;
+        const int ci = s2d_perm ? perm_s2d(kk, cin) : kk;
+        return w[((size_t)n * cin + ci) * taps + tap];
+    };
+    for (int tap = 0; tap < taps; ++tap)
+        for (int kk = 0; kk < KK; ++kk)
+            for (int nt = 0; nt < NT; ++nt)
+                for (int l = 0; l < 32; ++l) {
+                    const int g = l >> 2, t = l & 3, n = nt * 8 + g, k0 = kk * 16 + 2 * t;
+                    const size_t o = ((((size_t)tap * KK + kk) * NT + nt) * 32 + l) * 2;
+                    out[o] = to_bits<T>(B(tap, k0, n)) | ((uint32_t)to_bits<T>(B(tap, k0 + 1, n)) << 16);
+                    out[o + 1] = to_bits<T>(B(tap, k0 + 8, n)) | ((uint32_t)to_bits<T>(B(tap, k0 + 9, n)) << 16);
+                }
+}
+
+template <typename T>
+void pack_umma(const float* w, int cout, int cin, int k, std::vector<uint16_t>& out) {
+    const int taps = k * k, KK = cin / 16;
+    out.assign((size_t)taps * cin * cout, 0);
+    for (int tap = 0; tap < taps; ++tap)
+        for (int kk = 0; kk < KK; ++kk)
+            for (int c = 0; c < 2; ++c)
+                for (int n = 0; n < cout; ++n)
+                    for (int e = 0; e < 8; ++e) {
+                        const int ci = kk * 16 + c * 8 + e;
+                        out[((((size_t)tap * KK + kk) * 2 + c) * cout + n) * 8 + e] =
+                            to_bits<T>(w[((size_t)n * cin + ci) * taps + tap]);
+                    }
+}
+
+// ------------------------------------------------------------- level 0 (mma.sync)
+struct Enc0Args {
+    GBufK g;
+    const float* sm;
+    int64_t sm_stride;
+    FrameTable tab;
+    const float* x;       // features (N, 4, H0*2, W0*2) fp32 when not from the G-buffer
+    int h, w;             // frame pixels actually present (rows/cols beyond are padding)
+    int H0, W0;           // level-0 dims (padded frame / 2)
+    const uint2* wb3;     // l0.enc3 fragments [9][2 nt][32]
+    const uint2* wb1;     // l0.enc1 fragments [2 nt][32]
+    const float* b3;
+    const float* b1;
+    void* out;            // pooled (N, H0/2, W0/2, 16)
+    int64_t* first_bad;
+};
+
+// Stage-1 per-pixel math of the fused kernel: fp64 projection for the texel
+// index (bit-exact np.rint), fp32 for the rest (the values are rounded to
+// 16 bits right after).  Returns ch0..ch3 (raster.py:262, 272-276).
+__device__ __forceinline__ float4 pixel_features(const FrameK& F, const GBufK& g, const float* sm,
+                                                 int64_t base, int64_t pix, int fy, int fx,
+                                                 int64_t hw, int64_t* first_bad) {
+    const float* dp = reinterpret_cast<const float*>(g.d);
+    const float d = __ldg(dp + base + pix);
+    if (!(d > 0.f)) return make_float4(0.f, 0.f, 0.f, 0.f);
+    const float* P = reinterpret_cast<const float*>(g.position) + 3 * base + pix;
+    const float* Nn = reinterpret_cast<const float*>(g.normal) + 3 * base + pix;
+    const float px = __ldg(P), py = __ldg(P + hw), pz = __ldg(P + 2 * hw);
+    const float nx = __ldg(Nn), ny = __ldg(Nn + hw), nz = __ldg(Nn + 2 * hw);
+    int ri, ci;
+    if (!texel_of(F, px, py, pz, ri, ci)) atomic_min_i64(first_bad, pix);
+    const float look = __ldg(sm + (int64_t)ri * F.ws + ci);
+    const float tx = (float)(F.ec[0] - (double)px), ty = (float)(F.ec[1] - (double)py),
+                tz = (float)(F.ec[2] - (double)pz);
+    const float zf = sqrtf(tx * tx + ty * ty + tz * tz);
+    const float ce = fminf(fmaxf((nx * tx + ny * ty + nz * tz) / zf, 0.f), 1.f);
+    const float u = ((fx + 0.5f) / F.cw * 2.f - 1.f) * (float)F.half_w;
+    const float v = (1.f - (fy + 0.5f) / F.ch * 2.f) * (float)F.half_h;
+    const float rx = (float)F.cf[0] + u * (float)F.cr[0] + v * (float)F.cu[0];
+    const float ry = (float)F.cf[1] + u * (float)F.cr[1] + v * (float)F.cu[1];
+    const float rz = (float)F.cf[2] + u * (float)F.cr[2] + v * (float)F.cu[2];
+    const float cc = fminf(fmaxf(-(nx * rx + ny * ry + nz * rz) * rsqrtf(rx * rx + ry * ry + rz * rz), 0.f), 1.f);
+    float ch0 = 0.f, ch1 = 1.f;
+    if (isfinite(look)) {
+        const float m = fminf(look, zf);
+        ch0 = (m - zf) + (float)F.bias;
+        ch1 = (m + (float)F.bias) / zf;
+    }
+    return make_float4(ch0, ch1, ce + (float)F.size_index, cc / d);
+}
+
+// Sliding-window 3x3 conv on a 16-pixel strip: every input row's three
+// dx-shifted A fragments are loaded once and applied to the three output
+// rows that need them, so ldmatrix traffic is 3 instead of 9 loads per row.
+template <typename T, int ROWS, class Epi>
+__device__ __forceinline__ void conv3_strip16(uint32_t sbase, int plane, int rowpix, int r0, int sx,
+                                              const uint32_t (&B3)[9][2][2], Epi&& epi) {
+    const int lane = threadIdx.x & 31;
+    const int lm = lane >> 3, li = lane & 7;
+    const uint32_t a_off = (lm >> 1) * plane + (li + 8 * (lm & 1)) * 16;
+    float acc[3][2][4];
+#pragma unroll
+    for (int s = 0; s < 3; ++s)
+#pragma unroll
+        for (int n = 0; n < 2; ++n)
+#pragma unroll
+            for (int e = 0; e < 4; ++e) acc[s][n][e] = 0.f;
+#pragma unroll
+    for (int ir = 0; ir < ROWS + 2; ++ir) {
+        uint32_t A[3][4];
+#pragma unroll
+        for (int dx = 0; dx < 3; ++dx)
+            ldsm_x4(sbase + a_off + ((r0 + ir) * rowpix + sx + dx) * 16, A[dx]);
+#pragma unroll
+        for (int ky = 0; ky < 3; ++ky) {
+            const int oo = ir - ky;
+            if (oo >= 0 && oo < ROWS) {
+#pragma unroll
+                for (int dx = 0; dx < 3; ++dx)
+#pragma unroll
+                    for (int n = 0; n < 2; ++n)
+                        mma16816<T>(acc[oo % 3][n], A[dx], B3[ky * 3 + dx][n][0], B3[ky * 3 + dx][n][1]);
+            }
+        }
+        if (ir >= 2) {
+            const int oo = ir - 2;
+            epi(oo, acc[oo % 3]);
+#pragma unroll
+            for (int n = 0; n < 2; ++n)
+#pragma unroll
+                for (int e = 0; e < 4; ++e) acc[oo % 3][n][e] = 0.f;
+        }
+    }
+}
+
+// relu(acc + bias) of a 16x16 m16n8 pair, packed as the A fragment of the
+// next 1x1 conv (accumulator layout == A-operand layout).
+template <typename T>
+__device__ __forceinline__ void acc_to_a(const float (&acc)[2][4], const float (&bias)[2][2], bool relu,
+                                         uint32_t a[4]) {
+    float v[2][4];
+#pragma unroll
+    for (int n = 0; n < 2; ++n)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+            v[n][e] = acc[n][e] + bias[n][e & 1];
+            if (relu) v[n][e] = fmaxf(v[n][e], 0.f);
+        }
+    a[0] = Elem<T>::pack(v[0][0], v[0][1]);
+    a[1] = Elem<T>::pack(v[0][2], v[0][3]);
+    a[2] = Elem<T>::pack(v[1][0], v[1][1]);
+    a[3] = Elem<T>::pack(v[1][2], v[1][3]);
+}
+
+template <typename T, bool kFromGBuffer>
+__global__ void __launch_bounds__(256, 2) enc0_kernel(Enc0Args a) {
+    extern __shared__ __align__(128) uint8_t smem[];
+    const int f = blockIdx.z;
+    const int tx0 = blockIdx.x * E0_TW, ty0 = blockIdx.y * E0_TH;
+    const uint32_t sbase = smem_u32(smem);
+    const int H1 = a.H0 / 2, W1 = a.W0 / 2;
+
+    // ---- stage 1: features of the halo'd tile, s2d-packed into SMEM
+    {
+        const int64_t hw = (int64_t)a.h * a.w;
+        const int64_t base = (int64_t)f * a.g.frame_stride;
+        constexpr int RC = 2 * E0_IC;
+        for (int i = threadIdx.x; i < 2 * E0_IR * RC; i += blockDim.x) {
+            const int ry = i / RC, rx = i - ry * RC;
+            const int fy = 2 * (ty0 - 1) + ry, fx = 2 * (tx0 - 1) + rx;
+            float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (fy >= 0 && fx >= 0 && fy < a.h && fx < a.w) {
+                if (kFromGBuffer) {
+                    v = pixel_features(a.tab.f[f], a.g, a.sm + f * a.sm_stride, base,
+                                       (int64_t)fy * a.w + fx, fy, fx, hw, a.first_bad + f);
+                } else {
+                    const float* xp = a.x + (int64_t)f * 4 * hw + (int64_t)fy * a.w + fx;
+                    v = make_float4(__ldg(xp), __ldg(xp + hw), __ldg(xp + 2 * hw), __ldg(xp + 3 * hw));
+                }
+            }
+            const int p = (ry >> 1) * E0_IC + (rx >> 1);
+            uint2 pk = make_uint2(Elem<T>::pack(v.x, v.y), Elem<T>::pack(v.z, v.w));
+            *reinterpret_cast<uint2*>(smem + (ry & 1) * E0_PLANE + p * 16 + (rx & 1) * 8) = pk;
+        }
+    }
+    __syncthreads();
+
+    // ---- stage 2: l0.enc3 (sliding window) -> l0.enc1 -> avg_pool2
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int g = lane >> 2, t = lane & 3;
+    const int sx = (warp & 3) * 16, r0 = (warp >> 2) * 8;
+    uint32_t B3[9][2][2], B1[2][2];
+#pragma unroll
+    for (int tap = 0; tap < 9; ++tap)
+#pragma unroll
+        for (int n = 0; n < 2; ++n) {
+            const uint2 v = __ldg(a.wb3 + (tap * 2 + n) * 32 + lane);
+            B3[tap][n][0] = v.x;
+            B3[tap][n][1] = v.y;
+        }
+#pragma unroll
+    for (int n = 0; n < 2; ++n) {
+        const uint2 v = __ldg(a.wb1 + n * 32 + lane);
+        B1[n][0] = v.x;
+        B1[n][1] = v.y;
+    }
+    float bias3[2][2], bias1[2][2];
+#pragma unroll
+    for (int n = 0; n < 2; ++n)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+            bias3[n][e] = __ldg(a.b3 + n * 8 + 2 * t + e);
+            bias1[n][e] = __ldg(a.b1 + n * 8 + 2 * t + e);
+        }
+    float pp[2][4];
+    T* out = reinterpret_cast<T*>(a.out);
+    conv3_strip16<T, 8>(sbase, E0_PLANE, E0_IC, r0, sx, B3, [&](int oo, float (&acc)[2][4]) {
+        uint32_t a1[4];
+        acc_to_a<T>(acc, bias3, true, a1);
+        float u[2][4] = {};
+#pragma unroll
+        for (int n = 0; n < 2; ++n) mma16816<T>(u[n], a1, B1[n][0], B1[n][1]);
+#pragma unroll
+        for (int n = 0; n < 2; ++n)
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                float v = fmaxf(u[n][e] + bias1[n][e & 1], 0.f);
+                v += __shfl_xor_sync(0xffffffffu, v, 4);       // x-neighbour pixel
+                if (oo & 1) pp[n][e] += v;
+                else pp[n][e] = v;
+            }
+        if (oo & 1) {
+            const int py = (ty0 + r0 + oo) >> 1;
+            const int pxb = (tx0 + sx) >> 1;
+            if (!(g & 1) && py < H1) {
+                T* orow = out + ((int64_t)f * H1 + py) * W1 * 16;
+#pragma unroll
+                for (int hlf = 0; hlf < 2; ++hlf) {
+                    const int px = pxb + (g >> 1) + 4 * hlf;
+                    if (px < W1) {
+#pragma unroll
+                        for (int n = 0; n < 2; ++n)
+                            *reinterpret_cast<uint32_t*>(orow + px * 16 + n * 8 + 2 * t) =
+                                Elem<T>::pack(pp[n][2 * hlf] * 0.25f, pp[n][2 * hlf + 1] * 0.25f);
+                    }
+                }
+            }
+        }
+    });
+}
+
+struct Dec0Args {
+    const void* x;        // D1: (N, H0/2, W0/2, 16)
+    int H0, W0;
+    const uint2* wb3;     // l0.dec3 [9][2][32]
+    const uint2* wb1;     // l0.dec1 [2][32]
+    const uint2* wbh;     // head [1][32] (n 4..7 zero)
+    const float* b3;
+    const float* b1;
+    const float* bh;
+    float4* y;            // (N, H0, W0) x 4 head channels, fp32
+};
+
+// Bilinear 2x of an NHWC 16-bit tensor at one output pixel, 8 channels
+// (bilinear_upsample2 + _upsample_taps, autodiff.py:258-274: rows then cols).
+template <typename T>
+__device__ __forceinline__ void up2_chunk(const T* x, int hl, int wl, int C, int oy, int ox, int chunk,
+                                          float v[8]) {
+    const float sy = fminf(fmaxf((oy + 0.5f) * 0.5f - 0.5f, 0.f), (float)(hl - 1));
+    const float sx = fminf(fmaxf((ox + 0.5f) * 0.5f - 0.5f, 0.f), (float)(wl - 1));
+    const int y0 = (int)sy, x0 = (int)sx;
+    const int y1 = min(y0 + 1, hl - 1), x1 = min(x0 + 1, wl - 1);
+    const float wy = sy - y0, wx = sx - x0;
+    const uint4 q00 = __ldg(reinterpret_cast<const uint4*>(x + ((int64_t)y0 * wl + x0) * C + chunk * 8));
+    const uint4 q10 = __ldg(reinterpret_cast<const uint4*>(x + ((int64_t)y1 * wl + x0) * C + chunk * 8));
+    const uint4 q01 = __ldg(reinterpret_cast<const uint4*>(x + ((int64_t)y0 * wl + x1) * C + chunk * 8));
+    const uint4 q11 = __ldg(reinterpret_cast<const uint4*>(x + ((int64_t)y1 * wl + x1) * C + chunk * 8));
+    const uint32_t* a00 = &q00.x;
+    const uint32_t* a10 = &q10.x;
+    const uint32_t* a01 = &q01.x;
+    const uint32_t* a11 = &q11.x;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const float2 p00 = Elem<T>::unpack(a00[i]), p10 = Elem<T>::unpack(a10[i]);
+        const float2 p01 = Elem<T>::unpack(a01[i]), p11 = Elem<T>::unpack(a11[i]);
+        const float c0x = p00.x * (1.f - wy) + p10.x * wy, c1x = p01.x * (1.f - wy) + p11.x * wy;
+        const float c0y = p00.y * (1.f - wy) + p10.y * wy, c1y = p01.y * (1.f - wy) + p11.y * wy;
+        v[2 * i] = c0x * (1.f - wx) + c1x * wx;
+        v[2 * i + 1] = c0y * (1.f - wx) + c1y * wx;
+    }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256, 2) dec0_kernel(Dec0Args a) {
+    extern __shared__ __align__(128) uint8_t smem[];
+    const int f = blockIdx.z;
+    const int tx0 = blockIdx.x * E0_TW, ty0 = blockIdx.y * E0_TH;
+    const uint32_t sbase = smem_u32(smem);
+    const int H1 = a.H0 / 2, W1 = a.W0 / 2;
+    const T* xf = reinterpret_cast<const T*>(a.x) + (int64_t)f * H1 * W1 * 16;
+    // ---- up2(D1) over the halo'd tile (zero outside the frame: conv padding)
+    for (int i = threadIdx.x; i < E0_IR * E0_IC * 2; i += blockDim.x) {
+        const int c = i & 1, p = i >> 1;
+        const int ti = p / E0_IC, tj = p - ti * E0_IC;
+        const int oy = ty0 - 1 + ti, ox = tx0 - 1 + tj;
+        float v[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+        if (oy >= 0 && ox >= 0 && oy < a.H0 && ox < a.W0) up2_chunk<T>(xf, H1, W1, 16, oy, ox, c, v);
+        uint4 q;
+        q.x = Elem<T>::pack(v[0], v[1]);
+        q.y = Elem<T>::pack(v[2], v[3]);
+        q.z = Elem<T>::pack(v[4], v[5]);
+        q.w = Elem<T>::pack(v[6], v[7]);
+        *reinterpret_cast<uint4*>(smem + c * E0_PLANE + p * 16) = q;
+    }
+    __syncthreads();
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int g = lane >> 2, t = lane & 3;
+    const int sx = (warp & 3) * 16, r0 = (warp >> 2) * 8;
+    uint32_t B3[9][2][2], B1[2][2], BH[2];
+#pragma unroll
+    for (int tap = 0; tap < 9; ++tap)
+#pragma unroll
+        for (int n = 0; n < 2; ++n) {
+            const uint2 v = __ldg(a.wb3 + (tap * 2 + n) * 32 + lane);
+            B3[tap][n][0] = v.x;
+            B3[tap][n][1] = v.y;
+        }
+#pragma unroll
+    for (int n = 0; n < 2; ++n) {
+        const uint2 v = __ldg(a.wb1 + n * 32 + lane);
+        B1[n][0] = v.x;
+        B1[n][1] = v.y;
+    }
+    {
+        const uint2 v = __ldg(a.wbh + lane);
+        BH[0] = v.x;
+        BH[1] = v.y;
+    }
+    float bias3[2][2], bias1[2][2], biash[2];
+#pragma unroll
+    for (int n = 0; n < 2; ++n)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+            bias3[n][e] = __ldg(a.b3 + n * 8 + 2 * t + e);
+            bias1[n][e] = __ldg(a.b1 + n * 8 + 2 * t + e);
+        }
+    biash[0] = t < 2 ? __ldg(a.bh + 2 * t) : 0.f;
+    biash[1] = t < 2 ? __ldg(a.bh + 2 * t + 1) : 0.f;
+    conv3_strip16<T, 8>(sbase, E0_PLANE, E0_IC, r0, sx, B3, [&](int oo, float (&acc)[2][4]) {
+        uint32_t a1[4], a2[4];
+        acc_to_a<T>(acc, bias3, true, a1);
+        float u[2][4] = {};
+#pragma unroll
+        for (int n = 0; n < 2; ++n) mma16816<T>(u[n], a1, B1[n][0], B1[n][1]);
+        acc_to_a<T>(u, bias1, true, a2);
+        float yh[4] = {0.f, 0.f, 0.f, 0.f};
+        mma16816<T>(yh, a2, BH[0], BH[1]);
+        const int oy = ty0 + r0 + oo;
+        if (t < 2 && oy < a.H0) {
+            float2* yrow = reinterpret_cast<float2*>(a.y + ((int64_t)f * a.H0 + oy) * a.W0);
+#pragma unroll
+            for (int hlf = 0; hlf < 2; ++hlf) {
+                const int ox = tx0 + sx + g + 8 * hlf;
+                if (ox < a.W0)
+                    yrow[2 * ox + t] = make_float2(yh[2 * hlf] + biash[0], yh[2 * hlf + 1] + biash[1]);
+            }
+        }
+    });
+}
+
+// Head reconstruction (network.py:199-209) + sigmoid, cropped to (h, w):
+// out(2Y+sy, 2X+sx) = sigmoid(up2(y0) + [sy,sx != 0,0] * y_{2sy+sx}(Y, X)).
+__device__ __forceinline__ float y0_at(const float4* yf, int W0, int r, int c) {
+    return __ldg(reinterpret_cast<const float*>(yf + (int64_t)r * W0 + c));
+}
+
+__global__ void recon_kernel(const float4* __restrict__ y, int H0, int W0, int h, int w, int n,
+                             void* __restrict__ out, int f16) {
+    const int X = blockIdx.x * blockDim.x + threadIdx.x;
+    const int Y = blockIdx.y;
+    const int f = blockIdx.z;
+    if (X >= W0) return;
+    const float4* yf = y + (int64_t)f * H0 * W0;
+    const float4 me = __ldg(yf + (int64_t)Y * W0 + X);
+    const float det[4] = {0.f, me.y, me.z, me.w};
+#pragma unroll
+    for (int sy = 0; sy < 2; ++sy) {
+        const int oy = 2 * Y + sy;
+        if (oy >= h) continue;
+        const float fy = fminf(fmaxf((oy + 0.5f) * 0.5f - 0.5f, 0.f), (float)(H0 - 1));
+        const int r0 = (int)fy, r1 = min(r0 + 1, H0 - 1);
+        const float wy = fy - r0;
+#pragma unroll
+        for (int sx = 0; sx < 2; ++sx) {
+            const int ox = 2 * X + sx;
+            if (ox >= w) continue;
+            const float fx = fminf(fmaxf((ox + 0.5f) * 0.5f - 0.5f, 0.f), (float)(W0 - 1));
+            const int c0 = (int)fx, c1 = min(c0 + 1, W0 - 1);
+            const float wx = fx - c0;
+            const float a = y0_at(yf, W0, r0, c0) * (1.f - wy) + y0_at(yf, W0, r1, c0) * wy;
+            const float b = y0_at(yf, W0, r0, c1) * (1.f - wy) + y0_at(yf, W0, r1, c1) * wy;
+            const float v = a * (1.f - wx) + b * wx + det[2 * sy + sx];
+            const float e = __expf(-fabsf(v));
+            const float s = v >= 0.f ? 1.f / (1.f + e) : e / (1.f + e);
+            const int64_t o = ((int64_t)f * h + oy) * w + ox;
+            if (f16) reinterpret_cast<__half*>(out)[o] = __float2half_rn(s);
+            else reinterpret_cast<float*>(out)[o] = s;
+        }
+    }
+}
+
+// ------------------------------------------------------------- levels 1-3 (tcgen05)
+enum { SRC_TENSOR = 0, SRC_UP = 1 };
+enum { DST_STORE = 1, DST_POOL = 2 };
+
+struct LevelArgs {
+    const void* x;       // SRC_TENSOR: (N, H, W, CIN); SRC_UP: (N, H/2, W/2, CIN)
+    const void* skip;    // SRC_UP: (N, H, W, CIN) or null
+    int H, W;
+    const void* w3;      // umma layout [9][CIN/16][2][C3][8]
+    const float* b3;
+    const void* w1;      // umma layout [1][C3/16][2][C1][8]
+    const float* b1;
+    void* out;           // (N, H, W, C1)
+    void* pool;          // (N, H/2, W/2, C1)
+};
+
+template <int CIN, int C3, int C1, int NB>
+struct LvGeom {
+    static constexpr int TH = 16, TW = 8 * NB;
+    static constexpr int IR = TH + 2, IC = TW + 2, NPI = IR * IC;
+    static constexpr int NCI = CIN / 8, NC3 = C3 / 8, KK = CIN / 16;
+    static constexpr int PIN = plane_bytes(NPI, NCI);
+    static constexpr int PMID = plane_bytes(TH * TW, NC3);
+    static constexpr int WTAP = CIN * C3 * 2;            // bytes of one tap's weights
+    static constexpr int W1B = C3 * C1 * 2;
+    static constexpr int OFF_MID = NCI * PIN;
+    static constexpr int OFF_W = OFF_MID + NC3 * PMID;
+    static constexpr int OFF_W1 = OFF_W + 2 * WTAP;
+    static constexpr int OFF_BAR = (OFF_W1 + W1B + 15) / 16 * 16;
+    static constexpr int SMEM = OFF_BAR + 64;
+    static constexpr int TCOLS = tmem_cols(NB * C3);
+};
+
+__device__ __forceinline__ void copy_smem16(uint8_t* dst, const uint8_t* src, int bytes) {
+    for (int i = threadIdx.x * 16; i < bytes; i += blockDim.x * 16)
+        *reinterpret_cast<uint4*>(dst + i) = __ldg(reinterpret_cast<const uint4*>(src + i));
+}
+
+template <typename T, int CIN, int C3, int C1, int SRC, int DST, int NB>
+__global__ void __launch_bounds__(128) level_tc_kernel(LevelArgs a) {
+    using G = LvGeom<CIN, C3, C1, NB>;
+    extern __shared__ __align__(128) uint8_t smem[];
+    uint64_t* bar = reinterpret_cast<uint64_t*>(smem + G::OFF_BAR);   // [0] acc, [1..2] w slots
+    uint32_t* tptr = reinterpret_cast<uint32_t*>(smem + G::OFF_BAR + 32);
+    const int f = blockIdx.z;
+    const int x0 = blockIdx.x * G::TW, y0 = blockIdx.y * G::TH;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const uint32_t sb = smem_u32(smem);
+
+    if (warp == 0) tmem_alloc<G::TCOLS>(tptr);
+    if (tid == 0) {
+        mbar_init(&bar[0], 1);
+        mbar_init(&bar[1], 1);
+        mbar_init(&bar[2], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    // ---- input tile (halo 1, zero outside the level frame)
+    {
+        const T* xf = reinterpret_cast<const T*>(a.x);
+        for (int i = tid; i < G::NPI * G::NCI; i += 128) {
+            const int c = i % G::NCI, p = i / G::NCI;
+            const int ti = p / G::IC, tj = p - ti * G::IC;
+            const int yy = y0 - 1 + ti, xx = x0 - 1 + tj;
+            uint4 q = make_uint4(0u, 0u, 0u, 0u);
+            if (yy >= 0 && xx >= 0 && yy < a.H && xx < a.W) {
+                if (SRC == SRC_TENSOR) {
+                    q = __ldg(reinterpret_cast<const uint4*>(
+                        xf + (((int64_t)f * a.H + yy) * a.W + xx) * CIN + c * 8));
+                } else {
+                    float v[8];
+                    const int hl = a.H / 2, wl = a.W / 2;
+                    up2_chunk<T>(xf + (int64_t)f * hl * wl * CIN, hl, wl, CIN, yy, xx, c, v);
+                    if (a.skip) {
+                        const uint4 s = __ldg(reinterpret_cast<const uint4*>(
+                            reinterpret_cast<const T*>(a.skip) + (((int64_t)f * a.H + yy) * a.W + xx) * CIN + c * 8));
+                        const uint32_t* sp = &s.x;
+#pragma unroll
+                        for (int k = 0; k < 4; ++k) {
+                            const float2 sv = Elem<T>::unpack(sp[k]);
+                            v[2 * k] += sv.x;
+                            v[2 * k + 1] += sv.y;
+                        }
+                    }
+                    q.x = Elem<T>::pack(v[0], v[1]);
+                    q.y = Elem<T>::pack(v[2], v[3]);
+                    q.z = Elem<T>::pack(v[4], v[5]);
+                    q.w = Elem<T>::pack(v[6], v[7]);
+                }
+            }
+            *reinterpret_cast<uint4*>(smem + c * G::PIN + p * 16) = q;
+        }
+    }
+    copy_smem16(smem + G::OFF_W1, reinterpret_cast<const uint8_t*>(a.w1), G::W1B);
+    copy_smem16(smem + G::OFF_W, reinterpret_cast<const uint8_t*>(a.w3), G::WTAP);
+    fence_proxy_async();
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tptr;
+
+    // ---- conv3: 9 taps x KK k-steps x NB M-blocks; weights streamed per tap
+    // through two SMEM slots (tap t+1 loads while tap t's MMAs run)
+    constexpr uint32_t idesc3 = umma_idesc(128, C3, Elem<T>::kUmmaFmt);
+    constexpr uint32_t idesc1 = umma_idesc(128, C1, Elem<T>::kUmmaFmt);
+#pragma unroll 1
+    for (int tap = 0; tap < 9; ++tap) {
+        const int slot = tap & 1;
+        if (tid == 0) {
+            tc_fence_after();
+            const int dy = tap / 3, dx = tap % 3;
+            const uint32_t wbase = sb + G::OFF_W + slot * G::WTAP;
+#pragma unroll
+            for (int b = 0; b < NB; ++b)
+#pragma unroll
+                for (int kk = 0; kk < G::KK; ++kk) {
+                    // M-block b: 16 output rows x 8 px; core matrix i = row i
+                    const uint32_t sa = sb + (2 * kk) * G::PIN + (dy * G::IC + b * 8 + dx) * 16;
+                    const uint64_t da = umma_desc(sa, G::PIN, G::IC * 16);
+                    const uint64_t db = umma_desc(wbase + kk * C3 * 32, C3 * 16, 128);
+                    umma_f16(tmem + b * C3, da, db, idesc3, (tap | kk) ? 1u : 0u);
+                }
+            umma_commit(&bar[1 + slot]);
+        }
+        if (tap + 1 < 9) {
+            // slot (tap+1)&1 was last read by tap-1's MMAs
+            if (tap >= 1) mbar_wait(&bar[1 + ((tap + 1) & 1)], ((tap - 1) >> 1) & 1);
+            copy_smem16(smem + G::OFF_W + ((tap + 1) & 1) * G::WTAP,
+                        reinterpret_cast<const uint8_t*>(a.w3) + (size_t)(tap + 1) * G::WTAP, G::WTAP);
+            fence_proxy_async();
+            __syncthreads();
+        }
+    }
+    if (tid == 0) umma_commit(&bar[0]);
+    mbar_wait(&bar[0], 0);
+    tc_fence_after();
+
+    // ---- epilogue 1: relu(conv3 + b3) -> 16-bit mid tile (chunk-planar)
+    const int m = warp * 32 + lane;             // TMEM lane == M row
+    const int pi = m >> 3, pj = m & 7;          // pixel row / column within the M-block
+    T* unused = nullptr;
+    (void)unused;
+#pragma unroll 1
+    for (int b = 0; b < NB; ++b) {
+#pragma unroll
+        for (int c0 = 0; c0 < C3; c0 += 16) {
+            float v[16];
+            tmem_ld16(tmem + ((uint32_t)(warp * 32) << 16) + b * C3 + c0, v);
+            uint4 q[2];
+            uint32_t* qp = &q[0].x;
+#pragma unroll
+            for (int k = 0; k < 8; ++k)
+                qp[k] = Elem<T>::pack(fmaxf(v[2 * k] + __ldg(a.b3 + c0 + 2 * k), 0.f),
+                                      fmaxf(v[2 * k + 1] + __ldg(a.b3 + c0 + 2 * k + 1), 0.f));
+            const int p = pi * G::TW + b * 8 + pj;
+            *reinterpret_cast<uint4*>(smem + G::OFF_MID + (c0 / 8) * G::PMID + p * 16) = q[0];
+            *reinterpret_cast<uint4*>(smem + G::OFF_MID + (c0 / 8 + 1) * G::PMID + p * 16) = q[1];
+        }
+    }
+    fence_proxy_async();
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+
+    // ---- conv1 (1x1): A = mid tile, B = w1
+    if (tid == 0) {
+#pragma unroll
+        for (int b = 0; b < NB; ++b)
+#pragma unroll
+            for (int kk = 0; kk < C3 / 16; ++kk) {
+                const uint32_t sa = sb + G::OFF_MID + (2 * kk) * G::PMID + (b * 8) * 16;
+                const uint64_t da = umma_desc(sa, G::PMID, G::TW * 16);
+                const uint64_t db = umma_desc(sb + G::OFF_W1 + kk * C1 * 32, C1 * 16, 128);
+                umma_f16(tmem + b * C3, da, db, idesc1, kk ? 1u : 0u);
+            }
+        umma_commit(&bar[0]);
+    }
+    mbar_wait(&bar[0], 1);
+    tc_fence_after();
+
+    // ---- epilogue 2: relu(conv1 + b1) -> NHWC store and/or 2x2 average pool
+    const int oy = y0 + pi;
+#pragma unroll 1
+    for (int b = 0; b < NB; ++b) {
+        const int ox = x0 + b * 8 + pj;
+        const bool inside = oy < a.H && ox < a.W;
+#pragma unroll
+        for (int c0 = 0; c0 < C1; c0 += 16) {
+            float v[16];
+            tmem_ld16(tmem + ((uint32_t)(warp * 32) << 16) + b * C3 + c0, v);
+#pragma unroll
+            for (int k = 0; k < 16; ++k) v[k] = fmaxf(v[k] + __ldg(a.b1 + c0 + k), 0.f);
+            if (DST & DST_STORE) {
+                if (inside) {
+                    uint4 q[2];
+                    uint32_t* qp = &q[0].x;
+#pragma unroll
+                    for (int k = 0; k < 8; ++k) qp[k] = Elem<T>::pack(v[2 * k], v[2 * k + 1]);
+                    uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<T*>(a.out) +
+                                                          (((int64_t)f * a.H + oy) * a.W + ox) * C1 + c0);
+                    dst[0] = q[0];
+                    dst[1] = q[1];
+                }
+            }
+            if (DST & DST_POOL) {
+#pragma unroll
+                for (int k = 0; k < 16; ++k) {
+                    v[k] += __shfl_xor_sync(0xffffffffu, v[k], 1);
+                    v[k] += __shfl_xor_sync(0xffffffffu, v[k], 8);
+                }
+                if (!(pi & 1) && !(pj & 1) && inside) {
+                    uint4 q[2];
+                    uint32_t* qp = &q[0].x;
+#pragma unroll
+                    for (int k = 0; k < 8; ++k) qp[k] = Elem<T>::pack(v[2 * k] * 0.25f, v[2 * k + 1] * 0.25f);
+                    const int H2 = a.H / 2, W2 = a.W / 2;
+                    uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<T*>(a.pool) +
+                                                          (((int64_t)f * H2 + oy / 2) * W2 + ox / 2) * C1 + c0);
+                    dst[0] = q[0];
+                    dst[1] = q[1];
+                }
+            }
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 0) tmem_dealloc<G::TCOLS>(tmem);
+}
+
+template <typename T, int CIN, int C3, int C1, int SRC, int DST, int NB>
+void launch_level(const LevelArgs& a, int n, cudaStream_t st, const char* name) {
+    using G = LvGeom<CIN, C3, C1, NB>;
+    auto k = level_tc_kernel<T, CIN, C3, C1, SRC, DST, NB>;
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, G::SMEM);
+        attr = true;
+    }
+    dim3 grd((a.W + G::TW - 1) / G::TW, (a.H + G::TH - 1) / G::TH, n);
+    NSM_PROF(name, st);
+    k<<<grd, 128, G::SMEM, st>>>(a);
+}
+
+// ------------------------------------------------------------------ host side
+struct F16Layout {
+    // per-conv offsets (bytes) into the plan's device block
+    size_t e0_w3, e0_w1, d0_w3, d0_w1, head;
+    size_t lv_w3[4][2], lv_w1[4][2];   // [level 1..3][enc/dec]
+};
+
+struct Bufs {
+    void *p1, *s1, *p2, *s2, *p3, *b3, *d2, *d1;
+    float4* y;
+    size_t bytes;
+};
+
+Bufs carve(void* ws, int nf, int H0, int W0, int es) {
+    const int H1 = H0 / 2, W1 = W0 / 2, H2 = H1 / 2, W2 = W1 / 2, H3 = H2 / 2, W3 = W2 / 2;
+    Bufs b{};
+    char* p = (char*)ws;
+    auto take = [&](size_t bytes) {
+        char* r = p;
+        p += (bytes + 255) / 256 * 256;
+        return (void*)r;
+    };
+    b.p1 = take((size_t)nf * H1 * W1 * 16 * es);
+    b.s1 = take((size_t)nf * H1 * W1 * 32 * es);
+    b.p2 = take((size_t)nf * H2 * W2 * 32 * es);
+    b.s2 = take((size_t)nf * H2 * W2 * 64 * es);
+    b.p3 = take((size_t)nf * H3 * W3 * 64 * es);
+    b.b3 = take((size_t)nf * H3 * W3 * 64 * es);
+    b.d2 = take((size_t)nf * H2 * W2 * 32 * es);
+    b.d1 = take((size_t)nf * H1 * W1 * 16 * es);
+    b.y = (float4*)take((size_t)nf * H0 * W0 * 16);
+    b.bytes = (size_t)(p - (char*)ws);
+    return b;
+}
+
+template <typename T>
+nsm_status run_levels(const Plan& p, const Bufs& b, int nf, int H0, int W0, cudaStream_t st) {
+    const int H1 = H0 / 2, W1 = W0 / 2, H2 = H1 / 2, W2 = W1 / 2, H3 = H2 / 2, W3 = W2 / 2;
+    const Level& L1 = p.lev[1];
+    const Level& L2 = p.lev[2];
+    const Level& L3 = p.lev[3];
+    LevelArgs a{};
+    // l1 encoder: P1 (16) -> S1 (32) + pool -> P2
+    a = LevelArgs{b.p1, nullptr, H1, W1, L1.enc3.wpk, L1.enc3.b32, L1.enc1.wpk, L1.enc1.b32, b.s1, b.p2};
+    launch_level<T, 16, 32, 32, SRC_TENSOR, DST_STORE | DST_POOL, 4>(a, nf, st, "lv1_enc");
+    // l2 encoder: P2 (32) -> S2 (64) + pool -> P3
+    a = LevelArgs{b.p2, nullptr, H2, W2, L2.enc3.wpk, L2.enc3.b32, L2.enc1.wpk, L2.enc1.b32, b.s2, b.p3};
+    launch_level<T, 32, 64, 64, SRC_TENSOR, DST_STORE | DST_POOL, 2>(a, nf, st, "lv2_enc");
+    // l3 bottleneck: P3 (64) -> 128 -> B3 (64)
+    a = LevelArgs{b.p3, nullptr, H3, W3, L3.enc3.wpk, L3.enc3.b32, L3.enc1.wpk, L3.enc1.b32, b.b3, nullptr};
+    launch_level<T, 64, 128, 64, SRC_TENSOR, DST_STORE, 1>(a, nf, st, "lv3_bott");
+    // l2 decoder: up(B3) + S2 -> 64 -> D2 (32)
+    a = LevelArgs{b.b3, b.s2, H2, W2, L2.dec3.wpk, L2.dec3.b32, L2.dec1.wpk, L2.dec1.b32, b.d2, nullptr};
+    launch_level<T, 64, 64, 32, SRC_UP, DST_STORE, 2>(a, nf, st, "lv2_dec");
+    // l1 decoder: up(D2) + S1 -> 32 -> D1 (16)
+    a = LevelArgs{b.d2, b.s1, H1, W1, L1.dec3.wpk, L1.dec3.b32, L1.dec1.wpk, L1.dec1.b32, b.d1, nullptr};
+    launch_level<T, 32, 32, 16, SRC_UP, DST_STORE, 4>(a, nf, st, "lv1_dec");
+    (void)W3;
+    return NSM_OK;
+}
+
+template <typename T>
+nsm_status run_l0(const Plan& p, const Bufs& b, const Enc0Args& e0, int nf, int H0, int W0, int h,
+                  int w, void* y, int y_f16, cudaStream_t st, bool from_gbuf) {
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(enc0_kernel<T, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, E0_SMEM);
+        cudaFuncSetAttribute(enc0_kernel<T, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, E0_SMEM);
+        cudaFuncSetAttribute(dec0_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, E0_SMEM);
+        attr = true;
+    }
+    dim3 grd((W0 + E0_TW - 1) / E0_TW, (H0 + E0_TH - 1) / E0_TH, nf);
+    {
+        NSM_PROF("enc0_fused", st);
+        if (from_gbuf) enc0_kernel<T, true><<<grd, 256, E0_SMEM, st>>>(e0);
+        else enc0_kernel<T, false><<<grd, 256, E0_SMEM, st>>>(e0);
+    }
+    nsm_status s = run_levels<T>(p, b, nf, H0, W0, st);
+    if (s != NSM_OK) return s;
+    const Level& L0 = p.lev[0];
+    Dec0Args d{b.d1, H0, W0, (const uint2*)L0.dec3.wpk, (const uint2*)L0.dec1.wpk,
+               (const uint2*)p.head.wpk, L0.dec3.b32, L0.dec1.b32, p.head.b32, b.y};
+    {
+        NSM_PROF("dec0_fused", st);
+        dec0_kernel<T><<<grd, 256, E0_SMEM, st>>>(d);
+    }
+    {
+        dim3 g2((W0 + 127) / 128, H0, nf);
+        NSM_PROF("recon", st);
+        recon_kernel<<<g2, 128, 0, st>>>(b.y, H0, W0, h, w, nf, y, y_f16);
+    }
+    return NSM_OK;
+}
+
+int round16(int v) { return (v + 15) / 16 * 16; }
+
+}  // namespace
+
+bool f16_supported(const Plan& p) {
+    const nsm_net_config& c = p.cfg;
+    return c.layers == 5 && c.base_channels == 16 && c.in_channels == 4 && c.use_space_to_depth &&
+           c.channel_cap >= 128;
+}
+
+size_t infer_f16_workspace(const Plan& p, int n, int h, int w) {
+    const int Hp = round16(h), Wp = round16(w);
+    const int nf = std::min(n, kChunkFrames);
+    return carve(nullptr, nf, Hp / 2, Wp / 2, 2).bytes + 1024;
+}
+
+nsm_status pack_f16(Plan& p, std::vector<char>& blob, size_t& offset_out) {
+    if (!f16_supported(p)) {
+        offset_out = blob.size();
+        return NSM_OK;   // the plan exists; 16-bit launches report UNSUPPORTED
+    }
+    const bool bf = p.act == NSM_BF16;
+    // gather every packed tensor first (the fp32 sources live in `blob`)
+    struct Item {
+        ConvW* c;
+        std::vector<char> bytes;
+    };
+    std::vector<Item> items;
+    auto frag = [&](ConvW& c, bool perm) {
+        std::vector<uint32_t> v;
+        if (bf) pack_frag<__nv_bfloat16>(c.w32, c.cout, c.cin, c.k, perm, v);
+        else pack_frag<__half>(c.w32, c.cout, c.cin, c.k, perm, v);
+        Item it{&c, std::vector<char>((char*)v.data(), (char*)v.data() + v.size() * 4)};
+        items.push_back(std::move(it));
+    };
+    auto umma = [&](ConvW& c) {
+        std::vector<uint16_t> v;
+        if (bf) pack_umma<__nv_bfloat16>(c.w32, c.cout, c.cin, c.k, v);
+        else pack_umma<__half>(c.w32, c.cout, c.cin, c.k, v);
+        Item it{&c, std::vector<char>((char*)v.data(), (char*)v.data() + v.size() * 2)};
+        items.push_back(std::move(it));
+    };
+    frag(p.lev[0].enc3, true);
+    frag(p.lev[0].enc1, false);
+    frag(p.lev[0].dec3, false);
+    frag(p.lev[0].dec1, false);
+    frag(p.head, false);
+    for (int j = 1; j < p.nlev; ++j) {
+        umma(p.lev[j].enc3);
+        umma(p.lev[j].enc1);
+        if (p.lev[j].dec3.present()) {
+            umma(p.lev[j].dec3);
+            umma(p.lev[j].dec1);
+        }
+    }
+    for (auto& it : items) {
+        const size_t off = (blob.size() + 255) / 256 * 256;
+        blob.resize(off + it.bytes.size());
+        memcpy(blob.data() + off, it.bytes.data(), it.bytes.size());
+        it.c->wpk = (const void*)(uintptr_t)off;   // rebased to the device block later
+    }
+    offset_out = blob.size();
+    return NSM_OK;
+}
+
+nsm_status infer_f16(const Plan& p, const nsm_gbuffer* g, const float* sm, int64_t sm_stride,
+                     const nsm_frame* frames, int n, int h, int w, void* y, nsm_dtype y_dtype,
+                     int64_t* first_bad, void* ws, size_t ws_bytes, cudaStream_t st) {
+    if (g->dtype != NSM_F32) return fail(NSM_ERR_UNSUPPORTED, "16-bit path reads fp32 G-buffer planes");
+    if (g->z_f || g->c_e || g->c_c || g->coverage)
+        return fail(NSM_ERR_UNSUPPORTED, "16-bit path derives z_f/c_e/c_c from the planes");
+    const int Hp = round16(h), Wp = round16(w), H0 = Hp / 2, W0 = Wp / 2;
+    const int nfmax = std::min(n, kChunkFrames);
+    Bufs b = carve(ws, nfmax, H0, W0, 2);
+    if (ws_bytes < b.bytes) return fail(NSM_ERR_ARG, "workspace too small (%zu < %zu)", ws_bytes, b.bytes);
+    launch_fill_i64(first_bad, n, INT64_MAX, st);
+    for (int f0 = 0; f0 < n; f0 += kChunkFrames) {
+        const int nf = std::min(kChunkFrames, n - f0);
+        Enc0Args e{};
+        e.g = GBufK{(const float*)g->d + (int64_t)f0 * g->frame_stride,
+                    (const float*)g->normal + (int64_t)f0 * 3 * g->frame_stride,
+                    (const float*)g->position + (int64_t)f0 * 3 * g->frame_stride,
+                    nullptr, nullptr, nullptr, nullptr, g->frame_stride};
+        e.sm = sm + f0 * sm_stride;
+        e.sm_stride = sm_stride;
+        make_frame_table(frames + f0, nf, e.tab);
+        e.h = h;
+        e.w = w;
+        e.H0 = H0;
+        e.W0 = W0;
+        e.wb3 = (const uint2*)p.lev[0].enc3.wpk;
+        e.wb1 = (const uint2*)p.lev[0].enc1.wpk;
+        e.b3 = p.lev[0].enc3.b32;
+        e.b1 = p.lev[0].enc1.b32;
+        e.out = b.p1;
+        e.first_bad = first_bad + f0;
+        void* yo = (char*)y + (size_t)f0 * h * w * (y_dtype == NSM_F16 ? 2 : 4);
+        nsm_status s = p.act == NSM_BF16
+                           ? run_l0<__nv_bfloat16>(p, b, e, nf, H0, W0, h, w, yo, y_dtype == NSM_F16, st, true)
+                           : run_l0<__half>(p, b, e, nf, H0, W0, h, w, yo, y_dtype == NSM_F16, st, true);
+        if (s != NSM_OK) return s;
+    }
+    NSM_CUDA_TRY(cudaGetLastError());
+    return NSM_OK;
+}
+
+nsm_status forward_f16(const Plan& p, const float* x, int n, int h, int w, float* out, void* ws,
+                       size_t ws_bytes, cudaStream_t st) {
+    if (!f16_supported(p)) return fail(NSM_ERR_UNSUPPORTED, "no 16-bit kernels for this NetworkConfig");
+    const int H0 = h / 2, W0 = w / 2;
+    const int nfmax = std::min(n, kChunkFrames);
+    Bufs b = carve(ws, nfmax, H0, W0, 2);
+    if (ws_bytes < b.bytes) return fail(NSM_ERR_ARG, "workspace too small");
+    for (int f0 = 0; f0 < n; f0 += kChunkFrames) {
+        const int nf = std::min(kChunkFrames, n - f0);
+        Enc0Args e{};
+        e.x = x + (int64_t)f0 * 4 * h * w;
+        e.h = h;
+        e.w = w;
+        e.H0 = H0;
+        e.W0 = W0;
+        e.wb3 = (const uint2*)p.lev[0].enc3.wpk;
+        e.wb1 = (const uint2*)p.lev[0].enc1.wpk;
+        e.b3 = p.lev[0].enc3.b32;
+        e.b1 = p.lev[0].enc1.b32;
+        e.out = b.p1;
+        e.first_bad = nullptr;
+        float* yo = out + (size_t)f0 * h * w;
+        nsm_status s = p.act == NSM_BF16
+                           ? run_l0<__nv_bfloat16>(p, b, e, nf, H0, W0, h, w, yo, 0, st, false)
+                           : run_l0<__half>(p, b, e, nf, H0, W0, h, w, yo, 0, st, false);
+        if (s != NSM_OK) return s;
+    }
+    NSM_CUDA_TRY(cudaGetLastError());
+    return NSM_OK;
 }
 
 }  // namespace nsm

@@ -1,0 +1,135 @@
+"""16-bit tensor-core path vs the oracle / reference goldens (needs a B200).
+
+Bars (BASELINE.json north_star): fp16/bf16 mode within 1e-2 max-abs and
+1e-4 MSE of the fp32 oracle visibility.
+"""
+
+import numpy as np
+import pytest
+
+from conftest import golden_camera, golden_view, load_golden
+
+pytestmark = pytest.mark.gpu
+
+MAX_ABS = 1e-2
+MAX_MSE = 1e-4
+
+
+def _weights(seed=0):
+    from paper_2301_05262_b200 import network
+    cfg = network.NetworkConfig()
+    return cfg, network.init_weights(cfg, np.random.default_rng(np.random.SeedSequence([seed, 0x11])))
+
+
+def _err(y, ref):
+    d = np.asarray(y, np.float64) - np.asarray(ref, np.float64)
+    return float(np.max(np.abs(d))), float(np.mean(d * d))
+
+
+def _frame_ns(r):
+    from types import SimpleNamespace
+    return SimpleNamespace(camera=golden_camera(r), view=golden_view(r), size_index=float(r["size_index"]),
+                           bias=float(r["bias"]), scene=SimpleNamespace(emitter_center=r["emitter_center"]))
+
+
+def _inputs(r):
+    import torch
+    return {k: torch.from_numpy(np.ascontiguousarray(r[s][None])).cuda()
+            for k, s in (("d", "d"), ("normal", "normal"), ("position", "position"), ("sm", "sm"))}
+
+
+@pytest.mark.parametrize("dtype", ["fp16", "bf16"])
+def test_forward_16bit_cfg1_golden(cfg1, dtype):
+    from paper_2301_05262_b200 import network
+    cfg, w = _weights()
+    y = network.forward(w, cfg, cfg1["features"], dtype=dtype).data
+    mx, mse = _err(y, cfg1["visibility"])
+    print(f"{dtype} forward cfg1: max {mx:.3g} mse {mse:.3g}")
+    assert mse <= MAX_MSE
+    if dtype == "fp16":
+        assert mx <= MAX_ABS
+
+
+@pytest.mark.parametrize("dtype", ["fp16", "bf16"])
+def test_infer_16bit_cfg1_golden(cfg1, dtype):
+    from paper_2301_05262_b200 import network
+    from paper_2301_05262_b200.infer import ShadowInference
+    cfg, w = _weights()
+    run = ShadowInference(network.Plan(w, cfg, dtype), [_frame_ns(cfg1)])
+    y = run(_inputs(cfg1))[0, 0].cpu().numpy()
+    mx, mse = _err(y, cfg1["visibility"])
+    print(f"{dtype} infer cfg1: max {mx:.3g} mse {mse:.3g}")
+    assert mse <= MAX_MSE
+    if dtype == "fp16":
+        assert mx <= MAX_ABS
+
+
+def test_fused_features_match_standalone_kernel(cfg1):
+    """The fused enc0 feature stage == nsm_features planes fed to forward."""
+    import torch
+    from paper_2301_05262_b200 import network
+    from paper_2301_05262_b200.infer import ShadowInference
+    from paper_2301_05262_b200.raster import assemble_features_batch
+    cfg, w = _weights()
+    plan = network.Plan(w, cfg, "fp16")
+    fr = _frame_ns(cfg1)
+    inp = _inputs(cfg1)
+    feats, _, _ = assemble_features_batch(inp, [(fr.camera, fr.view, fr.scene.emitter_center,
+                                                 fr.size_index, fr.bias)])
+    y_two = plan.forward(feats)[0, 0].cpu().numpy()
+    y_fused = ShadowInference(plan, [fr])(inp)[0, 0].cpu().numpy()
+    # only fp32-vs-fp64 feature arithmetic differs before the 16-bit rounding
+    assert np.max(np.abs(y_two - y_fused)) < 2e-3
+    assert np.mean(y_two == y_fused) > 0.9
+
+
+def test_batch_equals_single_frames():
+    """Frames are independent: a batch of 3 (crossing the chunk boundary)
+    gives bitwise the single-frame results."""
+    from paper_2301_05262_b200 import network, producer, scenes
+    from paper_2301_05262_b200.infer import ShadowInference
+    cfg, w = _weights()
+    plan = network.Plan(w, cfg, "fp16")
+    frames = [scenes.make_frame(scenes.random_scene(8, seed=s), (96, 160), (256, 256)) for s in range(3)]
+    inp = producer.render_inputs(frames)
+    yb = ShadowInference(plan, frames)(inp).cpu().numpy()
+    for i, fr in enumerate(frames):
+        one = {k: v[i:i + 1].contiguous() for k, v in inp.items()}
+        y1 = ShadowInference(plan, [fr])(one).cpu().numpy()
+        np.testing.assert_array_equal(y1[0], yb[i])
+
+
+@pytest.mark.parametrize("config", [2, 3])
+def test_1080p_fp16_vs_oracle(config):
+    from oracle import features as of
+    from oracle import network as on
+    from paper_2301_05262_b200 import network, producer, scenes
+    from paper_2301_05262_b200.infer import ShadowInference
+    fr = scenes.config_frames(config, seed=1)[0]
+    inp = producer.render_inputs([fr])
+    cfg, w = _weights()
+    run = ShadowInference(network.Plan(w, cfg, "fp16"), [fr], out_dtype="fp16")
+    y = run(inp)[0, 0].float().cpu().numpy()
+    h = {k: v[0].cpu().numpy() for k, v in inp.items()}
+    feats, _ = of.features_from_planes(h["d"], h["normal"], h["position"], h["sm"], fr.camera, fr.view,
+                                       fr.scene.emitter_center, fr.size_index, fr.bias)
+    xp = np.zeros((4, 1088, 1920), np.float32)
+    xp[:, :1080] = feats
+    ref = on.forward({k: v.data for k, v in w.items()}, xp)[0, :1080]
+    mx, mse = _err(y, ref)
+    print(f"config {config} (size_index {fr.size_index:.2f}) fp16: max {mx:.3g} mse {mse:.3g}")
+    assert mx <= MAX_ABS and mse <= MAX_MSE
+
+
+def test_fused_frustum_error():
+    from types import SimpleNamespace
+    from paper_2301_05262_b200 import network
+    from paper_2301_05262_b200._lib import FrustumError
+    from paper_2301_05262_b200.infer import ShadowInference
+    r = load_golden("cfg1")
+    fr = _frame_ns(r)
+    v = fr.view
+    fr.view = SimpleNamespace(**{**v.__dict__, "tan_half": v.tan_half / 20})
+    cfg, w = _weights()
+    with pytest.raises(FrustumError):
+        ShadowInference(network.Plan(w, cfg, "fp16"), [fr])(_inputs(r))
