@@ -54,6 +54,7 @@ def parse():
     ap.add_argument("--no-graph", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-soak", action="store_true", help="skip the 1 s clock-sampling soak")
     return ap.parse_args()
 
 
@@ -224,7 +225,7 @@ def run_ours(args):
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clk:
         # keep the GPU loaded ~1 s so nvidia-smi samples clocks under load
-        t_end = time.time() + 1.0
+        t_end = time.time() + (0.0 if args.no_soak else 1.0)
         while time.time() < t_end:
             for _ in range(20):
                 step()

@@ -79,8 +79,9 @@ def test_fused_features_match_standalone_kernel(cfg1):
     y_two = plan.forward(feats)[0, 0].cpu().numpy()
     y_fused = ShadowInference(plan, [fr])(inp)[0, 0].cpu().numpy()
     # only fp32-vs-fp64 feature arithmetic differs before the 16-bit rounding
-    assert np.max(np.abs(y_two - y_fused)) < 2e-3
-    assert np.mean(y_two == y_fused) > 0.9
+    d = np.abs(y_two - y_fused)
+    print(f"fused vs two-stage: max {d.max():.3g} mean {d.mean():.3g}")
+    assert d.max() < 2e-3 and d.mean() < 1e-4
 
 
 def test_batch_equals_single_frames():
