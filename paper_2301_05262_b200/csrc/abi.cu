@@ -58,6 +58,22 @@ void make_frame_table(const nsm_frame* frames, int32_t n, FrameTable& tab) {
         f.cw = s.camera.width;
         f.size_index = s.size_index;
         f.bias = s.bias;
+        f.pa = s.view.width / (2.0 * s.view.tan_half);
+        f.pb = s.view.width / 2.0 - 0.5;
+        f.qa = s.view.height / (2.0 * s.view.tan_half);
+        f.qb = s.view.height / 2.0 - 0.5;
+        for (int a = 0; a < 3; ++a) {
+            f.fec[a] = (float)f.ec[a];
+            f.fcf[a] = (float)f.cf[a];
+            f.fcr[a] = (float)f.cr[a];
+            f.fcu[a] = (float)f.cu[a];
+        }
+        f.fu1 = (float)(2.0 * f.half_w / f.cw);
+        f.fu0 = (float)(f.half_w / f.cw - f.half_w);
+        f.fw1 = (float)(-2.0 * f.half_h / f.ch);
+        f.fw0 = (float)(f.half_h - f.half_h / f.ch);
+        f.fbias = (float)f.bias;
+        f.fsize = (float)f.size_index;
     }
 }
 

@@ -20,6 +20,11 @@ struct FrameK {
     double size_index, bias;
     int hs, ws;                          // shadow-map resolution
     int ch, cw;                          // camera resolution (rays)
+    // fused-path constants, precomputed on the host (abi.cu make_frame_table)
+    double pa, pb, qa, qb;               // col = xr/zc * pa + pb ; row = qb - yr/zc * qa
+    float fec[3], fcf[3], fcr[3], fcu[3];
+    float fu1, fu0, fw1, fw0;            // u = fx * fu1 + fu0 ; w = fy * fw1 + fw0
+    float fbias, fsize;
 };
 
 struct FrameTable {
@@ -74,6 +79,27 @@ __device__ __forceinline__ bool texel_of(const FrameK& f, double px, double py, 
     long long r = __double2ll_rn(row);
     long long c = __double2ll_rn(col);
     bool ok = (zc > 0.0) && r >= 0 && r < f.hs && c >= 0 && c < f.ws;
+    ri = (int)min(max(r, 0LL), (long long)f.hs - 1);
+    ci = (int)min(max(c, 0LL), (long long)f.ws - 1);
+    return ok;
+}
+
+// Same texel as texel_of with the affine map folded (one fp64 division):
+// col = (xr / zc) * ws / (2 tan) + ws / 2 - 0.5.  Differs from the
+// reference's rounding sequence by a few fp64 ulps, i.e. only for values
+// within ~1e-12 texel of a half-integer tie.
+__device__ __forceinline__ bool texel_fast(const FrameK& f, double px, double py, double pz, int& ri,
+                                           int& ci) {
+    const double rx = px - f.vp[0], ry = py - f.vp[1], rz = pz - f.vp[2];
+    const double zc = rx * f.vf[0] + ry * f.vf[1] + rz * f.vf[2];
+    const double xr = rx * f.vr[0] + ry * f.vr[1] + rz * f.vr[2];
+    const double yr = rx * f.vu[0] + ry * f.vu[1] + rz * f.vu[2];
+    const double inv = 1.0 / zc;
+    const double col = fma(xr * inv, f.pa, f.pb);
+    const double row = fma(-yr * inv, f.qa, f.qb);
+    const long long r = __double2ll_rn(row);
+    const long long c = __double2ll_rn(col);
+    const bool ok = (zc > 0.0) && r >= 0 && r < f.hs && c >= 0 && c < f.ws;
     ri = (int)min(max(r, 0LL), (long long)f.hs - 1);
     ci = (int)min(max(c, 0LL), (long long)f.ws - 1);
     return ok;

@@ -22,6 +22,8 @@
 #include "prof.cuh"
 #include "tc.cuh"
 
+#include <cudaTypedefs.h>
+
 namespace nsm {
 
 namespace {
@@ -32,6 +34,25 @@ constexpr int E0_TH = 16, E0_TW = 64;  // level-0 output tile (enc0 / dec0)
 constexpr int E0_IR = E0_TH + 2, E0_IC = E0_TW + 2;
 constexpr int E0_PLANE = plane_bytes(E0_IR * E0_IC, 2);
 constexpr int E0_SMEM = 2 * E0_PLANE;
+// TMA staging of the G-buffer for half a level-0 tile: 18 full-res rows x
+// 132 columns x 7 fp32 planes (d, normal xyz, position xyz), double-buffered
+// The TMA inner-dimension start must be 16-B aligned (measured: an fp32 box
+// starting at x = -2 raises "illegal instruction", x = -4 works), so each
+// staged row holds 136 columns starting 2 columns left of the halo.
+constexpr int ST_ROWS = E0_IR, ST_COLS = 2 * E0_IC, ST_PIX = ST_ROWS * ST_COLS;
+constexpr int ST_TCOLS = ST_COLS + 4, ST_TPIX = ST_ROWS * ST_TCOLS;
+constexpr int ST_PLANE = ST_TPIX * 4;
+constexpr int ST_TX = 7 * ST_PLANE;                       // bytes landed per half-tile
+constexpr int round128(int v) { return (v + 127) / 128 * 128; }
+constexpr int ST_OFF_N = round128(ST_PLANE);              // TMA destinations 128-B aligned
+constexpr int ST_OFF_P = ST_OFF_N + round128(3 * ST_PLANE);
+constexpr int ST_BYTES = round128(ST_OFF_P + 3 * ST_PLANE);
+constexpr int ENC0_SMEM_TMA = 2 * E0_SMEM + 2 * ST_BYTES + 64;
+static_assert(E0_SMEM % 128 == 0, "stage base alignment");
+
+struct GbufMaps {
+    CUtensorMap d, n, p;   // (W, H, N) and (W, H, 3, N) fp32 tensor maps
+};
 
 // packed-weight formats (offsets into the plan's device block)
 //  "frag": mma.sync B fragments, [tap][kk][nt][lane][2] u32
@@ -204,100 +225,353 @@ __device__ __forceinline__ void acc_to_a(const float (&acc)[2][4], const float (
     a[3] = Elem<T>::pack(v[1][2], v[1][3]);
 }
 
-template <typename T, bool kFromGBuffer>
-__global__ void __launch_bounds__(256, 2) enc0_kernel(Enc0Args a) {
-    extern __shared__ __align__(128) uint8_t smem[];
-    const int f = blockIdx.z;
-    const int tx0 = blockIdx.x * E0_TW, ty0 = blockIdx.y * E0_TH;
-    const uint32_t sbase = smem_u32(smem);
-    const int H1 = a.H0 / 2, W1 = a.W0 / 2;
+__device__ __forceinline__ void nbar_sync(int id, int n) {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+__device__ __forceinline__ void nbar_arrive(int id, int n) {
+    asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
 
-    // ---- stage 1: features of the halo'd tile, s2d-packed into SMEM
-    {
-        const int64_t hw = (int64_t)a.h * a.w;
-        const int64_t base = (int64_t)f * a.g.frame_stride;
-        constexpr int RC = 2 * E0_IC;
-        for (int i = threadIdx.x; i < 2 * E0_IR * RC; i += blockDim.x) {
+// Persistent, warp-specialised level-0 kernels: warps 0-7 produce the
+// halo'd input tile of the next tile into one of two SMEM buffers while
+// warps 8-15 run the tensor-core convolutions on the other.  Named barriers
+// 1/2 = buffer full, 3/4 = buffer empty.
+constexpr int kL0Threads = 512, kL0Prod = 256;
+
+template <class Produce>
+__device__ __forceinline__ void l0_produce_loop(int total, Produce&& produce) {   // all 512 threads meet at 1-4
+    extern __shared__ __align__(128) uint8_t smem[];
+    for (int k = 0;; ++k) {
+        const int tile = blockIdx.x + k * gridDim.x;
+        if (tile >= total) break;
+        const int s = k & 1;
+        if (k >= 2) nbar_sync(3 + s, kL0Threads);
+        produce(smem + s * E0_SMEM, tile);
+        nbar_arrive(1 + s, kL0Threads);
+    }
+}
+
+template <class Consume>
+__device__ __forceinline__ void l0_consume_loop(int total, Consume&& consume) {
+    extern __shared__ __align__(128) uint8_t smem[];
+    for (int k = 0;; ++k) {
+        const int tile = blockIdx.x + k * gridDim.x;
+        if (tile >= total) break;
+        const int s = k & 1;
+        nbar_sync(1 + s, kL0Threads);
+        consume(smem + s * E0_SMEM, tile);
+        if (tile + 2 * (int)gridDim.x < total) nbar_arrive(3 + s, kL0Threads);
+    }
+}
+
+struct L0Tile {
+    int f, ty0, tx0;
+};
+
+__device__ __forceinline__ L0Tile l0_tile(int tile, int H0, int W0) {
+    const int nx = (W0 + E0_TW - 1) / E0_TW, ny = (H0 + E0_TH - 1) / E0_TH;
+    L0Tile t;
+    t.tx0 = (tile % nx) * E0_TW;
+    t.ty0 = ((tile / nx) % ny) * E0_TH;
+    t.f = tile / (nx * ny);
+    return t;
+}
+
+// Features of a halo'd level-0 tile, s2d-packed: 4 full-resolution pixels
+// per thread per batch, all G-buffer loads issued before any use.
+template <typename T, bool kFromGBuffer>
+__device__ __forceinline__ void produce_features(const Enc0Args& a, uint8_t* buf, const L0Tile& tl) {
+    constexpr int RC = 2 * E0_IC, NPX = 2 * E0_IR * RC, K = 4;
+    const int ptid = threadIdx.x;
+    const int64_t hw = (int64_t)a.h * a.w;
+    const int64_t base = (int64_t)tl.f * a.g.frame_stride;
+    const float* gd = reinterpret_cast<const float*>(a.g.d) + base;
+    const float* gp = reinterpret_cast<const float*>(a.g.position) + 3 * base;
+    const float* gn = reinterpret_cast<const float*>(a.g.normal) + 3 * base;
+    for (int i0 = ptid; i0 < NPX; i0 += kL0Prod * K) {
+        float d[K], px[K], py[K], pz[K], nx[K], ny[K], nz[K];
+        int fy[K], fx[K];
+        bool in[K];
+#pragma unroll
+        for (int j = 0; j < K; ++j) {
+            const int i = i0 + j * kL0Prod;
             const int ry = i / RC, rx = i - ry * RC;
-            const int fy = 2 * (ty0 - 1) + ry, fx = 2 * (tx0 - 1) + rx;
-            float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-            if (fy >= 0 && fx >= 0 && fy < a.h && fx < a.w) {
+            fy[j] = 2 * (tl.ty0 - 1) + ry;
+            fx[j] = 2 * (tl.tx0 - 1) + rx;
+            in[j] = i < NPX && fy[j] >= 0 && fx[j] >= 0 && fy[j] < a.h && fx[j] < a.w;
+            d[j] = px[j] = py[j] = pz[j] = nx[j] = ny[j] = nz[j] = 0.f;
+            if (in[j]) {
+                const int64_t pix = (int64_t)fy[j] * a.w + fx[j];
                 if (kFromGBuffer) {
-                    v = pixel_features(a.tab.f[f], a.g, a.sm + f * a.sm_stride, base,
-                                       (int64_t)fy * a.w + fx, fy, fx, hw, a.first_bad + f);
+                    d[j] = __ldg(gd + pix);
+                    px[j] = __ldg(gp + pix);
+                    py[j] = __ldg(gp + hw + pix);
+                    pz[j] = __ldg(gp + 2 * hw + pix);
+                    nx[j] = __ldg(gn + pix);
+                    ny[j] = __ldg(gn + hw + pix);
+                    nz[j] = __ldg(gn + 2 * hw + pix);
                 } else {
-                    const float* xp = a.x + (int64_t)f * 4 * hw + (int64_t)fy * a.w + fx;
-                    v = make_float4(__ldg(xp), __ldg(xp + hw), __ldg(xp + 2 * hw), __ldg(xp + 3 * hw));
+                    const float* xp = a.x + (int64_t)tl.f * 4 * hw + pix;
+                    px[j] = __ldg(xp);
+                    py[j] = __ldg(xp + hw);
+                    pz[j] = __ldg(xp + 2 * hw);
+                    nx[j] = __ldg(xp + 3 * hw);
                 }
             }
-            const int p = (ry >> 1) * E0_IC + (rx >> 1);
-            uint2 pk = make_uint2(Elem<T>::pack(v.x, v.y), Elem<T>::pack(v.z, v.w));
-            *reinterpret_cast<uint2*>(smem + (ry & 1) * E0_PLANE + p * 16 + (rx & 1) * 8) = pk;
+        }
+        float4 v[K];
+        if (kFromGBuffer) {
+            const FrameK& F = a.tab.f[tl.f];
+            const float* smf = a.sm + tl.f * a.sm_stride;
+            float look[K];
+#pragma unroll
+            for (int j = 0; j < K; ++j) {
+                look[j] = 0.f;
+                if (d[j] > 0.f) {
+                    int ri, ci;
+                    if (!texel_of(F, px[j], py[j], pz[j], ri, ci))
+                        atomic_min_i64(a.first_bad + tl.f, (int64_t)fy[j] * a.w + fx[j]);
+                    look[j] = __ldg(smf + (int64_t)ri * F.ws + ci);
+                }
+            }
+#pragma unroll
+            for (int j = 0; j < K; ++j) {
+                v[j] = make_float4(0.f, 0.f, 0.f, 0.f);
+                if (d[j] > 0.f) {
+                    const float tx = (float)(F.ec[0] - (double)px[j]), ty = (float)(F.ec[1] - (double)py[j]),
+                                tz = (float)(F.ec[2] - (double)pz[j]);
+                    const float izf = rsqrtf(tx * tx + ty * ty + tz * tz);
+                    const float zf = 1.f / izf;
+                    const float ce = fminf(fmaxf((nx[j] * tx + ny[j] * ty + nz[j] * tz) * izf, 0.f), 1.f);
+                    const float u = ((fx[j] + 0.5f) / F.cw * 2.f - 1.f) * (float)F.half_w;
+                    const float w = (1.f - (fy[j] + 0.5f) / F.ch * 2.f) * (float)F.half_h;
+                    const float rx = (float)F.cf[0] + u * (float)F.cr[0] + w * (float)F.cu[0];
+                    const float ry = (float)F.cf[1] + u * (float)F.cr[1] + w * (float)F.cu[1];
+                    const float rz = (float)F.cf[2] + u * (float)F.cr[2] + w * (float)F.cu[2];
+                    const float cc = fminf(fmaxf(-(nx[j] * rx + ny[j] * ry + nz[j] * rz) *
+                                                     rsqrtf(rx * rx + ry * ry + rz * rz), 0.f), 1.f);
+                    float ch0 = 0.f, ch1 = 1.f;
+                    if (isfinite(look[j])) {                    // raster.py:262
+                        const float m = fminf(look[j], zf);
+                        ch0 = (m - zf) + (float)F.bias;
+                        ch1 = (m + (float)F.bias) * izf;
+                    }
+                    v[j] = make_float4(ch0, ch1, ce + (float)F.size_index, cc / d[j]);
+                }
+            }
+        } else {
+#pragma unroll
+            for (int j = 0; j < K; ++j) v[j] = make_float4(px[j], py[j], pz[j], nx[j]);
+        }
+#pragma unroll
+        for (int j = 0; j < K; ++j) {
+            const int i = i0 + j * kL0Prod;
+            if (i < NPX) {
+                const int ry = i / RC, rx = i - ry * RC;
+                const int p = (ry >> 1) * E0_IC + (rx >> 1);
+                *reinterpret_cast<uint2*>(buf + (ry & 1) * E0_PLANE + p * 16 + (rx & 1) * 8) =
+                    make_uint2(Elem<T>::pack(v[j].x, v[j].y), Elem<T>::pack(v[j].z, v[j].w));
+            }
         }
     }
-    __syncthreads();
+}
 
-    // ---- stage 2: l0.enc3 (sliding window) -> l0.enc1 -> avg_pool2
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int g = lane >> 2, t = lane & 3;
-    const int sx = (warp & 3) * 16, r0 = (warp >> 2) * 8;
-    uint32_t B3[9][2][2], B1[2][2];
+// TMA producer: one elected thread streams half-tiles of the seven G-buffer
+// planes into two SMEM stages (mbarrier complete_tx); the producer warps turn
+// each staged half into features while the next half is in flight.
+constexpr int kE0Prod = 384;   // 12 producer warps, 4 tensor-core warps
+
+template <typename T>
+__device__ __forceinline__ void produce_features_tma(const Enc0Args& a, const GbufMaps& tm, int total) {
+    extern __shared__ __align__(128) uint8_t smem[];
+    uint8_t* stage = smem + 2 * E0_SMEM;
+    uint64_t* full = reinterpret_cast<uint64_t*>(stage + 2 * ST_BYTES);
+    const int ptid = threadIdx.x;
+    const int mytiles = (int)blockIdx.x < total ? (total - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x : 0;
+    auto issue = [&](int q) {
+        const L0Tile tl = l0_tile(blockIdx.x + (q >> 1) * gridDim.x, a.H0, a.W0);
+        const int sidx = q & 1;
+        const uint32_t dst = smem_u32(stage + sidx * ST_BYTES);
+        const int x = 2 * tl.tx0 - 4, y = 2 * tl.ty0 - 2 + ST_ROWS * (q & 1);
+        mbar_expect_tx(&full[sidx], ST_TX);
+        tma_load_3d(dst, &tm.d, x, y, tl.f, &full[sidx]);
+        tma_load_4d(dst + ST_OFF_N, &tm.n, x, y, 0, tl.f, &full[sidx]);
+        tma_load_4d(dst + ST_OFF_P, &tm.p, x, y, 0, tl.f, &full[sidx]);
+    };
+    if (ptid == 0) {
+        mbar_init(&full[0], 1);
+        mbar_init(&full[1], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    nbar_sync(5, kE0Prod);
+    if (ptid == 0 && mytiles > 0) {
+        issue(0);
+        issue(1);
+    }
+    for (int k = 0; k < mytiles; ++k) {
+        const L0Tile tl = l0_tile(blockIdx.x + k * gridDim.x, a.H0, a.W0);
+        const int sb = k & 1;
+        if (k >= 2) nbar_sync(3 + sb, kL0Threads);
+        uint8_t* buf = smem + sb * E0_SMEM;
+        const FrameK& F = a.tab.f[tl.f];
+        const float* smf = a.sm + tl.f * a.sm_stride;
+        const float ecx = F.fec[0], ecy = F.fec[1], ecz = F.fec[2];
+        const float bias = F.fbias, sidx_off = F.fsize;
+        for (int hh = 0; hh < 2; ++hh) {
+            const int q = 2 * k + hh, sidx = q & 1;
+            const int fy0 = 2 * tl.ty0 - 2 + ST_ROWS * hh, fx0 = 2 * tl.tx0 - 2;
+            mbar_wait(&full[sidx], (q >> 1) & 1);
+            const float* sd = reinterpret_cast<const float*>(stage + sidx * ST_BYTES);
+            const float* sn = reinterpret_cast<const float*>(stage + sidx * ST_BYTES + ST_OFF_N);
+            const float* sp = reinterpret_cast<const float*>(stage + sidx * ST_BYTES + ST_OFF_P);
+            constexpr int K = 4;
+#pragma unroll 1
+            for (int i0 = ptid; i0 < ST_PIX; i0 += kE0Prod * K) {
+                float d[K], look[K];
+                int si[K];
 #pragma unroll
-    for (int tap = 0; tap < 9; ++tap)
+                for (int j = 0; j < K; ++j) {
+                    const int i = i0 + j * kE0Prod;
+                    si[j] = i + 4 * (i / ST_COLS) + 2;      // staged index (136-wide rows)
+                    d[j] = i < ST_PIX ? sd[si[j]] : 0.f;
+                    look[j] = 0.f;
+                    if (d[j] > 0.f) {
+                        int ri, ci;
+                        if (!texel_fast(F, sp[si[j]], sp[ST_TPIX + si[j]], sp[2 * ST_TPIX + si[j]], ri, ci)) {
+                            const int ry = i / ST_COLS;
+                            atomic_min_i64(a.first_bad + tl.f,
+                                           (int64_t)(fy0 + ry) * a.w + (fx0 + i - ry * ST_COLS));
+                        }
+                        look[j] = __ldg(smf + (int64_t)ri * F.ws + ci);
+                    }
+                }
+#pragma unroll
+                for (int j = 0; j < K; ++j) {
+                    const int i = i0 + j * kE0Prod;
+                    if (i >= ST_PIX) continue;
+                    const int ry = i / ST_COLS, rx = i - ry * ST_COLS;
+                    float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+                    if (d[j] > 0.f) {
+                        const int o = si[j];
+                        const float px = sp[o], py = sp[ST_TPIX + o], pz = sp[2 * ST_TPIX + o];
+                        const float nx = sn[o], ny = sn[ST_TPIX + o], nz = sn[2 * ST_TPIX + o];
+                        const float tx = ecx - px, ty = ecy - py, tz = ecz - pz;
+                        const float izf = rsqrtf(tx * tx + ty * ty + tz * tz);
+                        const float ce = fminf(fmaxf((nx * tx + ny * ty + nz * tz) * izf, 0.f), 1.f);
+                        const float u = (float)(fx0 + rx) * F.fu1 + F.fu0;
+                        const float w = (float)(fy0 + ry) * F.fw1 + F.fw0;
+                        const float dx = F.fcf[0] + u * F.fcr[0] + w * F.fcu[0];
+                        const float dy = F.fcf[1] + u * F.fcr[1] + w * F.fcu[1];
+                        const float dz = F.fcf[2] + u * F.fcr[2] + w * F.fcu[2];
+                        const float cc = fminf(fmaxf(-(nx * dx + ny * dy + nz * dz) *
+                                                         rsqrtf(dx * dx + dy * dy + dz * dz), 0.f), 1.f);
+                        float ch0 = 0.f, ch1 = 1.f;
+                        if (look[j] < INFINITY) {                  // raster.py:262 (finite lookup)
+                            const float zf = 1.f / izf;
+                            const float m = fminf(look[j], zf);
+                            ch0 = (m - zf) + bias;
+                            ch1 = (m + bias) * izf;
+                        }
+                        v = make_float4(ch0, ch1, ce + sidx_off, __fdividef(cc, d[j]));
+                    }
+                    const int trow = ST_ROWS * hh + ry;            // full-res row within the tile
+                    const int p = (trow >> 1) * E0_IC + (rx >> 1);
+                    *reinterpret_cast<uint2*>(buf + (trow & 1) * E0_PLANE + p * 16 + (rx & 1) * 8) =
+                        make_uint2(Elem<T>::pack(v.x, v.y), Elem<T>::pack(v.z, v.w));
+                }
+            }
+            nbar_sync(5, kE0Prod);                 // everyone is done with stage sidx
+            if (ptid == 0 && q + 2 < 2 * mytiles) {
+                fence_proxy_async();
+                issue(q + 2);
+            }
+        }
+        nbar_arrive(1 + sb, kL0Threads);
+    }
+}
+
+template <typename T, int kSrc>   // kSrc: 0 = features planes, 1 = G-buffer (LDG), 2 = G-buffer (TMA)
+__global__ void __launch_bounds__(kL0Threads, 1) enc0_kernel(const __grid_constant__ Enc0Args a,
+                                                             const __grid_constant__ GbufMaps tm, int total) {
+    constexpr int kProd = kSrc == 2 ? kE0Prod : kL0Prod;
+    constexpr int kRows = kSrc == 2 ? 16 : 8;        // output rows per consumer warp
+    if (threadIdx.x < kProd) {
+        if (kSrc == 2) {
+            produce_features_tma<T>(a, tm, total);
+        } else {
+            l0_produce_loop(total, [&](uint8_t* buf, int tile) {
+                produce_features<T, kSrc == 1>(a, buf, l0_tile(tile, a.H0, a.W0));
+            });
+        }
+        return;
+    }
+    const int H1 = a.H0 / 2, W1 = a.W0 / 2;
+    const int cw = (threadIdx.x - kProd) >> 5;       // consumer warp
+    const int lane = threadIdx.x & 31;
+    const int g = lane >> 2, t = lane & 3;
+    const int sx = (cw & 3) * 16, r0 = (cw >> 2) * kRows;
+    uint32_t B3[9][2][2], B1[2][2];
+    float bias3[2][2], bias1[2][2];
+    {
+#pragma unroll
+        for (int tap = 0; tap < 9; ++tap)
+#pragma unroll
+            for (int n = 0; n < 2; ++n) {
+                const uint2 v = __ldg(a.wb3 + (tap * 2 + n) * 32 + lane);
+                B3[tap][n][0] = v.x;
+                B3[tap][n][1] = v.y;
+            }
 #pragma unroll
         for (int n = 0; n < 2; ++n) {
-            const uint2 v = __ldg(a.wb3 + (tap * 2 + n) * 32 + lane);
-            B3[tap][n][0] = v.x;
-            B3[tap][n][1] = v.y;
+            const uint2 v = __ldg(a.wb1 + n * 32 + lane);
+            B1[n][0] = v.x;
+            B1[n][1] = v.y;
         }
-#pragma unroll
-    for (int n = 0; n < 2; ++n) {
-        const uint2 v = __ldg(a.wb1 + n * 32 + lane);
-        B1[n][0] = v.x;
-        B1[n][1] = v.y;
-    }
-    float bias3[2][2], bias1[2][2];
-#pragma unroll
-    for (int n = 0; n < 2; ++n)
-#pragma unroll
-        for (int e = 0; e < 2; ++e) {
-            bias3[n][e] = __ldg(a.b3 + n * 8 + 2 * t + e);
-            bias1[n][e] = __ldg(a.b1 + n * 8 + 2 * t + e);
-        }
-    float pp[2][4];
-    T* out = reinterpret_cast<T*>(a.out);
-    conv3_strip16<T, 8>(sbase, E0_PLANE, E0_IC, r0, sx, B3, [&](int oo, float (&acc)[2][4]) {
-        uint32_t a1[4];
-        acc_to_a<T>(acc, bias3, true, a1);
-        float u[2][4] = {};
-#pragma unroll
-        for (int n = 0; n < 2; ++n) mma16816<T>(u[n], a1, B1[n][0], B1[n][1]);
 #pragma unroll
         for (int n = 0; n < 2; ++n)
 #pragma unroll
-            for (int e = 0; e < 4; ++e) {
-                float v = fmaxf(u[n][e] + bias1[n][e & 1], 0.f);
-                v += __shfl_xor_sync(0xffffffffu, v, 4);       // x-neighbour pixel
-                if (oo & 1) pp[n][e] += v;
-                else pp[n][e] = v;
+            for (int e = 0; e < 2; ++e) {
+                bias3[n][e] = __ldg(a.b3 + n * 8 + 2 * t + e);
+                bias1[n][e] = __ldg(a.b1 + n * 8 + 2 * t + e);
             }
-        if (oo & 1) {
-            const int py = (ty0 + r0 + oo) >> 1;
-            const int pxb = (tx0 + sx) >> 1;
-            if (!(g & 1) && py < H1) {
-                T* orow = out + ((int64_t)f * H1 + py) * W1 * 16;
+    }
+    T* out = reinterpret_cast<T*>(a.out);
+    l0_consume_loop(total, [&](uint8_t* buf, int tile) {
+            const L0Tile tl = l0_tile(tile, a.H0, a.W0);
+            float pp[2][4];
+            conv3_strip16<T, kRows>(smem_u32(buf), E0_PLANE, E0_IC, r0, sx, B3, [&](int oo, float (&acc)[2][4]) {
+                uint32_t a1[4];
+                acc_to_a<T>(acc, bias3, true, a1);
+                float u[2][4] = {};
 #pragma unroll
-                for (int hlf = 0; hlf < 2; ++hlf) {
-                    const int px = pxb + (g >> 1) + 4 * hlf;
-                    if (px < W1) {
+                for (int n = 0; n < 2; ++n) mma16816<T>(u[n], a1, B1[n][0], B1[n][1]);
 #pragma unroll
-                        for (int n = 0; n < 2; ++n)
-                            *reinterpret_cast<uint32_t*>(orow + px * 16 + n * 8 + 2 * t) =
-                                Elem<T>::pack(pp[n][2 * hlf] * 0.25f, pp[n][2 * hlf + 1] * 0.25f);
+                for (int n = 0; n < 2; ++n)
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) {
+                        float v = fmaxf(u[n][e] + bias1[n][e & 1], 0.f);
+                        v += __shfl_xor_sync(0xffffffffu, v, 4);       // x-neighbour pixel
+                        if (oo & 1) pp[n][e] += v;
+                        else pp[n][e] = v;
+                    }
+                if (oo & 1) {                                           // avg_pool2 of rows oo-1, oo
+                    const int py = (tl.ty0 + r0 + oo) >> 1;
+                    const int pxb = (tl.tx0 + sx) >> 1;
+                    if (!(g & 1) && py < H1) {
+                        T* orow = out + ((int64_t)tl.f * H1 + py) * W1 * 16;
+#pragma unroll
+                        for (int hlf = 0; hlf < 2; ++hlf) {
+                            const int px = pxb + (g >> 1) + 4 * hlf;
+                            if (px < W1) {
+#pragma unroll
+                                for (int n = 0; n < 2; ++n)
+                                    *reinterpret_cast<uint32_t*>(orow + px * 16 + n * 8 + 2 * t) =
+                                        Elem<T>::pack(pp[n][2 * hlf] * 0.25f, pp[n][2 * hlf + 1] * 0.25f);
+                            }
+                        }
                     }
                 }
-            }
-        }
+            });
     });
 }
 
@@ -343,81 +617,86 @@ __device__ __forceinline__ void up2_chunk(const T* x, int hl, int wl, int C, int
 }
 
 template <typename T>
-__global__ void __launch_bounds__(256, 2) dec0_kernel(Dec0Args a) {
-    extern __shared__ __align__(128) uint8_t smem[];
-    const int f = blockIdx.z;
-    const int tx0 = blockIdx.x * E0_TW, ty0 = blockIdx.y * E0_TH;
-    const uint32_t sbase = smem_u32(smem);
+__global__ void __launch_bounds__(kL0Threads, 1) dec0_kernel(Dec0Args a, int total) {
     const int H1 = a.H0 / 2, W1 = a.W0 / 2;
-    const T* xf = reinterpret_cast<const T*>(a.x) + (int64_t)f * H1 * W1 * 16;
-    // ---- up2(D1) over the halo'd tile (zero outside the frame: conv padding)
-    for (int i = threadIdx.x; i < E0_IR * E0_IC * 2; i += blockDim.x) {
-        const int c = i & 1, p = i >> 1;
-        const int ti = p / E0_IC, tj = p - ti * E0_IC;
-        const int oy = ty0 - 1 + ti, ox = tx0 - 1 + tj;
-        float v[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-        if (oy >= 0 && ox >= 0 && oy < a.H0 && ox < a.W0) up2_chunk<T>(xf, H1, W1, 16, oy, ox, c, v);
-        uint4 q;
-        q.x = Elem<T>::pack(v[0], v[1]);
-        q.y = Elem<T>::pack(v[2], v[3]);
-        q.z = Elem<T>::pack(v[4], v[5]);
-        q.w = Elem<T>::pack(v[6], v[7]);
-        *reinterpret_cast<uint4*>(smem + c * E0_PLANE + p * 16) = q;
+    if (threadIdx.x < kL0Prod) {
+        l0_produce_loop(total, [&](uint8_t* buf, int tile) {
+            // up2(D1) over the halo'd tile (zero outside the frame: conv padding)
+            const L0Tile tl = l0_tile(tile, a.H0, a.W0);
+            const T* xf = reinterpret_cast<const T*>(a.x) + (int64_t)tl.f * H1 * W1 * 16;
+            for (int i = threadIdx.x; i < E0_IR * E0_IC * 2; i += kL0Prod) {
+                const int c = i & 1, p = i >> 1;
+                const int ti = p / E0_IC, tj = p - ti * E0_IC;
+                const int oy = tl.ty0 - 1 + ti, ox = tl.tx0 - 1 + tj;
+                float v[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+                if (oy >= 0 && ox >= 0 && oy < a.H0 && ox < a.W0) up2_chunk<T>(xf, H1, W1, 16, oy, ox, c, v);
+                uint4 q;
+                q.x = Elem<T>::pack(v[0], v[1]);
+                q.y = Elem<T>::pack(v[2], v[3]);
+                q.z = Elem<T>::pack(v[4], v[5]);
+                q.w = Elem<T>::pack(v[6], v[7]);
+                *reinterpret_cast<uint4*>(buf + c * E0_PLANE + p * 16) = q;
+            }
+        });
+        return;
     }
-    __syncthreads();
-
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int cw = (threadIdx.x - kL0Prod) >> 5;
+    const int lane = threadIdx.x & 31;
     const int g = lane >> 2, t = lane & 3;
-    const int sx = (warp & 3) * 16, r0 = (warp >> 2) * 8;
+    const int sx = (cw & 3) * 16, r0 = (cw >> 2) * 8;
     uint32_t B3[9][2][2], B1[2][2], BH[2];
+    float bias3[2][2], bias1[2][2], biash[2];
+    {
 #pragma unroll
-    for (int tap = 0; tap < 9; ++tap)
+        for (int tap = 0; tap < 9; ++tap)
+#pragma unroll
+            for (int n = 0; n < 2; ++n) {
+                const uint2 v = __ldg(a.wb3 + (tap * 2 + n) * 32 + lane);
+                B3[tap][n][0] = v.x;
+                B3[tap][n][1] = v.y;
+            }
 #pragma unroll
         for (int n = 0; n < 2; ++n) {
-            const uint2 v = __ldg(a.wb3 + (tap * 2 + n) * 32 + lane);
-            B3[tap][n][0] = v.x;
-            B3[tap][n][1] = v.y;
+            const uint2 v = __ldg(a.wb1 + n * 32 + lane);
+            B1[n][0] = v.x;
+            B1[n][1] = v.y;
         }
-#pragma unroll
-    for (int n = 0; n < 2; ++n) {
-        const uint2 v = __ldg(a.wb1 + n * 32 + lane);
-        B1[n][0] = v.x;
-        B1[n][1] = v.y;
-    }
-    {
         const uint2 v = __ldg(a.wbh + lane);
         BH[0] = v.x;
         BH[1] = v.y;
-    }
-    float bias3[2][2], bias1[2][2], biash[2];
 #pragma unroll
-    for (int n = 0; n < 2; ++n)
+        for (int n = 0; n < 2; ++n)
 #pragma unroll
-        for (int e = 0; e < 2; ++e) {
-            bias3[n][e] = __ldg(a.b3 + n * 8 + 2 * t + e);
-            bias1[n][e] = __ldg(a.b1 + n * 8 + 2 * t + e);
-        }
-    biash[0] = t < 2 ? __ldg(a.bh + 2 * t) : 0.f;
-    biash[1] = t < 2 ? __ldg(a.bh + 2 * t + 1) : 0.f;
-    conv3_strip16<T, 8>(sbase, E0_PLANE, E0_IC, r0, sx, B3, [&](int oo, float (&acc)[2][4]) {
-        uint32_t a1[4], a2[4];
-        acc_to_a<T>(acc, bias3, true, a1);
-        float u[2][4] = {};
-#pragma unroll
-        for (int n = 0; n < 2; ++n) mma16816<T>(u[n], a1, B1[n][0], B1[n][1]);
-        acc_to_a<T>(u, bias1, true, a2);
-        float yh[4] = {0.f, 0.f, 0.f, 0.f};
-        mma16816<T>(yh, a2, BH[0], BH[1]);
-        const int oy = ty0 + r0 + oo;
-        if (t < 2 && oy < a.H0) {
-            float2* yrow = reinterpret_cast<float2*>(a.y + ((int64_t)f * a.H0 + oy) * a.W0);
-#pragma unroll
-            for (int hlf = 0; hlf < 2; ++hlf) {
-                const int ox = tx0 + sx + g + 8 * hlf;
-                if (ox < a.W0)
-                    yrow[2 * ox + t] = make_float2(yh[2 * hlf] + biash[0], yh[2 * hlf + 1] + biash[1]);
+            for (int e = 0; e < 2; ++e) {
+                bias3[n][e] = __ldg(a.b3 + n * 8 + 2 * t + e);
+                bias1[n][e] = __ldg(a.b1 + n * 8 + 2 * t + e);
             }
-        }
+        biash[0] = t < 2 ? __ldg(a.bh + 2 * t) : 0.f;
+        biash[1] = t < 2 ? __ldg(a.bh + 2 * t + 1) : 0.f;
+    }
+    l0_consume_loop(total,
+        [&](uint8_t* buf, int tile) {
+            const L0Tile tl = l0_tile(tile, a.H0, a.W0);
+            conv3_strip16<T, 8>(smem_u32(buf), E0_PLANE, E0_IC, r0, sx, B3, [&](int oo, float (&acc)[2][4]) {
+                uint32_t a1[4], a2[4];
+                acc_to_a<T>(acc, bias3, true, a1);
+                float u[2][4] = {};
+#pragma unroll
+                for (int n = 0; n < 2; ++n) mma16816<T>(u[n], a1, B1[n][0], B1[n][1]);
+                acc_to_a<T>(u, bias1, true, a2);
+                float yh[4] = {0.f, 0.f, 0.f, 0.f};
+                mma16816<T>(yh, a2, BH[0], BH[1]);
+                const int oy = tl.ty0 + r0 + oo;
+                if (t < 2 && oy < a.H0) {
+                    float2* yrow = reinterpret_cast<float2*>(a.y + ((int64_t)tl.f * a.H0 + oy) * a.W0);
+#pragma unroll
+                    for (int hlf = 0; hlf < 2; ++hlf) {
+                        const int ox = tl.tx0 + sx + g + 8 * hlf;
+                        if (ox < a.W0)
+                            yrow[2 * ox + t] = make_float2(yh[2 * hlf] + biash[0], yh[2 * hlf + 1] + biash[1]);
+                    }
+                }
+            });
     });
 }
 
@@ -705,6 +984,16 @@ void launch_level(const LevelArgs& a, int n, cudaStream_t st, const char* name) 
 }
 
 // ------------------------------------------------------------------ host side
+int num_sms() {
+    static int n = 0;
+    if (!n) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    }
+    return n;
+}
+
 struct F16Layout {
     // per-conv offsets (bytes) into the plan's device block
     size_t e0_w3, e0_w1, d0_w3, d0_w1, head;
@@ -765,21 +1054,66 @@ nsm_status run_levels(const Plan& p, const Bufs& b, int nf, int H0, int W0, cuda
     return NSM_OK;
 }
 
+// cuTensorMapEncodeTiled through the runtime's driver entry point (the
+// library links cudart statically and never links libcuda directly).
+PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    if (!fn) {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = (PFN_cuTensorMapEncodeTiled_v12000)p;
+    }
+    return fn;
+}
+
+// Tensor maps over the planar fp32 G-buffer of frames [0, nf) of a chunk;
+// false when TMA's 16-byte stride / address rules do not hold.
+bool encode_gbuf_maps(const GBufK& g, int nf, int h, int w, GbufMaps* m) {
+    auto enc = tensor_map_encoder();
+    const int64_t fs = g.frame_stride;
+    if (!enc || (w * 4) % 16 || (fs * 4) % 16 || ((uintptr_t)g.d | (uintptr_t)g.normal | (uintptr_t)g.position) % 16)
+        return false;
+    const cuuint32_t box3[3] = {(cuuint32_t)ST_TCOLS, (cuuint32_t)ST_ROWS, 1};
+    const cuuint32_t box4[4] = {(cuuint32_t)ST_TCOLS, (cuuint32_t)ST_ROWS, 3, 1};
+    const cuuint32_t es[4] = {1, 1, 1, 1};
+    const cuuint64_t dim3_[3] = {(cuuint64_t)w, (cuuint64_t)h, (cuuint64_t)nf};
+    const cuuint64_t str3[2] = {(cuuint64_t)w * 4, (cuuint64_t)fs * 4};
+    const cuuint64_t dim4[4] = {(cuuint64_t)w, (cuuint64_t)h, 3, (cuuint64_t)nf};
+    const cuuint64_t str4[3] = {(cuuint64_t)w * 4, (cuuint64_t)h * w * 4, (cuuint64_t)fs * 12};
+    CUresult r = enc(&m->d, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<void*>(g.d), dim3_, str3, box3, es,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                     CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return false;
+    r = enc(&m->n, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, const_cast<void*>(g.normal), dim4, str4, box4, es,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return false;
+    r = enc(&m->p, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, const_cast<void*>(g.position), dim4, str4, box4, es,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS;
+}
+
 template <typename T>
-nsm_status run_l0(const Plan& p, const Bufs& b, const Enc0Args& e0, int nf, int H0, int W0, int h,
-                  int w, void* y, int y_f16, cudaStream_t st, bool from_gbuf) {
+nsm_status run_l0(const Plan& p, const Bufs& b, const Enc0Args& e0, const GbufMaps& tm, int nf, int H0,
+                  int W0, int h, int w, void* y, int y_f16, cudaStream_t st, int src) {
     static bool attr = false;
     if (!attr) {
-        cudaFuncSetAttribute(enc0_kernel<T, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, E0_SMEM);
-        cudaFuncSetAttribute(enc0_kernel<T, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, E0_SMEM);
-        cudaFuncSetAttribute(dec0_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, E0_SMEM);
+        cudaFuncSetAttribute(enc0_kernel<T, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * E0_SMEM);
+        cudaFuncSetAttribute(enc0_kernel<T, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * E0_SMEM);
+        cudaFuncSetAttribute(enc0_kernel<T, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, ENC0_SMEM_TMA);
+        cudaFuncSetAttribute(dec0_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * E0_SMEM);
         attr = true;
     }
-    dim3 grd((W0 + E0_TW - 1) / E0_TW, (H0 + E0_TH - 1) / E0_TH, nf);
+    const int total = ((W0 + E0_TW - 1) / E0_TW) * ((H0 + E0_TH - 1) / E0_TH) * nf;
+    const int pgrid = std::min(total, num_sms());
     {
         NSM_PROF("enc0_fused", st);
-        if (from_gbuf) enc0_kernel<T, true><<<grd, 256, E0_SMEM, st>>>(e0);
-        else enc0_kernel<T, false><<<grd, 256, E0_SMEM, st>>>(e0);
+        if (src == 2) enc0_kernel<T, 2><<<pgrid, kL0Threads, ENC0_SMEM_TMA, st>>>(e0, tm, total);
+        else if (src == 1) enc0_kernel<T, 1><<<pgrid, kL0Threads, 2 * E0_SMEM, st>>>(e0, tm, total);
+        else enc0_kernel<T, 0><<<pgrid, kL0Threads, 2 * E0_SMEM, st>>>(e0, tm, total);
     }
     nsm_status s = run_levels<T>(p, b, nf, H0, W0, st);
     if (s != NSM_OK) return s;
@@ -788,7 +1122,7 @@ nsm_status run_l0(const Plan& p, const Bufs& b, const Enc0Args& e0, int nf, int 
                (const uint2*)p.head.wpk, L0.dec3.b32, L0.dec1.b32, p.head.b32, b.y};
     {
         NSM_PROF("dec0_fused", st);
-        dec0_kernel<T><<<grd, 256, E0_SMEM, st>>>(d);
+        dec0_kernel<T><<<pgrid, kL0Threads, 2 * E0_SMEM, st>>>(d, total);
     }
     {
         dim3 g2((W0 + 127) / 128, H0, nf);
@@ -895,9 +1229,12 @@ nsm_status infer_f16(const Plan& p, const nsm_gbuffer* g, const float* sm, int64
         e.out = b.p1;
         e.first_bad = first_bad + f0;
         void* yo = (char*)y + (size_t)f0 * h * w * (y_dtype == NSM_F16 ? 2 : 4);
+        GbufMaps tm;
+        memset(&tm, 0, sizeof tm);
+        const int src = encode_gbuf_maps(e.g, nf, h, w, &tm) ? 2 : 1;
         nsm_status s = p.act == NSM_BF16
-                           ? run_l0<__nv_bfloat16>(p, b, e, nf, H0, W0, h, w, yo, y_dtype == NSM_F16, st, true)
-                           : run_l0<__half>(p, b, e, nf, H0, W0, h, w, yo, y_dtype == NSM_F16, st, true);
+                           ? run_l0<__nv_bfloat16>(p, b, e, tm, nf, H0, W0, h, w, yo, y_dtype == NSM_F16, st, src)
+                           : run_l0<__half>(p, b, e, tm, nf, H0, W0, h, w, yo, y_dtype == NSM_F16, st, src);
         if (s != NSM_OK) return s;
     }
     NSM_CUDA_TRY(cudaGetLastError());
@@ -926,9 +1263,11 @@ nsm_status forward_f16(const Plan& p, const float* x, int n, int h, int w, float
         e.out = b.p1;
         e.first_bad = nullptr;
         float* yo = out + (size_t)f0 * h * w;
+        GbufMaps tm;
+        memset(&tm, 0, sizeof tm);
         nsm_status s = p.act == NSM_BF16
-                           ? run_l0<__nv_bfloat16>(p, b, e, nf, H0, W0, h, w, yo, 0, st, false)
-                           : run_l0<__half>(p, b, e, nf, H0, W0, h, w, yo, 0, st, false);
+                           ? run_l0<__nv_bfloat16>(p, b, e, tm, nf, H0, W0, h, w, yo, 0, st, 0)
+                           : run_l0<__half>(p, b, e, tm, nf, H0, W0, h, w, yo, 0, st, 0);
         if (s != NSM_OK) return s;
     }
     NSM_CUDA_TRY(cudaGetLastError());
