@@ -14,6 +14,7 @@
 // for ldmatrix rows and for UMMA descriptors alike.  Bias, ReLU, pooling,
 // upsampling, skip sums, the head and the sigmoid run in fp32 registers.
 #include <algorithm>
+#include <type_traits>
 #include <cmath>
 #include <vector>
 
@@ -757,21 +758,25 @@ struct LevelArgs {
     void* pool;          // (N, H/2, W/2, C1)
 };
 
-template <int CIN, int C3, int C1, int NB>
+template <int CIN, int C3, int C1, int NB, int NIN, int NMID>
 struct LvGeom {
     static constexpr int TH = 16, TW = 8 * NB;
     static constexpr int IR = TH + 2, IC = TW + 2, NPI = IR * IC;
     static constexpr int NCI = CIN / 8, NC3 = C3 / 8, KK = CIN / 16;
-    static constexpr int PIN = plane_bytes(NPI, NCI);
+    static constexpr int PIN = NPI * 16;                       // dense: the TMA box layout
+    static constexpr int INB = round128(NCI * PIN);
     static constexpr int PMID = plane_bytes(TH * TW, NC3);
-    static constexpr int WTAP = CIN * C3 * 2;            // bytes of one tap's weights
-    static constexpr int W1B = C3 * C1 * 2;
-    static constexpr int OFF_MID = NCI * PIN;
-    static constexpr int OFF_W = OFF_MID + NC3 * PMID;
-    static constexpr int OFF_W1 = OFF_W + 2 * WTAP;
-    static constexpr int OFF_BAR = (OFF_W1 + W1B + 15) / 16 * 16;
-    static constexpr int SMEM = OFF_BAR + 64;
-    static constexpr int TCOLS = tmem_cols(NB * C3);
+    static constexpr int MIDB = round128(NC3 * PMID);
+    static constexpr int W3B = 9 * CIN * C3 * 2, W1B = C3 * C1 * 2;
+    static constexpr int OFF_MID = NIN * INB;
+    static constexpr int OFF_W3 = OFF_MID + NMID * MIDB;
+    static constexpr int OFF_W1 = OFF_W3 + W3B;
+    static constexpr int OFF_B = OFF_W1 + W1B;
+    static constexpr int OFF_BAR = (OFF_B + (C3 + C1) * 4 + 15) / 16 * 16;
+    static constexpr int SMEM = OFF_BAR + 160;
+    static constexpr int ACC3 = 0, ACC1 = 2 * NB * C3;         // TMEM columns (both double-buffered)
+    static constexpr int TCOLS = tmem_cols(2 * NB * (C3 + C1));
+    static constexpr int TX_BYTES = NCI * PIN;
 };
 
 __device__ __forceinline__ void copy_smem16(uint8_t* dst, const uint8_t* src, int bytes) {
@@ -779,208 +784,282 @@ __device__ __forceinline__ void copy_smem16(uint8_t* dst, const uint8_t* src, in
         *reinterpret_cast<uint4*>(dst + i) = __ldg(reinterpret_cast<const uint4*>(src + i));
 }
 
-template <typename T, int CIN, int C3, int C1, int SRC, int DST, int NB>
-__global__ void __launch_bounds__(128) level_tc_kernel(LevelArgs a) {
-    using G = LvGeom<CIN, C3, C1, NB>;
-    extern __shared__ __align__(128) uint8_t smem[];
-    uint64_t* bar = reinterpret_cast<uint64_t*>(smem + G::OFF_BAR);   // [0] acc, [1..2] w slots
-    uint32_t* tptr = reinterpret_cast<uint32_t*>(smem + G::OFF_BAR + 32);
-    const int f = blockIdx.z;
-    const int x0 = blockIdx.x * G::TW, y0 = blockIdx.y * G::TH;
-    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    const uint32_t sb = smem_u32(smem);
+__device__ __forceinline__ void tma_load_5d(uint32_t dst, const CUtensorMap* map, int c0, int c1, int c2,
+                                            int c3, int c4, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.5d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], "
+        "[%1, {%2, %3, %4, %5, %6}], [%7];" ::"r"(dst),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4), "r"(smem_u32(bar))
+        : "memory");
+}
 
-    if (warp == 0) tmem_alloc<G::TCOLS>(tptr);
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+// Persistent, warp-specialised level kernel (levels 1-3):
+//   producer warps  - TMA (SRC_TENSOR: a 5-D box turns NHWC into the
+//                     chunk-planar tile, zero-filled halo) or up2(low)+skip
+//                     in fp32 (SRC_UP) into NIN input buffers
+//   MMA warp        - one thread issues conv3x3 as 9 taps x CIN/16 UMMAs per
+//                     128-pixel M-block (A = shifted views of the input tile,
+//                     B = resident weights) into one of two TMEM accumulators,
+//                     then conv1x1 on the 16-bit mid tile into two more
+//   epilogue warps  - TMEM -> bias+ReLU -> mid tile; TMEM -> bias+ReLU ->
+//                     NHWC store and/or 2x2 average pool
+// All hand-offs are mbarriers (tcgen05.commit on the tensor-core side), so
+// conv3 of tile k+1 overlaps the epilogues of tile k.
+template <typename T, int CIN, int C3, int C1, int SRC, int DST, int NB, int NIN, int NMID, int NPW>
+__global__ void __launch_bounds__((NPW + 5) * 32, 1) level_kernel(const __grid_constant__ LevelArgs a,
+                                                                   const __grid_constant__ CUtensorMap tin,
+                                                                   int total) {
+    using G = LvGeom<CIN, C3, C1, NB, NIN, NMID>;
+    extern __shared__ __align__(128) uint8_t smem[];
+    uint64_t* bar = reinterpret_cast<uint64_t*>(smem + G::OFF_BAR);
+    uint64_t* in_full = bar + 0;      // [2]
+    uint64_t* in_empty = bar + 2;     // [2]
+    uint64_t* a3_full = bar + 4;
+    uint64_t* a3_empty = bar + 6;
+    uint64_t* mid_full = bar + 8;
+    uint64_t* mid_empty = bar + 10;
+    uint64_t* a1_full = bar + 12;
+    uint64_t* a1_empty = bar + 14;
+    uint32_t* tptr = reinterpret_cast<uint32_t*>(smem + G::OFF_BAR + 128);
+    float* sb3 = reinterpret_cast<float*>(smem + G::OFF_B);
+    float* sb1 = sb3 + C3;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    constexpr int EW0 = NPW, MW = NPW + 4;          // first epilogue warp, MMA warp
+    constexpr int NPT = NPW * 32;
+    const uint32_t sbase = smem_u32(smem);
+    const int ntx = (a.W + G::TW - 1) / G::TW, nty = (a.H + G::TH - 1) / G::TH;
+    const int mytiles = (int)blockIdx.x < total ? (total - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x : 0;
+    auto tile_of = [&](int k, int& f, int& y0, int& x0) {
+        const int t = blockIdx.x + k * gridDim.x;
+        x0 = (t % ntx) * G::TW;
+        y0 = ((t / ntx) % nty) * G::TH;
+        f = t / (ntx * nty);
+    };
+
+    if (warp == EW0) tmem_alloc<G::TCOLS>(tptr);
     if (tid == 0) {
-        mbar_init(&bar[0], 1);
-        mbar_init(&bar[1], 1);
-        mbar_init(&bar[2], 1);
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(&in_full[i], SRC == SRC_TENSOR ? 1 : NPT);
+            mbar_init(&in_empty[i], 1);
+            mbar_init(&a3_full[i], 1);
+            mbar_init(&a3_empty[i], 128);
+            mbar_init(&mid_full[i], 128);
+            mbar_init(&mid_empty[i], 1);
+            mbar_init(&a1_full[i], 1);
+            mbar_init(&a1_empty[i], 128);
+        }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
-    // ---- input tile (halo 1, zero outside the level frame)
-    {
-        const T* xf = reinterpret_cast<const T*>(a.x);
-        for (int i = tid; i < G::NPI * G::NCI; i += 128) {
-            const int c = i % G::NCI, p = i / G::NCI;
-            const int ti = p / G::IC, tj = p - ti * G::IC;
-            const int yy = y0 - 1 + ti, xx = x0 - 1 + tj;
-            uint4 q = make_uint4(0u, 0u, 0u, 0u);
-            if (yy >= 0 && xx >= 0 && yy < a.H && xx < a.W) {
-                if (SRC == SRC_TENSOR) {
-                    q = __ldg(reinterpret_cast<const uint4*>(
-                        xf + (((int64_t)f * a.H + yy) * a.W + xx) * CIN + c * 8));
-                } else {
-                    float v[8];
-                    const int hl = a.H / 2, wl = a.W / 2;
-                    up2_chunk<T>(xf + (int64_t)f * hl * wl * CIN, hl, wl, CIN, yy, xx, c, v);
-                    if (a.skip) {
-                        const uint4 s = __ldg(reinterpret_cast<const uint4*>(
-                            reinterpret_cast<const T*>(a.skip) + (((int64_t)f * a.H + yy) * a.W + xx) * CIN + c * 8));
-                        const uint32_t* sp = &s.x;
-#pragma unroll
-                        for (int k = 0; k < 4; ++k) {
-                            const float2 sv = Elem<T>::unpack(sp[k]);
-                            v[2 * k] += sv.x;
-                            v[2 * k + 1] += sv.y;
-                        }
-                    }
-                    q.x = Elem<T>::pack(v[0], v[1]);
-                    q.y = Elem<T>::pack(v[2], v[3]);
-                    q.z = Elem<T>::pack(v[4], v[5]);
-                    q.w = Elem<T>::pack(v[6], v[7]);
-                }
-            }
-            *reinterpret_cast<uint4*>(smem + c * G::PIN + p * 16) = q;
-        }
-    }
+    copy_smem16(smem + G::OFF_W3, reinterpret_cast<const uint8_t*>(a.w3), G::W3B);
     copy_smem16(smem + G::OFF_W1, reinterpret_cast<const uint8_t*>(a.w1), G::W1B);
-    copy_smem16(smem + G::OFF_W, reinterpret_cast<const uint8_t*>(a.w3), G::WTAP);
+    for (int i = tid; i < C3; i += blockDim.x) sb3[i] = a.b3[i];
+    for (int i = tid; i < C1; i += blockDim.x) sb1[i] = a.b1[i];
     fence_proxy_async();
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = *tptr;
 
-    // ---- conv3: 9 taps x KK k-steps x NB M-blocks; weights streamed per tap
-    // through two SMEM slots (tap t+1 loads while tap t's MMAs run)
-    constexpr uint32_t idesc3 = umma_idesc(128, C3, Elem<T>::kUmmaFmt);
-    constexpr uint32_t idesc1 = umma_idesc(128, C1, Elem<T>::kUmmaFmt);
+    if (warp < NPW) {
+        // ------------------------------------------------------------ producer
+        if (SRC == SRC_TENSOR) {
+            if (tid == 0) {
+                for (int k = 0; k < mytiles; ++k) {
+                    const int s = k % NIN;
+                    mbar_wait(&in_empty[s], ((k / NIN) & 1) ^ 1);
+                    int f, y0, x0;
+                    tile_of(k, f, y0, x0);
+                    mbar_expect_tx(&in_full[s], G::TX_BYTES);
+                    tma_load_5d(sbase + s * G::INB, &tin, 0, x0 - 1, y0 - 1, 0, f, &in_full[s]);
+                }
+            }
+        } else {
+            const T* xf = reinterpret_cast<const T*>(a.x);
+            const int hl = a.H / 2, wl = a.W / 2;
+            for (int k = 0; k < mytiles; ++k) {
+                const int s = k % NIN;
+                mbar_wait(&in_empty[s], ((k / NIN) & 1) ^ 1);
+                int f, y0, x0;
+                tile_of(k, f, y0, x0);
+                uint8_t* in = smem + s * G::INB;
+                const T* xlf = xf + (int64_t)f * hl * wl * CIN;
+                for (int i = tid; i < G::NPI * G::NCI; i += NPT) {
+                    const int c = i % G::NCI, p = i / G::NCI;
+                    const int ti = p / G::IC, tj = p - ti * G::IC;
+                    const int yy = y0 - 1 + ti, xx = x0 - 1 + tj;
+                    uint4 q = make_uint4(0u, 0u, 0u, 0u);
+                    if (yy >= 0 && xx >= 0 && yy < a.H && xx < a.W) {
+                        float v[8];
+                        up2_chunk<T>(xlf, hl, wl, CIN, yy, xx, c, v);
+                        if (a.skip) {
+                            const uint4 sk = __ldg(reinterpret_cast<const uint4*>(
+                                reinterpret_cast<const T*>(a.skip) + (((int64_t)f * a.H + yy) * a.W + xx) * CIN + c * 8));
+                            const uint32_t* sp = &sk.x;
+#pragma unroll
+                            for (int e = 0; e < 4; ++e) {
+                                const float2 sv = Elem<T>::unpack(sp[e]);
+                                v[2 * e] += sv.x;
+                                v[2 * e + 1] += sv.y;
+                            }
+                        }
+                        q.x = Elem<T>::pack(v[0], v[1]);
+                        q.y = Elem<T>::pack(v[2], v[3]);
+                        q.z = Elem<T>::pack(v[4], v[5]);
+                        q.w = Elem<T>::pack(v[6], v[7]);
+                    }
+                    *reinterpret_cast<uint4*>(in + c * G::PIN + p * 16) = q;
+                }
+                fence_proxy_async();
+                mbar_arrive(&in_full[s]);
+            }
+        }
+    } else if (warp == MW) {
+        // ------------------------------------------------------------ MMA issuer
+        if (lane == 0) {
+            constexpr uint32_t idesc3 = umma_idesc(128, C3, Elem<T>::kUmmaFmt);
+            constexpr uint32_t idesc1 = umma_idesc(128, C1, Elem<T>::kUmmaFmt);
+            auto conv1 = [&](int j) {
+                const int m = j % NMID, a1 = j & 1;
+                mbar_wait(&mid_full[m], (j / NMID) & 1);
+                mbar_wait(&a1_empty[a1], ((j >> 1) & 1) ^ 1);
+                tc_fence_after();
+                const uint32_t mid = sbase + G::OFF_MID + m * G::MIDB;
+#pragma unroll
+                for (int b = 0; b < NB; ++b)
+#pragma unroll
+                    for (int kk = 0; kk < C3 / 16; ++kk) {
+                        const uint64_t da = umma_desc(mid + (2 * kk) * G::PMID + (b * 8) * 16, G::PMID, G::TW * 16);
+                        const uint64_t db = umma_desc(sbase + G::OFF_W1 + kk * C1 * 32, C1 * 16, 128);
+                        umma_f16(tmem + G::ACC1 + (a1 * NB + b) * C1, da, db, idesc1, kk ? 1u : 0u);
+                    }
+                umma_commit(&mid_empty[m]);
+                umma_commit(&a1_full[a1]);
+            };
+            for (int k = 0; k < mytiles; ++k) {
+                const int s = k % NIN, a3 = k & 1;
+                mbar_wait(&in_full[s], (k / NIN) & 1);
+                mbar_wait(&a3_empty[a3], ((k >> 1) & 1) ^ 1);
+                tc_fence_after();
+                const uint32_t in = sbase + s * G::INB;
 #pragma unroll 1
-    for (int tap = 0; tap < 9; ++tap) {
-        const int slot = tap & 1;
-        if (tid == 0) {
+                for (int tap = 0; tap < 9; ++tap) {
+                    const int dy = tap / 3, dx = tap % 3;
+#pragma unroll
+                    for (int b = 0; b < NB; ++b)
+#pragma unroll
+                        for (int kk = 0; kk < G::KK; ++kk) {
+                            // M-block b: 16 output rows x 8 px; core matrix i = output row i
+                            const uint64_t da = umma_desc(in + (2 * kk) * G::PIN + (dy * G::IC + b * 8 + dx) * 16,
+                                                          G::PIN, G::IC * 16);
+                            const uint64_t db = umma_desc(sbase + G::OFF_W3 + (tap * G::KK + kk) * C3 * 32, C3 * 16, 128);
+                            umma_f16(tmem + G::ACC3 + (a3 * NB + b) * C3, da, db, idesc3, (tap | kk) ? 1u : 0u);
+                        }
+                }
+                umma_commit(&in_empty[s]);
+                umma_commit(&a3_full[a3]);
+                if (k >= 1) conv1(k - 1);
+            }
+            if (mytiles > 0) conv1(mytiles - 1);
+        }
+    } else {
+        // ------------------------------------------------------------ epilogue
+        const int q = warp & 3;                      // TMEM lane quadrant of this warp
+        const int m = q * 32 + lane;                 // M row == TMEM lane
+        const int pi = m >> 3, pj = m & 7;           // pixel row / column inside an M-block
+        const uint32_t tl = (uint32_t)(q * 32) << 16;
+        auto epi1 = [&](int k) {
+            const int a3 = k & 1, mm = k % NMID;
+            mbar_wait(&a3_full[a3], (k >> 1) & 1);
+            mbar_wait(&mid_empty[mm], ((k / NMID) & 1) ^ 1);
             tc_fence_after();
-            const int dy = tap / 3, dx = tap % 3;
-            const uint32_t wbase = sb + G::OFF_W + slot * G::WTAP;
+            uint8_t* mid = smem + G::OFF_MID + mm * G::MIDB;
+#pragma unroll 1
+            for (int b = 0; b < NB; ++b) {
 #pragma unroll
-            for (int b = 0; b < NB; ++b)
+                for (int c0 = 0; c0 < C3; c0 += 16) {
+                    float v[16];
+                    tmem_ld16(tmem + tl + G::ACC3 + (a3 * NB + b) * C3 + c0, v);
+                    uint4 qv[2];
+                    uint32_t* qp = &qv[0].x;
 #pragma unroll
-                for (int kk = 0; kk < G::KK; ++kk) {
-                    // M-block b: 16 output rows x 8 px; core matrix i = row i
-                    const uint32_t sa = sb + (2 * kk) * G::PIN + (dy * G::IC + b * 8 + dx) * 16;
-                    const uint64_t da = umma_desc(sa, G::PIN, G::IC * 16);
-                    const uint64_t db = umma_desc(wbase + kk * C3 * 32, C3 * 16, 128);
-                    umma_f16(tmem + b * C3, da, db, idesc3, (tap | kk) ? 1u : 0u);
+                    for (int e = 0; e < 8; ++e)
+                        qp[e] = Elem<T>::pack(fmaxf(v[2 * e] + sb3[c0 + 2 * e], 0.f),
+                                              fmaxf(v[2 * e + 1] + sb3[c0 + 2 * e + 1], 0.f));
+                    const int p = pi * G::TW + b * 8 + pj;
+                    *reinterpret_cast<uint4*>(mid + (c0 / 8) * G::PMID + p * 16) = qv[0];
+                    *reinterpret_cast<uint4*>(mid + (c0 / 8 + 1) * G::PMID + p * 16) = qv[1];
                 }
-            umma_commit(&bar[1 + slot]);
-        }
-        if (tap + 1 < 9) {
-            // slot (tap+1)&1 was last read by tap-1's MMAs
-            if (tap >= 1) mbar_wait(&bar[1 + ((tap + 1) & 1)], ((tap - 1) >> 1) & 1);
-            copy_smem16(smem + G::OFF_W + ((tap + 1) & 1) * G::WTAP,
-                        reinterpret_cast<const uint8_t*>(a.w3) + (size_t)(tap + 1) * G::WTAP, G::WTAP);
+            }
             fence_proxy_async();
-            __syncthreads();
-        }
-    }
-    if (tid == 0) umma_commit(&bar[0]);
-    mbar_wait(&bar[0], 0);
-    tc_fence_after();
-
-    // ---- epilogue 1: relu(conv3 + b3) -> 16-bit mid tile (chunk-planar)
-    const int m = warp * 32 + lane;             // TMEM lane == M row
-    const int pi = m >> 3, pj = m & 7;          // pixel row / column within the M-block
-    T* unused = nullptr;
-    (void)unused;
+            tc_fence_before();
+            mbar_arrive(&a3_empty[a3]);
+            mbar_arrive(&mid_full[mm]);
+        };
+        auto epi2 = [&](int j) {
+            const int a1 = j & 1;
+            int f, y0, x0;
+            tile_of(j, f, y0, x0);
+            mbar_wait(&a1_full[a1], (j >> 1) & 1);
+            tc_fence_after();
+            const int oy = y0 + pi;
 #pragma unroll 1
-    for (int b = 0; b < NB; ++b) {
+            for (int b = 0; b < NB; ++b) {
+                const int ox = x0 + b * 8 + pj;
+                const bool inside = oy < a.H && ox < a.W;
 #pragma unroll
-        for (int c0 = 0; c0 < C3; c0 += 16) {
-            float v[16];
-            tmem_ld16(tmem + ((uint32_t)(warp * 32) << 16) + b * C3 + c0, v);
-            uint4 q[2];
-            uint32_t* qp = &q[0].x;
+                for (int c0 = 0; c0 < C1; c0 += 16) {
+                    float v[16];
+                    tmem_ld16(tmem + tl + G::ACC1 + (a1 * NB + b) * C1 + c0, v);
 #pragma unroll
-            for (int k = 0; k < 8; ++k)
-                qp[k] = Elem<T>::pack(fmaxf(v[2 * k] + __ldg(a.b3 + c0 + 2 * k), 0.f),
-                                      fmaxf(v[2 * k + 1] + __ldg(a.b3 + c0 + 2 * k + 1), 0.f));
-            const int p = pi * G::TW + b * 8 + pj;
-            *reinterpret_cast<uint4*>(smem + G::OFF_MID + (c0 / 8) * G::PMID + p * 16) = q[0];
-            *reinterpret_cast<uint4*>(smem + G::OFF_MID + (c0 / 8 + 1) * G::PMID + p * 16) = q[1];
+                    for (int e = 0; e < 16; ++e) v[e] = fmaxf(v[e] + sb1[c0 + e], 0.f);
+                    if (DST & DST_STORE) {
+                        if (inside) {
+                            uint4 qv[2];
+                            uint32_t* qp = &qv[0].x;
+#pragma unroll
+                            for (int e = 0; e < 8; ++e) qp[e] = Elem<T>::pack(v[2 * e], v[2 * e + 1]);
+                            uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<T*>(a.out) +
+                                                                  (((int64_t)f * a.H + oy) * a.W + ox) * C1 + c0);
+                            dst[0] = qv[0];
+                            dst[1] = qv[1];
+                        }
+                    }
+                    if (DST & DST_POOL) {
+#pragma unroll
+                        for (int e = 0; e < 16; ++e) {
+                            v[e] += __shfl_xor_sync(0xffffffffu, v[e], 1);
+                            v[e] += __shfl_xor_sync(0xffffffffu, v[e], 8);
+                        }
+                        if (!(pi & 1) && !(pj & 1) && inside) {
+                            uint4 qv[2];
+                            uint32_t* qp = &qv[0].x;
+#pragma unroll
+                            for (int e = 0; e < 8; ++e) qp[e] = Elem<T>::pack(v[2 * e] * 0.25f, v[2 * e + 1] * 0.25f);
+                            const int H2 = a.H / 2, W2 = a.W / 2;
+                            uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<T*>(a.pool) +
+                                                                  (((int64_t)f * H2 + oy / 2) * W2 + ox / 2) * C1 + c0);
+                            dst[0] = qv[0];
+                            dst[1] = qv[1];
+                        }
+                    }
+                }
+            }
+            tc_fence_before();
+            mbar_arrive(&a1_empty[a1]);
+        };
+        for (int k = 0; k < mytiles; ++k) {
+            epi1(k);
+            if (k >= 1) epi2(k - 1);
         }
-    }
-    fence_proxy_async();
-    tc_fence_before();
-    __syncthreads();
-    tc_fence_after();
-
-    // ---- conv1 (1x1): A = mid tile, B = w1
-    if (tid == 0) {
-#pragma unroll
-        for (int b = 0; b < NB; ++b)
-#pragma unroll
-            for (int kk = 0; kk < C3 / 16; ++kk) {
-                const uint32_t sa = sb + G::OFF_MID + (2 * kk) * G::PMID + (b * 8) * 16;
-                const uint64_t da = umma_desc(sa, G::PMID, G::TW * 16);
-                const uint64_t db = umma_desc(sb + G::OFF_W1 + kk * C1 * 32, C1 * 16, 128);
-                umma_f16(tmem + b * C3, da, db, idesc1, kk ? 1u : 0u);
-            }
-        umma_commit(&bar[0]);
-    }
-    mbar_wait(&bar[0], 1);
-    tc_fence_after();
-
-    // ---- epilogue 2: relu(conv1 + b1) -> NHWC store and/or 2x2 average pool
-    const int oy = y0 + pi;
-#pragma unroll 1
-    for (int b = 0; b < NB; ++b) {
-        const int ox = x0 + b * 8 + pj;
-        const bool inside = oy < a.H && ox < a.W;
-#pragma unroll
-        for (int c0 = 0; c0 < C1; c0 += 16) {
-            float v[16];
-            tmem_ld16(tmem + ((uint32_t)(warp * 32) << 16) + b * C3 + c0, v);
-#pragma unroll
-            for (int k = 0; k < 16; ++k) v[k] = fmaxf(v[k] + __ldg(a.b1 + c0 + k), 0.f);
-            if (DST & DST_STORE) {
-                if (inside) {
-                    uint4 q[2];
-                    uint32_t* qp = &q[0].x;
-#pragma unroll
-                    for (int k = 0; k < 8; ++k) qp[k] = Elem<T>::pack(v[2 * k], v[2 * k + 1]);
-                    uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<T*>(a.out) +
-                                                          (((int64_t)f * a.H + oy) * a.W + ox) * C1 + c0);
-                    dst[0] = q[0];
-                    dst[1] = q[1];
-                }
-            }
-            if (DST & DST_POOL) {
-#pragma unroll
-                for (int k = 0; k < 16; ++k) {
-                    v[k] += __shfl_xor_sync(0xffffffffu, v[k], 1);
-                    v[k] += __shfl_xor_sync(0xffffffffu, v[k], 8);
-                }
-                if (!(pi & 1) && !(pj & 1) && inside) {
-                    uint4 q[2];
-                    uint32_t* qp = &q[0].x;
-#pragma unroll
-                    for (int k = 0; k < 8; ++k) qp[k] = Elem<T>::pack(v[2 * k] * 0.25f, v[2 * k + 1] * 0.25f);
-                    const int H2 = a.H / 2, W2 = a.W / 2;
-                    uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<T*>(a.pool) +
-                                                          (((int64_t)f * H2 + oy / 2) * W2 + ox / 2) * C1 + c0);
-                    dst[0] = q[0];
-                    dst[1] = q[1];
-                }
-            }
-        }
+        if (mytiles > 0) epi2(mytiles - 1);
     }
     tc_fence_before();
     __syncthreads();
-    if (warp == 0) tmem_dealloc<G::TCOLS>(tmem);
-}
-
-template <typename T, int CIN, int C3, int C1, int SRC, int DST, int NB>
-void launch_level(const LevelArgs& a, int n, cudaStream_t st, const char* name) {
-    using G = LvGeom<CIN, C3, C1, NB>;
-    auto k = level_tc_kernel<T, CIN, C3, C1, SRC, DST, NB>;
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, G::SMEM);
-        attr = true;
-    }
-    dim3 grd((a.W + G::TW - 1) / G::TW, (a.H + G::TH - 1) / G::TH, n);
-    NSM_PROF(name, st);
-    k<<<grd, 128, G::SMEM, st>>>(a);
+    if (warp == EW0) tmem_dealloc<G::TCOLS>(tmem);
 }
 
 // ------------------------------------------------------------------ host side
@@ -994,11 +1073,57 @@ int num_sms() {
     return n;
 }
 
-struct F16Layout {
-    // per-conv offsets (bytes) into the plan's device block
-    size_t e0_w3, e0_w1, d0_w3, d0_w1, head;
-    size_t lv_w3[4][2], lv_w1[4][2];   // [level 1..3][enc/dec]
-};
+// cuTensorMapEncodeTiled through the runtime's driver entry point (the
+// library links cudart statically and never links libcuda directly).
+PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    if (!fn) {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = (PFN_cuTensorMapEncodeTiled_v12000)p;
+    }
+    return fn;
+}
+
+// 5-D view of an NHWC 16-bit tensor (8 elems, x, y, chunk, frame) whose
+// TMA box lands in SMEM as [chunk][y][x][8], i.e. the chunk-planar tile.
+bool encode_nhwc_map(const void* base, bool bf16, int C, int H, int W, int nf, int box_w, int box_h,
+                     CUtensorMap* m) {
+    auto enc = tensor_map_encoder();
+    if (!enc || ((uintptr_t)base % 16)) return false;
+    const cuuint64_t dims[5] = {8, (cuuint64_t)W, (cuuint64_t)H, (cuuint64_t)(C / 8), (cuuint64_t)nf};
+    const cuuint64_t strides[4] = {(cuuint64_t)C * 2, (cuuint64_t)W * C * 2, 16, (cuuint64_t)H * W * C * 2};
+    const cuuint32_t box[5] = {8, (cuuint32_t)box_w, (cuuint32_t)box_h, (cuuint32_t)(C / 8), 1};
+    const cuuint32_t es[5] = {1, 1, 1, 1, 1};
+    return enc(m, bf16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 5,
+               const_cast<void*>(base), dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+               CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+template <typename T, int CIN, int C3, int C1, int SRC, int DST, int NB, int NIN, int NMID>
+nsm_status launch_level(const LevelArgs& a, int nf, cudaStream_t st, const char* name) {
+    using G = LvGeom<CIN, C3, C1, NB, NIN, NMID>;
+    constexpr int NPW = SRC == SRC_TENSOR ? 1 : 8;
+    auto k = level_kernel<T, CIN, C3, C1, SRC, DST, NB, NIN, NMID, NPW>;
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, G::SMEM);
+        attr = true;
+    }
+    CUtensorMap tin;
+    memset(&tin, 0, sizeof tin);
+    if (SRC == SRC_TENSOR &&
+        !encode_nhwc_map(a.x, std::is_same<T, __nv_bfloat16>::value, CIN, a.H, a.W, nf, G::IC, G::IR, &tin))
+        return fail(NSM_ERR_CUDA, "%s: TMA tensor map encoding failed", name);
+    const int total = ((a.W + G::TW - 1) / G::TW) * ((a.H + G::TH - 1) / G::TH) * nf;
+    const int grid = std::min(total, num_sms());      // TMEM: 512 columns -> one CTA per SM
+    NSM_PROF(name, st);
+    k<<<grid, (NPW + 5) * 32, G::SMEM, st>>>(a, tin, total);
+    return NSM_OK;
+}
 
 struct Bufs {
     void *p1, *s1, *p2, *s2, *p3, *b3, *d2, *d1;
@@ -1037,35 +1162,25 @@ nsm_status run_levels(const Plan& p, const Bufs& b, int nf, int H0, int W0, cuda
     LevelArgs a{};
     // l1 encoder: P1 (16) -> S1 (32) + pool -> P2
     a = LevelArgs{b.p1, nullptr, H1, W1, L1.enc3.wpk, L1.enc3.b32, L1.enc1.wpk, L1.enc1.b32, b.s1, b.p2};
-    launch_level<T, 16, 32, 32, SRC_TENSOR, DST_STORE | DST_POOL, 4>(a, nf, st, "lv1_enc");
+    nsm_status s = launch_level<T, 16, 32, 32, SRC_TENSOR, DST_STORE | DST_POOL, 4, 2, 2>(a, nf, st, "lv1_enc");
+    if (s != NSM_OK) return s;
     // l2 encoder: P2 (32) -> S2 (64) + pool -> P3
     a = LevelArgs{b.p2, nullptr, H2, W2, L2.enc3.wpk, L2.enc3.b32, L2.enc1.wpk, L2.enc1.b32, b.s2, b.p3};
-    launch_level<T, 32, 64, 64, SRC_TENSOR, DST_STORE | DST_POOL, 2>(a, nf, st, "lv2_enc");
+    s = launch_level<T, 32, 64, 64, SRC_TENSOR, DST_STORE | DST_POOL, 2, 2, 2>(a, nf, st, "lv2_enc");
+    if (s != NSM_OK) return s;
     // l3 bottleneck: P3 (64) -> 128 -> B3 (64)
     a = LevelArgs{b.p3, nullptr, H3, W3, L3.enc3.wpk, L3.enc3.b32, L3.enc1.wpk, L3.enc1.b32, b.b3, nullptr};
-    launch_level<T, 64, 128, 64, SRC_TENSOR, DST_STORE, 1>(a, nf, st, "lv3_bott");
+    s = launch_level<T, 64, 128, 64, SRC_TENSOR, DST_STORE, 1, 1, 1>(a, nf, st, "lv3_bott");
+    if (s != NSM_OK) return s;
     // l2 decoder: up(B3) + S2 -> 64 -> D2 (32)
     a = LevelArgs{b.b3, b.s2, H2, W2, L2.dec3.wpk, L2.dec3.b32, L2.dec1.wpk, L2.dec1.b32, b.d2, nullptr};
-    launch_level<T, 64, 64, 32, SRC_UP, DST_STORE, 2>(a, nf, st, "lv2_dec");
+    s = launch_level<T, 64, 64, 32, SRC_UP, DST_STORE, 2, 2, 2>(a, nf, st, "lv2_dec");
+    if (s != NSM_OK) return s;
     // l1 decoder: up(D2) + S1 -> 32 -> D1 (16)
     a = LevelArgs{b.d2, b.s1, H1, W1, L1.dec3.wpk, L1.dec3.b32, L1.dec1.wpk, L1.dec1.b32, b.d1, nullptr};
-    launch_level<T, 32, 32, 16, SRC_UP, DST_STORE, 4>(a, nf, st, "lv1_dec");
+    s = launch_level<T, 32, 32, 16, SRC_UP, DST_STORE, 4, 2, 2>(a, nf, st, "lv1_dec");
     (void)W3;
-    return NSM_OK;
-}
-
-// cuTensorMapEncodeTiled through the runtime's driver entry point (the
-// library links cudart statically and never links libcuda directly).
-PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
-    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
-    if (!fn) {
-        void* p = nullptr;
-        cudaDriverEntryPointQueryResult q;
-        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
-            q == cudaDriverEntryPointSuccess)
-            fn = (PFN_cuTensorMapEncodeTiled_v12000)p;
-    }
-    return fn;
+    return s;
 }
 
 // Tensor maps over the planar fp32 G-buffer of frames [0, nf) of a chunk;
