@@ -773,7 +773,7 @@ struct LvGeom {
     static constexpr int OFF_W1 = OFF_W3 + W3B;
     static constexpr int OFF_B = OFF_W1 + W1B;
     static constexpr int OFF_BAR = (OFF_B + (C3 + C1) * 4 + 15) / 16 * 16;
-    static constexpr int SMEM = OFF_BAR + 160;
+    static constexpr int SMEM = OFF_BAR + 176;
     static constexpr int ACC3 = 0, ACC1 = 2 * NB * C3;         // TMEM columns (both double-buffered)
     static constexpr int TCOLS = tmem_cols(2 * NB * (C3 + C1));
     static constexpr int TX_BYTES = NCI * PIN;
@@ -791,6 +791,13 @@ __device__ __forceinline__ void tma_load_5d(uint32_t dst, const CUtensorMap* map
         "[%1, {%2, %3, %4, %5, %6}], [%7];" ::"r"(dst),
         "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4), "r"(smem_u32(bar))
         : "memory");
+}
+
+// 1-D bulk copy global -> SMEM (TMA engine, no tensor map), 16-B granules.
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+                 "l"(src), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
 }
 
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
@@ -824,7 +831,8 @@ __global__ void __launch_bounds__((NPW + 5) * 32, 1) level_kernel(const __grid_c
     uint64_t* mid_empty = bar + 10;
     uint64_t* a1_full = bar + 12;
     uint64_t* a1_empty = bar + 14;
-    uint32_t* tptr = reinterpret_cast<uint32_t*>(smem + G::OFF_BAR + 128);
+    uint64_t* wbar = bar + 16;        // weights landed
+    uint32_t* tptr = reinterpret_cast<uint32_t*>(smem + G::OFF_BAR + 136);
     float* sb3 = reinterpret_cast<float*>(smem + G::OFF_B);
     float* sb1 = sb3 + C3;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -852,10 +860,13 @@ __global__ void __launch_bounds__((NPW + 5) * 32, 1) level_kernel(const __grid_c
             mbar_init(&a1_full[i], 1);
             mbar_init(&a1_empty[i], 128);
         }
+        mbar_init(wbar, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        // resident weights: two async bulk copies, waited on by the MMA warp only
+        mbar_expect_tx(wbar, G::W3B + G::W1B);
+        bulk_g2s(sbase + G::OFF_W3, a.w3, G::W3B, wbar);
+        bulk_g2s(sbase + G::OFF_W1, a.w1, G::W1B, wbar);
     }
-    copy_smem16(smem + G::OFF_W3, reinterpret_cast<const uint8_t*>(a.w3), G::W3B);
-    copy_smem16(smem + G::OFF_W1, reinterpret_cast<const uint8_t*>(a.w1), G::W1B);
     for (int i = tid; i < C3; i += blockDim.x) sb3[i] = a.b3[i];
     for (int i = tid; i < C1; i += blockDim.x) sb1[i] = a.b1[i];
     fence_proxy_async();
@@ -939,6 +950,7 @@ __global__ void __launch_bounds__((NPW + 5) * 32, 1) level_kernel(const __grid_c
                 umma_commit(&mid_empty[m]);
                 umma_commit(&a1_full[a1]);
             };
+            mbar_wait(wbar, 0);
             for (int k = 0; k < mytiles; ++k) {
                 const int s = k % NIN, a3 = k & 1;
                 mbar_wait(&in_full[s], (k / NIN) & 1);
