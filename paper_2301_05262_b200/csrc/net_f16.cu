@@ -30,7 +30,16 @@ namespace nsm {
 namespace {
 
 // ------------------------------------------------------------------ config
-constexpr int kChunkFrames = 2;       // frames per pass through all levels (L2 residency)
+// frames per pass through all levels (L2 residency vs. launch fill/drain);
+// NSM_CHUNK_FRAMES overrides it for experiments
+int chunk_frames() {
+    static int v = 0;
+    if (!v) {
+        const char* e = getenv("NSM_CHUNK_FRAMES");
+        v = e ? std::max(1, std::min(NSM_MAX_FRAMES_PER_LAUNCH, atoi(e))) : 4;
+    }
+    return v;
+}
 constexpr int E0_TH = 16, E0_TW = 64;  // level-0 output tile (enc0 / dec0)
 constexpr int E0_IR = E0_TH + 2, E0_IC = E0_TW + 2;
 constexpr int E0_PLANE = plane_bytes(E0_IR * E0_IC, 2);
@@ -585,7 +594,7 @@ struct Dec0Args {
     const float* b3;
     const float* b1;
     const float* bh;
-    float4* y;            // (N, H0, W0) x 4 head channels, fp32
+    float* y;             // head output, 4 fp32 planes per frame: (N, 4, H0, W0)
 };
 
 // Bilinear 2x of an NHWC 16-bit tensor at one output pixel, 8 channels
@@ -689,12 +698,15 @@ __global__ void __launch_bounds__(kL0Threads, 1) dec0_kernel(Dec0Args a, int tot
                 mma16816<T>(yh, a2, BH[0], BH[1]);
                 const int oy = tl.ty0 + r0 + oo;
                 if (t < 2 && oy < a.H0) {
-                    float2* yrow = reinterpret_cast<float2*>(a.y + ((int64_t)tl.f * a.H0 + oy) * a.W0);
+                    const int64_t hw0 = (int64_t)a.H0 * a.W0;
+                    float* yp = a.y + ((int64_t)tl.f * 4 + 2 * t) * hw0 + (int64_t)oy * a.W0;
 #pragma unroll
                     for (int hlf = 0; hlf < 2; ++hlf) {
                         const int ox = tl.tx0 + sx + g + 8 * hlf;
-                        if (ox < a.W0)
-                            yrow[2 * ox + t] = make_float2(yh[2 * hlf] + biash[0], yh[2 * hlf + 1] + biash[1]);
+                        if (ox < a.W0) {
+                            yp[ox] = yh[2 * hlf] + biash[0];
+                            yp[hw0 + ox] = yh[2 * hlf + 1] + biash[1];
+                        }
                     }
                 }
             });
@@ -703,41 +715,54 @@ __global__ void __launch_bounds__(kL0Threads, 1) dec0_kernel(Dec0Args a, int tot
 
 // Head reconstruction (network.py:199-209) + sigmoid, cropped to (h, w):
 // out(2Y+sy, 2X+sx) = sigmoid(up2(y0) + [sy,sx != 0,0] * y_{2sy+sx}(Y, X)).
-__device__ __forceinline__ float y0_at(const float4* yf, int W0, int r, int c) {
-    return __ldg(reinterpret_cast<const float*>(yf + (int64_t)r * W0 + c));
-}
-
-__global__ void recon_kernel(const float4* __restrict__ y, int H0, int W0, int h, int w, int n,
-                             void* __restrict__ out, int f16) {
+// The 2x half-pixel bilinear of y0 at the 4 outputs of L0 pixel (Y, X) uses
+// rows/cols Y-1..Y+1 with weights (1/4, 3/4); clamping the neighbour indices
+// reproduces the reference's edge clamp (_upsample_taps, autodiff.py:258-264).
+__global__ void __launch_bounds__(128) recon_kernel(const float* __restrict__ y, int H0, int W0, int h,
+                                                     int w, int n, void* __restrict__ out, int f16) {
     const int X = blockIdx.x * blockDim.x + threadIdx.x;
     const int Y = blockIdx.y;
     const int f = blockIdx.z;
     if (X >= W0) return;
-    const float4* yf = y + (int64_t)f * H0 * W0;
-    const float4 me = __ldg(yf + (int64_t)Y * W0 + X);
-    const float det[4] = {0.f, me.y, me.z, me.w};
+    const int64_t hw0 = (int64_t)H0 * W0;
+    const float* y0 = y + (int64_t)f * 4 * hw0;
+    const int xm = max(X - 1, 0), xp = min(X + 1, W0 - 1);
+    const int ym = max(Y - 1, 0), yp = min(Y + 1, H0 - 1);
+    float r[3][3];
+    const int rows[3] = {ym, Y, yp}, cols[3] = {xm, X, xp};
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+#pragma unroll
+        for (int j = 0; j < 3; ++j) r[i][j] = __ldg(y0 + (int64_t)rows[i] * W0 + cols[j]);
+    const int64_t me = (int64_t)Y * W0 + X;
+    const float det[4] = {0.f, __ldg(y0 + hw0 + me), __ldg(y0 + 2 * hw0 + me), __ldg(y0 + 3 * hw0 + me)};
 #pragma unroll
     for (int sy = 0; sy < 2; ++sy) {
         const int oy = 2 * Y + sy;
         if (oy >= h) continue;
-        const float fy = fminf(fmaxf((oy + 0.5f) * 0.5f - 0.5f, 0.f), (float)(H0 - 1));
-        const int r0 = (int)fy, r1 = min(r0 + 1, H0 - 1);
-        const float wy = fy - r0;
+        // rows: sy = 0 -> (Y-1, Y) weights (1/4, 3/4); sy = 1 -> (Y, Y+1) weights (3/4, 1/4)
+        float cr[3];
+#pragma unroll
+        for (int j = 0; j < 3; ++j) cr[j] = sy ? r[1][j] * 0.75f + r[2][j] * 0.25f : r[0][j] * 0.25f + r[1][j] * 0.75f;
+        float o2[2];
 #pragma unroll
         for (int sx = 0; sx < 2; ++sx) {
-            const int ox = 2 * X + sx;
-            if (ox >= w) continue;
-            const float fx = fminf(fmaxf((ox + 0.5f) * 0.5f - 0.5f, 0.f), (float)(W0 - 1));
-            const int c0 = (int)fx, c1 = min(c0 + 1, W0 - 1);
-            const float wx = fx - c0;
-            const float a = y0_at(yf, W0, r0, c0) * (1.f - wy) + y0_at(yf, W0, r1, c0) * wy;
-            const float b = y0_at(yf, W0, r0, c1) * (1.f - wy) + y0_at(yf, W0, r1, c1) * wy;
-            const float v = a * (1.f - wx) + b * wx + det[2 * sy + sx];
+            const float base = sx ? cr[1] * 0.75f + cr[2] * 0.25f : cr[0] * 0.25f + cr[1] * 0.75f;
+            const float v = base + det[2 * sy + sx];
             const float e = __expf(-fabsf(v));
-            const float s = v >= 0.f ? 1.f / (1.f + e) : e / (1.f + e);
-            const int64_t o = ((int64_t)f * h + oy) * w + ox;
-            if (f16) reinterpret_cast<__half*>(out)[o] = __float2half_rn(s);
-            else reinterpret_cast<float*>(out)[o] = s;
+            o2[sx] = v >= 0.f ? __frcp_rn(1.f + e) : __fdividef(e, 1.f + e);
+        }
+        const int64_t o = ((int64_t)f * h + oy) * w + 2 * X;
+        if (2 * X + 1 < w && !(w & 1)) {
+            if (f16) *reinterpret_cast<__half2*>(reinterpret_cast<__half*>(out) + o) = __floats2half2_rn(o2[0], o2[1]);
+            else *reinterpret_cast<float2*>(reinterpret_cast<float*>(out) + o) = make_float2(o2[0], o2[1]);
+        } else {
+#pragma unroll
+            for (int sx = 0; sx < 2; ++sx) {
+                if (2 * X + sx >= w) break;
+                if (f16) reinterpret_cast<__half*>(out)[o + sx] = __float2half_rn(o2[sx]);
+                else reinterpret_cast<float*>(out)[o + sx] = o2[sx];
+            }
         }
     }
 }
@@ -756,9 +781,10 @@ struct LevelArgs {
     const float* b1;
     void* out;           // (N, H, W, C1)
     void* pool;          // (N, H/2, W/2, C1)
+    int dbg;             // experiments only: 1 skip producer math, 2 skip epilogue math, 4 skip MMAs
 };
 
-template <int CIN, int C3, int C1, int NB, int NIN, int NMID>
+template <int CIN, int C3, int C1, int NB, int NIN, int NMID, int STG>
 struct LvGeom {
     static constexpr int TH = 16, TW = 8 * NB;
     static constexpr int IR = TH + 2, IC = TW + 2, NPI = IR * IC;
@@ -771,9 +797,14 @@ struct LvGeom {
     static constexpr int OFF_MID = NIN * INB;
     static constexpr int OFF_W3 = OFF_MID + NMID * MIDB;
     static constexpr int OFF_W1 = OFF_W3 + W3B;
-    static constexpr int OFF_B = OFF_W1 + W1B;
+    // SRC_UP staging (STG): skip tile (halo'd, pixel-major) and low-res tile
+    static constexpr int LR = TH / 2 + 2, LC = TW / 2 + 2;
+    static constexpr int SKB = STG ? IR * IC * CIN * 2 : 0, LOB = STG ? LR * LC * CIN * 2 : 0;
+    static constexpr int OFF_SK = round128(OFF_W1 + W1B);
+    static constexpr int OFF_LO = round128(OFF_SK + SKB);
+    static constexpr int OFF_B = round128(OFF_LO + LOB);
     static constexpr int OFF_BAR = (OFF_B + (C3 + C1) * 4 + 15) / 16 * 16;
-    static constexpr int SMEM = OFF_BAR + 176;
+    static constexpr int SMEM = OFF_BAR + 192;
     static constexpr int ACC3 = 0, ACC1 = 2 * NB * C3;         // TMEM columns (both double-buffered)
     static constexpr int TCOLS = tmem_cols(2 * NB * (C3 + C1));
     static constexpr int TX_BYTES = NCI * PIN;
@@ -817,10 +848,11 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
 // All hand-offs are mbarriers (tcgen05.commit on the tensor-core side), so
 // conv3 of tile k+1 overlaps the epilogues of tile k.
 template <typename T, int CIN, int C3, int C1, int SRC, int DST, int NB, int NIN, int NMID, int NPW>
-__global__ void __launch_bounds__((NPW + 5) * 32, 1) level_kernel(const __grid_constant__ LevelArgs a,
+__global__ void __launch_bounds__((NPW + 9) * 32, 1) level_kernel(const __grid_constant__ LevelArgs a,
                                                                    const __grid_constant__ CUtensorMap tin,
+                                                                   const __grid_constant__ CUtensorMap tlo,
                                                                    int total) {
-    using G = LvGeom<CIN, C3, C1, NB, NIN, NMID>;
+    using G = LvGeom<CIN, C3, C1, NB, NIN, NMID, SRC == SRC_UP>;
     extern __shared__ __align__(128) uint8_t smem[];
     uint64_t* bar = reinterpret_cast<uint64_t*>(smem + G::OFF_BAR);
     uint64_t* in_full = bar + 0;      // [2]
@@ -832,11 +864,12 @@ __global__ void __launch_bounds__((NPW + 5) * 32, 1) level_kernel(const __grid_c
     uint64_t* a1_full = bar + 12;
     uint64_t* a1_empty = bar + 14;
     uint64_t* wbar = bar + 16;        // weights landed
-    uint32_t* tptr = reinterpret_cast<uint32_t*>(smem + G::OFF_BAR + 136);
+    uint64_t* stg_full = bar + 17;    // SRC_UP staging landed
+    uint32_t* tptr = reinterpret_cast<uint32_t*>(smem + G::OFF_BAR + 144);
     float* sb3 = reinterpret_cast<float*>(smem + G::OFF_B);
     float* sb1 = sb3 + C3;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    constexpr int EW0 = NPW, MW = NPW + 4;          // first epilogue warp, MMA warp
+    constexpr int EW0 = NPW, MW = NPW + 8;          // first of 8 epilogue warps, MMA warp
     constexpr int NPT = NPW * 32;
     const uint32_t sbase = smem_u32(smem);
     const int ntx = (a.W + G::TW - 1) / G::TW, nty = (a.H + G::TH - 1) / G::TH;
@@ -854,13 +887,14 @@ __global__ void __launch_bounds__((NPW + 5) * 32, 1) level_kernel(const __grid_c
             mbar_init(&in_full[i], SRC == SRC_TENSOR ? 1 : NPT);
             mbar_init(&in_empty[i], 1);
             mbar_init(&a3_full[i], 1);
-            mbar_init(&a3_empty[i], 128);
-            mbar_init(&mid_full[i], 128);
+            mbar_init(&a3_empty[i], 256);
+            mbar_init(&mid_full[i], 256);
             mbar_init(&mid_empty[i], 1);
             mbar_init(&a1_full[i], 1);
-            mbar_init(&a1_empty[i], 128);
+            mbar_init(&a1_empty[i], 256);
         }
         mbar_init(wbar, 1);
+        mbar_init(stg_full, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         // resident weights: two async bulk copies, waited on by the MMA warp only
         mbar_expect_tx(wbar, G::W3B + G::W1B);
@@ -889,43 +923,62 @@ __global__ void __launch_bounds__((NPW + 5) * 32, 1) level_kernel(const __grid_c
                 }
             }
         } else {
-            const T* xf = reinterpret_cast<const T*>(a.x);
+            // up2(low) + skip from TMA-staged pixel-major tiles (skip: the halo'd
+            // tile; low: (TH/2+2) x (TW/2+2) source pixels, edge-clamped indices)
             const int hl = a.H / 2, wl = a.W / 2;
-            for (int k = 0; k < mytiles; ++k) {
-                const int s = k % NIN;
-                mbar_wait(&in_empty[s], ((k / NIN) & 1) ^ 1);
+            const uint8_t* sk = smem + G::OFF_SK;
+            const uint8_t* lo = smem + G::OFF_LO;
+            auto stage = [&](int k) {          // thread 0 only
                 int f, y0, x0;
                 tile_of(k, f, y0, x0);
+                mbar_expect_tx(stg_full, (a.skip ? G::SKB : 0) + G::LOB);
+                if (a.skip) tma_load_4d(sbase + G::OFF_SK, &tin, 0, x0 - 1, y0 - 1, f, stg_full);
+                tma_load_4d(sbase + G::OFF_LO, &tlo, 0, x0 / 2 - 1, y0 / 2 - 1, f, stg_full);
+            };
+            if (tid == 0 && mytiles > 0) stage(0);
+            for (int k = 0; k < mytiles; ++k) {
+                const int s = k % NIN;
+                int f, y0, x0;
+                tile_of(k, f, y0, x0);
+                const int ly0 = y0 / 2 - 1, lx0 = x0 / 2 - 1;
+                mbar_wait(&in_empty[s], ((k / NIN) & 1) ^ 1);
+                mbar_wait(stg_full, k & 1);
                 uint8_t* in = smem + s * G::INB;
-                const T* xlf = xf + (int64_t)f * hl * wl * CIN;
-                for (int i = tid; i < G::NPI * G::NCI; i += NPT) {
+                for (int i = tid; i < ((a.dbg & 1) ? 0 : G::NPI * G::NCI); i += NPT) {
                     const int c = i % G::NCI, p = i / G::NCI;
                     const int ti = p / G::IC, tj = p - ti * G::IC;
                     const int yy = y0 - 1 + ti, xx = x0 - 1 + tj;
                     uint4 q = make_uint4(0u, 0u, 0u, 0u);
                     if (yy >= 0 && xx >= 0 && yy < a.H && xx < a.W) {
-                        float v[8];
-                        up2_chunk<T>(xlf, hl, wl, CIN, yy, xx, c, v);
-                        if (a.skip) {
-                            const uint4 sk = __ldg(reinterpret_cast<const uint4*>(
-                                reinterpret_cast<const T*>(a.skip) + (((int64_t)f * a.H + yy) * a.W + xx) * CIN + c * 8));
-                            const uint32_t* sp = &sk.x;
+                        const float sy = fminf(fmaxf((yy + 0.5f) * 0.5f - 0.5f, 0.f), (float)(hl - 1));
+                        const float sx = fminf(fmaxf((xx + 0.5f) * 0.5f - 0.5f, 0.f), (float)(wl - 1));
+                        const int r0 = (int)sy, c0 = (int)sx;
+                        const int r1 = min(r0 + 1, hl - 1), c1 = min(c0 + 1, wl - 1);
+                        const float wy = sy - r0, wx = sx - c0;
+                        auto ld = [&](int r, int cc) {
+                            return *reinterpret_cast<const uint4*>(lo + (((r - ly0) * G::LC + (cc - lx0)) * CIN + c * 8) * 2);
+                        };
+                        const uint4 q00 = ld(r0, c0), q10 = ld(r1, c0), q01 = ld(r0, c1), q11 = ld(r1, c1);
+                        uint4 qs = make_uint4(0u, 0u, 0u, 0u);
+                        if (a.skip) qs = *reinterpret_cast<const uint4*>(sk + (p * CIN + c * 8) * 2);
+                        const uint32_t *a00 = &q00.x, *a10 = &q10.x, *a01 = &q01.x, *a11 = &q11.x, *as = &qs.x;
+                        uint32_t* qo = &q.x;
 #pragma unroll
-                            for (int e = 0; e < 4; ++e) {
-                                const float2 sv = Elem<T>::unpack(sp[e]);
-                                v[2 * e] += sv.x;
-                                v[2 * e + 1] += sv.y;
-                            }
+                        for (int e = 0; e < 4; ++e) {
+                            const float2 p00 = Elem<T>::unpack(a00[e]), p10 = Elem<T>::unpack(a10[e]);
+                            const float2 p01 = Elem<T>::unpack(a01[e]), p11 = Elem<T>::unpack(a11[e]);
+                            const float2 ps = Elem<T>::unpack(as[e]);
+                            const float c0x = p00.x * (1.f - wy) + p10.x * wy, c1x = p01.x * (1.f - wy) + p11.x * wy;
+                            const float c0y = p00.y * (1.f - wy) + p10.y * wy, c1y = p01.y * (1.f - wy) + p11.y * wy;
+                            qo[e] = Elem<T>::pack(c0x * (1.f - wx) + c1x * wx + ps.x, c0y * (1.f - wx) + c1y * wx + ps.y);
                         }
-                        q.x = Elem<T>::pack(v[0], v[1]);
-                        q.y = Elem<T>::pack(v[2], v[3]);
-                        q.z = Elem<T>::pack(v[4], v[5]);
-                        q.w = Elem<T>::pack(v[6], v[7]);
                     }
                     *reinterpret_cast<uint4*>(in + c * G::PIN + p * 16) = q;
                 }
                 fence_proxy_async();
                 mbar_arrive(&in_full[s]);
+                nbar_sync(1, NPT);                 // all producers done with the staging tiles
+                if (tid == 0 && k + 1 < mytiles) stage(k + 1);
             }
         }
     } else if (warp == MW) {
@@ -958,7 +1011,7 @@ __global__ void __launch_bounds__((NPW + 5) * 32, 1) level_kernel(const __grid_c
                 tc_fence_after();
                 const uint32_t in = sbase + s * G::INB;
 #pragma unroll 1
-                for (int tap = 0; tap < 9; ++tap) {
+                for (int tap = 0; tap < ((a.dbg & 4) ? 0 : 9); ++tap) {
                     const int dy = tap / 3, dx = tap % 3;
 #pragma unroll
                     for (int b = 0; b < NB; ++b)
@@ -980,6 +1033,7 @@ __global__ void __launch_bounds__((NPW + 5) * 32, 1) level_kernel(const __grid_c
     } else {
         // ------------------------------------------------------------ epilogue
         const int q = warp & 3;                      // TMEM lane quadrant of this warp
+        const int grp = (warp - EW0) >> 2;           // two warps per quadrant split the columns
         const int m = q * 32 + lane;                 // M row == TMEM lane
         const int pi = m >> 3, pj = m & 7;           // pixel row / column inside an M-block
         const uint32_t tl = (uint32_t)(q * 32) << 16;
@@ -990,9 +1044,9 @@ __global__ void __launch_bounds__((NPW + 5) * 32, 1) level_kernel(const __grid_c
             tc_fence_after();
             uint8_t* mid = smem + G::OFF_MID + mm * G::MIDB;
 #pragma unroll 1
-            for (int b = 0; b < NB; ++b) {
-#pragma unroll
-                for (int c0 = 0; c0 < C3; c0 += 16) {
+            for (int it = grp; it < ((a.dbg & 2) ? 0 : NB * (C3 / 16)); it += 2) {
+                const int b = it / (C3 / 16), c0 = (it % (C3 / 16)) * 16;
+                {
                     float v[16];
                     tmem_ld16(tmem + tl + G::ACC3 + (a3 * NB + b) * C3 + c0, v);
                     uint4 qv[2];
@@ -1019,11 +1073,11 @@ __global__ void __launch_bounds__((NPW + 5) * 32, 1) level_kernel(const __grid_c
             tc_fence_after();
             const int oy = y0 + pi;
 #pragma unroll 1
-            for (int b = 0; b < NB; ++b) {
+            for (int it = grp; it < ((a.dbg & 2) ? 0 : NB * (C1 / 16)); it += 2) {
+                const int b = it / (C1 / 16), c0 = (it % (C1 / 16)) * 16;
                 const int ox = x0 + b * 8 + pj;
                 const bool inside = oy < a.H && ox < a.W;
-#pragma unroll
-                for (int c0 = 0; c0 < C1; c0 += 16) {
+                {
                     float v[16];
                     tmem_ld16(tmem + tl + G::ACC1 + (a1 * NB + b) * C1 + c0, v);
 #pragma unroll
@@ -1041,21 +1095,31 @@ __global__ void __launch_bounds__((NPW + 5) * 32, 1) level_kernel(const __grid_c
                         }
                     }
                     if (DST & DST_POOL) {
+                        // 2x2 average pool as a transposing reduction: the x-partner
+                        // (lane^1) and y-partner (lane^8) each take half of the
+                        // channels, 12 shuffles instead of 32; every thread of the
+                        // 2x2 group then owns 4 channels of the pooled pixel.
+                        const bool xo = pj & 1, yo = pi & 1;
+                        float h8[8], h4[4];
 #pragma unroll
-                        for (int e = 0; e < 16; ++e) {
-                            v[e] += __shfl_xor_sync(0xffffffffu, v[e], 1);
-                            v[e] += __shfl_xor_sync(0xffffffffu, v[e], 8);
+                        for (int e = 0; e < 8; ++e) {
+                            const float send = xo ? v[e] : v[e + 8];
+                            const float keep = xo ? v[e + 8] : v[e];
+                            h8[e] = keep + __shfl_xor_sync(0xffffffffu, send, 1);
                         }
-                        if (!(pi & 1) && !(pj & 1) && inside) {
-                            uint4 qv[2];
-                            uint32_t* qp = &qv[0].x;
 #pragma unroll
-                            for (int e = 0; e < 8; ++e) qp[e] = Elem<T>::pack(v[2 * e] * 0.25f, v[2 * e + 1] * 0.25f);
+                        for (int e = 0; e < 4; ++e) {
+                            const float send = yo ? h8[e] : h8[e + 4];
+                            const float keep = yo ? h8[e + 4] : h8[e];
+                            h4[e] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
+                        }
+                        if (inside) {
                             const int H2 = a.H / 2, W2 = a.W / 2;
-                            uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<T*>(a.pool) +
-                                                                  (((int64_t)f * H2 + oy / 2) * W2 + ox / 2) * C1 + c0);
-                            dst[0] = qv[0];
-                            dst[1] = qv[1];
+                            const int cb = c0 + (xo ? 8 : 0) + (yo ? 4 : 0);
+                            uint2 qv = make_uint2(Elem<T>::pack(h4[0] * 0.25f, h4[1] * 0.25f),
+                                                  Elem<T>::pack(h4[2] * 0.25f, h4[3] * 0.25f));
+                            *reinterpret_cast<uint2*>(reinterpret_cast<T*>(a.pool) +
+                                                      (((int64_t)f * H2 + oy / 2) * W2 + ox / 2) * C1 + cb) = qv;
                         }
                     }
                 }
@@ -1115,9 +1179,24 @@ bool encode_nhwc_map(const void* base, bool bf16, int C, int H, int W, int nf, i
                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+// 4-D pixel-major view (C elems, x, y, frame) of an NHWC 16-bit tensor.
+bool encode_nhwc_map4(const void* base, bool bf16, int C, int H, int W, int nf, int box_w, int box_h,
+                      CUtensorMap* m) {
+    auto enc = tensor_map_encoder();
+    if (!enc || ((uintptr_t)base % 16)) return false;
+    const cuuint64_t dims[4] = {(cuuint64_t)C, (cuuint64_t)W, (cuuint64_t)H, (cuuint64_t)nf};
+    const cuuint64_t strides[3] = {(cuuint64_t)C * 2, (cuuint64_t)W * C * 2, (cuuint64_t)H * W * C * 2};
+    const cuuint32_t box[4] = {(cuuint32_t)C, (cuuint32_t)box_w, (cuuint32_t)box_h, 1};
+    const cuuint32_t es[4] = {1, 1, 1, 1};
+    return enc(m, bf16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 4,
+               const_cast<void*>(base), dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+               CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 template <typename T, int CIN, int C3, int C1, int SRC, int DST, int NB, int NIN, int NMID>
 nsm_status launch_level(const LevelArgs& a, int nf, cudaStream_t st, const char* name) {
-    using G = LvGeom<CIN, C3, C1, NB, NIN, NMID>;
+    using G = LvGeom<CIN, C3, C1, NB, NIN, NMID, SRC == SRC_UP>;
     constexpr int NPW = SRC == SRC_TENSOR ? 1 : 8;
     auto k = level_kernel<T, CIN, C3, C1, SRC, DST, NB, NIN, NMID, NPW>;
     static bool attr = false;
@@ -1125,21 +1204,30 @@ nsm_status launch_level(const LevelArgs& a, int nf, cudaStream_t st, const char*
         cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, G::SMEM);
         attr = true;
     }
-    CUtensorMap tin;
+    CUtensorMap tin, tlo;
     memset(&tin, 0, sizeof tin);
-    if (SRC == SRC_TENSOR &&
-        !encode_nhwc_map(a.x, std::is_same<T, __nv_bfloat16>::value, CIN, a.H, a.W, nf, G::IC, G::IR, &tin))
-        return fail(NSM_ERR_CUDA, "%s: TMA tensor map encoding failed", name);
+    memset(&tlo, 0, sizeof tlo);
+    constexpr bool bf = std::is_same<T, __nv_bfloat16>::value;
+    bool ok = true;
+    if (SRC == SRC_TENSOR) {
+        ok = encode_nhwc_map(a.x, bf, CIN, a.H, a.W, nf, G::IC, G::IR, &tin);
+    } else {
+        ok = encode_nhwc_map4(a.x, bf, CIN, a.H / 2, a.W / 2, nf, G::LC, G::LR, &tlo);
+        if (a.skip) ok = ok && encode_nhwc_map4(a.skip, bf, CIN, a.H, a.W, nf, G::IC, G::IR, &tin);
+    }
+    if (!ok) return fail(NSM_ERR_CUDA, "%s: TMA tensor map encoding failed", name);
     const int total = ((a.W + G::TW - 1) / G::TW) * ((a.H + G::TH - 1) / G::TH) * nf;
     const int grid = std::min(total, num_sms());      // TMEM: 512 columns -> one CTA per SM
+    static const int dbg = getenv("NSM_LEVEL_DBG") ? atoi(getenv("NSM_LEVEL_DBG")) : 0;
+    const_cast<LevelArgs&>(a).dbg = dbg;
     NSM_PROF(name, st);
-    k<<<grid, (NPW + 5) * 32, G::SMEM, st>>>(a, tin, total);
+    k<<<grid, (NPW + 9) * 32, G::SMEM, st>>>(a, tin, tlo, total);
     return NSM_OK;
 }
 
 struct Bufs {
     void *p1, *s1, *p2, *s2, *p3, *b3, *d2, *d1;
-    float4* y;
+    float* y;
     size_t bytes;
 };
 
@@ -1160,7 +1248,7 @@ Bufs carve(void* ws, int nf, int H0, int W0, int es) {
     b.b3 = take((size_t)nf * H3 * W3 * 64 * es);
     b.d2 = take((size_t)nf * H2 * W2 * 32 * es);
     b.d1 = take((size_t)nf * H1 * W1 * 16 * es);
-    b.y = (float4*)take((size_t)nf * H0 * W0 * 16);
+    b.y = (float*)take((size_t)nf * H0 * W0 * 16);
     b.bytes = (size_t)(p - (char*)ws);
     return b;
 }
@@ -1186,7 +1274,7 @@ nsm_status run_levels(const Plan& p, const Bufs& b, int nf, int H0, int W0, cuda
     if (s != NSM_OK) return s;
     // l2 decoder: up(B3) + S2 -> 64 -> D2 (32)
     a = LevelArgs{b.b3, b.s2, H2, W2, L2.dec3.wpk, L2.dec3.b32, L2.dec1.wpk, L2.dec1.b32, b.d2, nullptr};
-    s = launch_level<T, 64, 64, 32, SRC_UP, DST_STORE, 2, 2, 2>(a, nf, st, "lv2_dec");
+    s = launch_level<T, 64, 64, 32, SRC_UP, DST_STORE, 2, 1, 1>(a, nf, st, "lv2_dec");
     if (s != NSM_OK) return s;
     // l1 decoder: up(D2) + S1 -> 32 -> D1 (16)
     a = LevelArgs{b.d2, b.s1, H1, W1, L1.dec3.wpk, L1.dec3.b32, L1.dec1.wpk, L1.dec1.b32, b.d1, nullptr};
@@ -1271,7 +1359,7 @@ bool f16_supported(const Plan& p) {
 
 size_t infer_f16_workspace(const Plan& p, int n, int h, int w) {
     const int Hp = round16(h), Wp = round16(w);
-    const int nf = std::min(n, kChunkFrames);
+    const int nf = std::min(n, chunk_frames());
     return carve(nullptr, nf, Hp / 2, Wp / 2, 2).bytes + 1024;
 }
 
@@ -1331,12 +1419,12 @@ nsm_status infer_f16(const Plan& p, const nsm_gbuffer* g, const float* sm, int64
     if (g->z_f || g->c_e || g->c_c || g->coverage)
         return fail(NSM_ERR_UNSUPPORTED, "16-bit path derives z_f/c_e/c_c from the planes");
     const int Hp = round16(h), Wp = round16(w), H0 = Hp / 2, W0 = Wp / 2;
-    const int nfmax = std::min(n, kChunkFrames);
+    const int nfmax = std::min(n, chunk_frames());
     Bufs b = carve(ws, nfmax, H0, W0, 2);
     if (ws_bytes < b.bytes) return fail(NSM_ERR_ARG, "workspace too small (%zu < %zu)", ws_bytes, b.bytes);
     launch_fill_i64(first_bad, n, INT64_MAX, st);
-    for (int f0 = 0; f0 < n; f0 += kChunkFrames) {
-        const int nf = std::min(kChunkFrames, n - f0);
+    for (int f0 = 0; f0 < n; f0 += chunk_frames()) {
+        const int nf = std::min(chunk_frames(), n - f0);
         Enc0Args e{};
         e.g = GBufK{(const float*)g->d + (int64_t)f0 * g->frame_stride,
                     (const float*)g->normal + (int64_t)f0 * 3 * g->frame_stride,
@@ -1372,11 +1460,11 @@ nsm_status forward_f16(const Plan& p, const float* x, int n, int h, int w, float
                        size_t ws_bytes, cudaStream_t st) {
     if (!f16_supported(p)) return fail(NSM_ERR_UNSUPPORTED, "no 16-bit kernels for this NetworkConfig");
     const int H0 = h / 2, W0 = w / 2;
-    const int nfmax = std::min(n, kChunkFrames);
+    const int nfmax = std::min(n, chunk_frames());
     Bufs b = carve(ws, nfmax, H0, W0, 2);
     if (ws_bytes < b.bytes) return fail(NSM_ERR_ARG, "workspace too small");
-    for (int f0 = 0; f0 < n; f0 += kChunkFrames) {
-        const int nf = std::min(kChunkFrames, n - f0);
+    for (int f0 = 0; f0 < n; f0 += chunk_frames()) {
+        const int nf = std::min(chunk_frames(), n - f0);
         Enc0Args e{};
         e.x = x + (int64_t)f0 * 4 * h * w;
         e.h = h;
