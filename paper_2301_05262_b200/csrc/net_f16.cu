@@ -626,28 +626,78 @@ __device__ __forceinline__ void up2_chunk(const T* x, int hl, int wl, int C, int
     }
 }
 
+// dec0 source staging: the D1 (level-1, 16 ch) pixels a level-0 tile's
+// up2 reads, (TH/2 + 2) x (TW/2 + 2), pixel-major, double-buffered by TMA.
+constexpr int D0_LR = E0_TH / 2 + 2, D0_LC = E0_TW / 2 + 2;
+constexpr int D0_STG = round128(D0_LR * D0_LC * 32);
+constexpr int DEC0_SMEM = 2 * E0_SMEM + 2 * D0_STG + 32;
+
 template <typename T>
-__global__ void __launch_bounds__(kL0Threads, 1) dec0_kernel(Dec0Args a, int total) {
+__global__ void __launch_bounds__(kL0Threads, 1) dec0_kernel(const __grid_constant__ Dec0Args a,
+                                                             const __grid_constant__ CUtensorMap tm, int total) {
     const int H1 = a.H0 / 2, W1 = a.W0 / 2;
     if (threadIdx.x < kL0Prod) {
-        l0_produce_loop(total, [&](uint8_t* buf, int tile) {
+        extern __shared__ __align__(128) uint8_t smem[];
+        uint8_t* stg = smem + 2 * E0_SMEM;
+        uint64_t* full = reinterpret_cast<uint64_t*>(stg + 2 * D0_STG);
+        const int ptid = threadIdx.x;
+        const int mytiles = (int)blockIdx.x < total ? (total - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x : 0;
+        auto issue = [&](int k) {
+            const L0Tile tl = l0_tile(blockIdx.x + k * gridDim.x, a.H0, a.W0);
+            mbar_expect_tx(&full[k & 1], D0_LR * D0_LC * 32);
+            tma_load_4d(smem_u32(stg + (k & 1) * D0_STG), &tm, 0, tl.tx0 / 2 - 1, tl.ty0 / 2 - 1, tl.f, &full[k & 1]);
+        };
+        if (ptid == 0) {
+            mbar_init(&full[0], 1);
+            mbar_init(&full[1], 1);
+            asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        }
+        nbar_sync(5, kL0Prod);
+        if (ptid == 0) {
+            if (mytiles > 0) issue(0);
+            if (mytiles > 1) issue(1);
+        }
+        for (int k = 0; k < mytiles; ++k) {
+            const L0Tile tl = l0_tile(blockIdx.x + k * gridDim.x, a.H0, a.W0);
+            const int sb = k & 1;
+            if (k >= 2) nbar_sync(3 + sb, kL0Threads);
+            uint8_t* buf = smem + sb * E0_SMEM;
+            mbar_wait(&full[sb], (k >> 1) & 1);
+            const uint8_t* lo = stg + sb * D0_STG;
+            const int ly0 = tl.ty0 / 2 - 1, lx0 = tl.tx0 / 2 - 1;
             // up2(D1) over the halo'd tile (zero outside the frame: conv padding)
-            const L0Tile tl = l0_tile(tile, a.H0, a.W0);
-            const T* xf = reinterpret_cast<const T*>(a.x) + (int64_t)tl.f * H1 * W1 * 16;
-            for (int i = threadIdx.x; i < E0_IR * E0_IC * 2; i += kL0Prod) {
+            for (int i = ptid; i < E0_IR * E0_IC * 2; i += kL0Prod) {
                 const int c = i & 1, p = i >> 1;
                 const int ti = p / E0_IC, tj = p - ti * E0_IC;
                 const int oy = tl.ty0 - 1 + ti, ox = tl.tx0 - 1 + tj;
-                float v[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-                if (oy >= 0 && ox >= 0 && oy < a.H0 && ox < a.W0) up2_chunk<T>(xf, H1, W1, 16, oy, ox, c, v);
-                uint4 q;
-                q.x = Elem<T>::pack(v[0], v[1]);
-                q.y = Elem<T>::pack(v[2], v[3]);
-                q.z = Elem<T>::pack(v[4], v[5]);
-                q.w = Elem<T>::pack(v[6], v[7]);
+                uint4 q = make_uint4(0u, 0u, 0u, 0u);
+                if (oy >= 0 && ox >= 0 && oy < a.H0 && ox < a.W0) {
+                    const float sy = fminf(fmaxf((oy + 0.5f) * 0.5f - 0.5f, 0.f), (float)(H1 - 1));
+                    const float sx = fminf(fmaxf((ox + 0.5f) * 0.5f - 0.5f, 0.f), (float)(W1 - 1));
+                    const int r0 = (int)sy, c0 = (int)sx;
+                    const int r1 = min(r0 + 1, H1 - 1), c1 = min(c0 + 1, W1 - 1);
+                    const float wy = sy - r0, wx = sx - c0;
+                    auto ld = [&](int r, int cc) {
+                        return *reinterpret_cast<const uint4*>(lo + (((r - ly0) * D0_LC + (cc - lx0)) * 16 + c * 8) * 2);
+                    };
+                    const uint4 q00 = ld(r0, c0), q10 = ld(r1, c0), q01 = ld(r0, c1), q11 = ld(r1, c1);
+                    const uint32_t *a00 = &q00.x, *a10 = &q10.x, *a01 = &q01.x, *a11 = &q11.x;
+                    uint32_t* qo = &q.x;
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) {
+                        const float2 p00 = Elem<T>::unpack(a00[e]), p10 = Elem<T>::unpack(a10[e]);
+                        const float2 p01 = Elem<T>::unpack(a01[e]), p11 = Elem<T>::unpack(a11[e]);
+                        const float c0x = p00.x * (1.f - wy) + p10.x * wy, c1x = p01.x * (1.f - wy) + p11.x * wy;
+                        const float c0y = p00.y * (1.f - wy) + p10.y * wy, c1y = p01.y * (1.f - wy) + p11.y * wy;
+                        qo[e] = Elem<T>::pack(c0x * (1.f - wx) + c1x * wx, c0y * (1.f - wx) + c1y * wx);
+                    }
+                }
                 *reinterpret_cast<uint4*>(buf + c * E0_PLANE + p * 16) = q;
             }
-        });
+            nbar_sync(5, kL0Prod);                 // everyone is done with stage sb
+            if (ptid == 0 && k + 2 < mytiles) issue(k + 2);
+            nbar_arrive(1 + sb, kL0Threads);
+        }
         return;
     }
     const int cw = (threadIdx.x - kL0Prod) >> 5;
@@ -1319,7 +1369,7 @@ nsm_status run_l0(const Plan& p, const Bufs& b, const Enc0Args& e0, const GbufMa
         cudaFuncSetAttribute(enc0_kernel<T, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * E0_SMEM);
         cudaFuncSetAttribute(enc0_kernel<T, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * E0_SMEM);
         cudaFuncSetAttribute(enc0_kernel<T, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, ENC0_SMEM_TMA);
-        cudaFuncSetAttribute(dec0_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * E0_SMEM);
+        cudaFuncSetAttribute(dec0_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, DEC0_SMEM);
         attr = true;
     }
     const int total = ((W0 + E0_TW - 1) / E0_TW) * ((H0 + E0_TH - 1) / E0_TH) * nf;
@@ -1336,8 +1386,12 @@ nsm_status run_l0(const Plan& p, const Bufs& b, const Enc0Args& e0, const GbufMa
     Dec0Args d{b.d1, H0, W0, (const uint2*)L0.dec3.wpk, (const uint2*)L0.dec1.wpk,
                (const uint2*)p.head.wpk, L0.dec3.b32, L0.dec1.b32, p.head.b32, b.y};
     {
+        CUtensorMap dm;
+        memset(&dm, 0, sizeof dm);
+        if (!encode_nhwc_map4(b.d1, std::is_same<T, __nv_bfloat16>::value, 16, H0 / 2, W0 / 2, nf, D0_LC, D0_LR, &dm))
+            return fail(NSM_ERR_CUDA, "dec0: TMA tensor map encoding failed");
         NSM_PROF("dec0_fused", st);
-        dec0_kernel<T><<<pgrid, kL0Threads, 2 * E0_SMEM, st>>>(d, total);
+        dec0_kernel<T><<<pgrid, kL0Threads, DEC0_SMEM, st>>>(d, dm, total);
     }
     {
         dim3 g2((W0 + 127) / 128, H0, nf);
