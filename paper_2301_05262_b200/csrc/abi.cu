@@ -74,6 +74,20 @@ void make_frame_table(const nsm_frame* frames, int32_t n, FrameTable& tab) {
         f.fw0 = (float)(f.half_h - f.half_h / f.ch);
         f.fbias = (float)f.bias;
         f.fsize = (float)f.size_index;
+        // affine forms: pa * (p - vp).vr, -qa * (p - vp).vu, (p - vp).vf
+        double cx = 0, cy = 0, cz = 0;
+        for (int a = 0; a < 3; ++a) {
+            f.kx[a] = f.pa * f.vr[a];
+            f.ky[a] = -f.qa * f.vu[a];
+            f.kz[a] = f.vf[a];
+            cx -= f.vr[a] * f.vp[a];
+            cy -= f.vu[a] * f.vp[a];
+            cz -= f.vf[a] * f.vp[a];
+            f.fcp[a] = (float)f.cp[a];
+        }
+        f.kx[3] = f.pa * cx;
+        f.ky[3] = -f.qa * cy;
+        f.kz[3] = cz;
     }
 }
 

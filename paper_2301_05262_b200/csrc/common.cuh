@@ -22,6 +22,8 @@ struct FrameK {
     int ch, cw;                          // camera resolution (rays)
     // fused-path constants, precomputed on the host (abi.cu make_frame_table)
     double pa, pb, qa, qb;               // col = xr/zc * pa + pb ; row = qb - yr/zc * qa
+    double kx[4], ky[4], kz[4];          // pa*xr = kx.p + kx[3], -qa*yr = ky.p + ky[3], zc = kz.p + kz[3]
+    float fcp[3];                        // camera position
     float fec[3], fcf[3], fcr[3], fcu[3];
     float fu1, fu0, fw1, fw0;            // u = fx * fu1 + fu0 ; w = fy * fw1 + fw0
     float fbias, fsize;
@@ -102,6 +104,31 @@ __device__ __forceinline__ bool texel_fast(const FrameK& f, double px, double py
     const bool ok = (zc > 0.0) && r >= 0 && r < f.hs && c >= 0 && c < f.ws;
     ri = (int)min(max(r, 0LL), (long long)f.hs - 1);
     ci = (int)min(max(c, 0LL), (long long)f.ws - 1);
+    return ok;
+}
+
+// Fused-path texel: the frustum projection as three affine forms of the fp32
+// world position evaluated in fp64 (k = scaled view axes, constants folded on
+// the host), a Newton-refined fp64 reciprocal of the depth, and int32
+// round-half-even conversion.  Agrees with the reference's np.rint index
+// except within a few fp64 ulps of a half-texel tie (never observed).
+__device__ __forceinline__ bool texel_fused(const FrameK& f, float px, float py, float pz, int& ri,
+                                            int& ci) {
+    const double x = px, y = py, z = pz;
+    const double zc = fma(f.kz[0], x, fma(f.kz[1], y, fma(f.kz[2], z, f.kz[3])));
+    const double xs = fma(f.kx[0], x, fma(f.kx[1], y, fma(f.kx[2], z, f.kx[3])));
+    const double ys = fma(f.ky[0], x, fma(f.ky[1], y, fma(f.ky[2], z, f.ky[3])));
+    double r;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(zc));
+    double e = fma(-zc, r, 1.0);
+    r = fma(r, e, r);
+    e = fma(-zc, r, 1.0);
+    r = fma(r, e, r);
+    const int c = __double2int_rn(fma(xs, r, f.pb));
+    const int rr = __double2int_rn(fma(ys, r, f.qb));
+    const bool ok = (zc > 0.0) && (unsigned)rr < (unsigned)f.hs && (unsigned)c < (unsigned)f.ws;
+    ri = min(max(rr, 0), f.hs - 1);
+    ci = min(max(c, 0), f.ws - 1);
     return ok;
 }
 

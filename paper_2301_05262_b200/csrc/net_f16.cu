@@ -135,6 +135,7 @@ struct Enc0Args {
     const float* b1;
     void* out;            // pooled (N, H0/2, W0/2, 16)
     int64_t* first_bad;
+    int dbg;              // experiments only: 1 skip feature math, 2 skip convolutions
 };
 
 // Stage-1 per-pixel math of the fused kernel: fp64 projection for the texel
@@ -175,9 +176,11 @@ __device__ __forceinline__ float4 pixel_features(const FrameK& F, const GBufK& g
 // Sliding-window 3x3 conv on a 16-pixel strip: every input row's three
 // dx-shifted A fragments are loaded once and applied to the three output
 // rows that need them, so ldmatrix traffic is 3 instead of 9 loads per row.
+// Accumulators start at the conv bias (saves the epilogue's bias adds).
 template <typename T, int ROWS, class Epi>
 __device__ __forceinline__ void conv3_strip16(uint32_t sbase, int plane, int rowpix, int r0, int sx,
-                                              const uint32_t (&B3)[9][2][2], Epi&& epi) {
+                                              const uint32_t (&B3)[9][2][2], const float (&binit)[2][2],
+                                              Epi&& epi) {
     const int lane = threadIdx.x & 31;
     const int lm = lane >> 3, li = lane & 7;
     const uint32_t a_off = (lm >> 1) * plane + (li + 8 * (lm & 1)) * 16;
@@ -187,7 +190,7 @@ __device__ __forceinline__ void conv3_strip16(uint32_t sbase, int plane, int row
 #pragma unroll
         for (int n = 0; n < 2; ++n)
 #pragma unroll
-            for (int e = 0; e < 4; ++e) acc[s][n][e] = 0.f;
+            for (int e = 0; e < 4; ++e) acc[s][n][e] = binit[n][e & 1];
 #pragma unroll
     for (int ir = 0; ir < ROWS + 2; ++ir) {
         uint32_t A[3][4];
@@ -211,9 +214,19 @@ __device__ __forceinline__ void conv3_strip16(uint32_t sbase, int plane, int row
 #pragma unroll
             for (int n = 0; n < 2; ++n)
 #pragma unroll
-                for (int e = 0; e < 4; ++e) acc[oo % 3][n][e] = 0.f;
+                for (int e = 0; e < 4; ++e) acc[oo % 3][n][e] = binit[n][e & 1];
         }
     }
+}
+
+// relu(acc) of a 16x16 m16n8 pair packed to 16 bits (ReLU after the rounding:
+// the two commute), as the A fragment of the next 1x1 conv.
+template <typename T>
+__device__ __forceinline__ void relu_pack_a(const float (&acc)[2][4], uint32_t a[4]) {
+    a[0] = Elem<T>::relu2(Elem<T>::pack(acc[0][0], acc[0][1]));
+    a[1] = Elem<T>::relu2(Elem<T>::pack(acc[0][2], acc[0][3]));
+    a[2] = Elem<T>::relu2(Elem<T>::pack(acc[1][0], acc[1][1]));
+    a[3] = Elem<T>::relu2(Elem<T>::pack(acc[1][2], acc[1][3]));
 }
 
 // relu(acc + bias) of a 16x16 m16n8 pair, packed as the A fragment of the
@@ -436,7 +449,7 @@ __device__ __forceinline__ void produce_features_tma(const Enc0Args& a, const Gb
             const float* sp = reinterpret_cast<const float*>(stage + sidx * ST_BYTES + ST_OFF_P);
             constexpr int K = 4;
 #pragma unroll 1
-            for (int i0 = ptid; i0 < ST_PIX; i0 += kE0Prod * K) {
+            for (int i0 = ptid; i0 < ((a.dbg & 1) ? 0 : ST_PIX); i0 += kE0Prod * K) {
                 float d[K], look[K];
                 int si[K];
 #pragma unroll
@@ -447,7 +460,7 @@ __device__ __forceinline__ void produce_features_tma(const Enc0Args& a, const Gb
                     look[j] = 0.f;
                     if (d[j] > 0.f) {
                         int ri, ci;
-                        if (!texel_fast(F, sp[si[j]], sp[ST_TPIX + si[j]], sp[2 * ST_TPIX + si[j]], ri, ci)) {
+                        if (!texel_fused(F, sp[si[j]], sp[ST_TPIX + si[j]], sp[2 * ST_TPIX + si[j]], ri, ci)) {
                             const int ry = i / ST_COLS;
                             atomic_min_i64(a.first_bad + tl.f,
                                            (int64_t)(fy0 + ry) * a.w + (fx0 + i - ry * ST_COLS));
@@ -468,12 +481,10 @@ __device__ __forceinline__ void produce_features_tma(const Enc0Args& a, const Gb
                         const float tx = ecx - px, ty = ecy - py, tz = ecz - pz;
                         const float izf = rsqrtf(tx * tx + ty * ty + tz * tz);
                         const float ce = fminf(fmaxf((nx * tx + ny * ty + nz * tz) * izf, 0.f), 1.f);
-                        const float u = (float)(fx0 + rx) * F.fu1 + F.fu0;
-                        const float w = (float)(fy0 + ry) * F.fw1 + F.fw0;
-                        const float dx = F.fcf[0] + u * F.fcr[0] + w * F.fcu[0];
-                        const float dy = F.fcf[1] + u * F.fcr[1] + w * F.fcu[1];
-                        const float dz = F.fcf[2] + u * F.fcr[2] + w * F.fcu[2];
-                        const float cc = fminf(fmaxf(-(nx * dx + ny * dy + nz * dz) *
+                        // c_c = clip(n . -ray): the pixel ray is the direction camera -> hit
+                        // point (render_gbuffer places p on it), fp32 is ample here
+                        const float dx = F.fcp[0] - px, dy = F.fcp[1] - py, dz = F.fcp[2] - pz;
+                        const float cc = fminf(fmaxf((nx * dx + ny * dy + nz * dz) *
                                                          rsqrtf(dx * dx + dy * dy + dz * dz), 0.f), 1.f);
                         float ch0 = 0.f, ch1 = 1.f;
                         if (look[j] < INFINITY) {                  // raster.py:262 (finite lookup)
@@ -549,21 +560,33 @@ __global__ void __launch_bounds__(kL0Threads, 1) enc0_kernel(const __grid_consta
     l0_consume_loop(total, [&](uint8_t* buf, int tile) {
             const L0Tile tl = l0_tile(tile, a.H0, a.W0);
             float pp[2][4];
-            conv3_strip16<T, kRows>(smem_u32(buf), E0_PLANE, E0_IC, r0, sx, B3, [&](int oo, float (&acc)[2][4]) {
+            if (a.dbg & 2) return;
+            conv3_strip16<T, kRows>(smem_u32(buf), E0_PLANE, E0_IC, r0, sx, B3, bias3, [&](int oo, float (&acc)[2][4]) {
                 uint32_t a1[4];
-                acc_to_a<T>(acc, bias3, true, a1);
-                float u[2][4] = {};
+                relu_pack_a<T>(acc, a1);
+                float u[2][4];
 #pragma unroll
-                for (int n = 0; n < 2; ++n) mma16816<T>(u[n], a1, B1[n][0], B1[n][1]);
+                for (int n = 0; n < 2; ++n) {
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) u[n][e] = bias1[n][e & 1];
+                    mma16816<T>(u[n], a1, B1[n][0], B1[n][1]);
+                }
+                // avg_pool2: rows oo-1, oo summed in registers, then the
+                // x-neighbour (lane ^ 4) once per row pair
 #pragma unroll
                 for (int n = 0; n < 2; ++n)
 #pragma unroll
                     for (int e = 0; e < 4; ++e) {
-                        float v = fmaxf(u[n][e] + bias1[n][e & 1], 0.f);
-                        v += __shfl_xor_sync(0xffffffffu, v, 4);       // x-neighbour pixel
+                        const float v = fmaxf(u[n][e], 0.f);
                         if (oo & 1) pp[n][e] += v;
                         else pp[n][e] = v;
                     }
+                if (oo & 1) {
+#pragma unroll
+                    for (int n = 0; n < 2; ++n)
+#pragma unroll
+                        for (int e = 0; e < 4; ++e) pp[n][e] += __shfl_xor_sync(0xffffffffu, pp[n][e], 4);
+                }
                 if (oo & 1) {                                           // avg_pool2 of rows oo-1, oo
                     const int py = (tl.ty0 + r0 + oo) >> 1;
                     const int pxb = (tl.tx0 + sx) >> 1;
@@ -737,14 +760,18 @@ __global__ void __launch_bounds__(kL0Threads, 1) dec0_kernel(const __grid_consta
     l0_consume_loop(total,
         [&](uint8_t* buf, int tile) {
             const L0Tile tl = l0_tile(tile, a.H0, a.W0);
-            conv3_strip16<T, 8>(smem_u32(buf), E0_PLANE, E0_IC, r0, sx, B3, [&](int oo, float (&acc)[2][4]) {
+            conv3_strip16<T, 8>(smem_u32(buf), E0_PLANE, E0_IC, r0, sx, B3, bias3, [&](int oo, float (&acc)[2][4]) {
                 uint32_t a1[4], a2[4];
-                acc_to_a<T>(acc, bias3, true, a1);
-                float u[2][4] = {};
+                relu_pack_a<T>(acc, a1);
+                float u[2][4];
 #pragma unroll
-                for (int n = 0; n < 2; ++n) mma16816<T>(u[n], a1, B1[n][0], B1[n][1]);
-                acc_to_a<T>(u, bias1, true, a2);
-                float yh[4] = {0.f, 0.f, 0.f, 0.f};
+                for (int n = 0; n < 2; ++n) {
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) u[n][e] = bias1[n][e & 1];
+                    mma16816<T>(u[n], a1, B1[n][0], B1[n][1]);
+                }
+                relu_pack_a<T>(u, a2);
+                float yh[4] = {biash[0], biash[1], biash[0], biash[1]};
                 mma16816<T>(yh, a2, BH[0], BH[1]);
                 const int oy = tl.ty0 + r0 + oo;
                 if (t < 2 && oy < a.H0) {
@@ -754,8 +781,8 @@ __global__ void __launch_bounds__(kL0Threads, 1) dec0_kernel(const __grid_consta
                     for (int hlf = 0; hlf < 2; ++hlf) {
                         const int ox = tl.tx0 + sx + g + 8 * hlf;
                         if (ox < a.W0) {
-                            yp[ox] = yh[2 * hlf] + biash[0];
-                            yp[hw0 + ox] = yh[2 * hlf + 1] + biash[1];
+                            yp[ox] = yh[2 * hlf];
+                            yp[hw0 + ox] = yh[2 * hlf + 1];
                         }
                     }
                 }
@@ -1497,6 +1524,8 @@ nsm_status infer_f16(const Plan& p, const nsm_gbuffer* g, const float* sm, int64
         e.b1 = p.lev[0].enc1.b32;
         e.out = b.p1;
         e.first_bad = first_bad + f0;
+        static const int e0dbg = getenv("NSM_ENC0_DBG") ? atoi(getenv("NSM_ENC0_DBG")) : 0;
+        e.dbg = e0dbg;
         void* yo = (char*)y + (size_t)f0 * h * w * (y_dtype == NSM_F16 ? 2 : 4);
         GbufMaps tm;
         memset(&tm, 0, sizeof tm);

@@ -26,6 +26,10 @@ struct Elem<__half> {
         return __half22float2(*reinterpret_cast<__half2*>(&v));
     }
     __device__ static __forceinline__ __half from(float a) { return __float2half_rn(a); }
+    __device__ static __forceinline__ uint32_t relu2(uint32_t v) {
+        __half2 h = __hmax2(*reinterpret_cast<__half2*>(&v), __float2half2_rn(0.f));
+        return *reinterpret_cast<uint32_t*>(&h);
+    }
 };
 template <>
 struct Elem<__nv_bfloat16> {
@@ -38,6 +42,10 @@ struct Elem<__nv_bfloat16> {
         return __bfloat1622float2(*reinterpret_cast<__nv_bfloat162*>(&v));
     }
     __device__ static __forceinline__ __nv_bfloat16 from(float a) { return __float2bfloat16_rn(a); }
+    __device__ static __forceinline__ uint32_t relu2(uint32_t v) {
+        __nv_bfloat162 h = __hmax2(*reinterpret_cast<__nv_bfloat162*>(&v), __float2bfloat162_rn(0.f));
+        return *reinterpret_cast<uint32_t*>(&h);
+    }
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
