@@ -274,16 +274,16 @@ __device__ __forceinline__ void l0_produce_loop(int total, Produce&& produce) { 
     }
 }
 
-template <class Consume>
+template <int NT = kL0Threads, class Consume>
 __device__ __forceinline__ void l0_consume_loop(int total, Consume&& consume) {
     extern __shared__ __align__(128) uint8_t smem[];
     for (int k = 0;; ++k) {
         const int tile = blockIdx.x + k * gridDim.x;
         if (tile >= total) break;
         const int s = k & 1;
-        nbar_sync(1 + s, kL0Threads);
+        nbar_sync(1 + s, NT);
         consume(smem + s * E0_SMEM, tile);
-        if (tile + 2 * (int)gridDim.x < total) nbar_arrive(3 + s, kL0Threads);
+        if (tile + 2 * (int)gridDim.x < total) nbar_arrive(3 + s, NT);
     }
 }
 
@@ -402,7 +402,10 @@ __device__ __forceinline__ void produce_features(const Enc0Args& a, uint8_t* buf
 // TMA producer: one elected thread streams half-tiles of the seven G-buffer
 // planes into two SMEM stages (mbarrier complete_tx); the producer warps turn
 // each staged half into features while the next half is in flight.
-constexpr int kE0Prod = 384;   // 12 producer warps, 4 tensor-core warps
+// 16 producer warps (features) + 4 tensor-core warps; setmaxnreg moves the
+// register budget from the producers (96 -> 88) to the MMA warps (96 -> 128);
+// .inc can only claim what .dec released within the CTA (more deadlocks).
+constexpr int kE0Prod = 512, kE0Threads = 640;
 
 template <typename T>
 __device__ __forceinline__ void produce_features_tma(const Enc0Args& a, const GbufMaps& tm, int total) {
@@ -434,7 +437,7 @@ __device__ __forceinline__ void produce_features_tma(const Enc0Args& a, const Gb
     for (int k = 0; k < mytiles; ++k) {
         const L0Tile tl = l0_tile(blockIdx.x + k * gridDim.x, a.H0, a.W0);
         const int sb = k & 1;
-        if (k >= 2) nbar_sync(3 + sb, kL0Threads);
+        if (k >= 2) nbar_sync(3 + sb, kE0Threads);
         uint8_t* buf = smem + sb * E0_SMEM;
         const FrameK& F = a.tab.f[tl.f];
         const float* smf = a.sm + tl.f * a.sm_stride;
@@ -447,7 +450,7 @@ __device__ __forceinline__ void produce_features_tma(const Enc0Args& a, const Gb
             const float* sd = reinterpret_cast<const float*>(stage + sidx * ST_BYTES);
             const float* sn = reinterpret_cast<const float*>(stage + sidx * ST_BYTES + ST_OFF_N);
             const float* sp = reinterpret_cast<const float*>(stage + sidx * ST_BYTES + ST_OFF_P);
-            constexpr int K = 4;
+            constexpr int K = 5;
 #pragma unroll 1
             for (int i0 = ptid; i0 < ((a.dbg & 1) ? 0 : ST_PIX); i0 += kE0Prod * K) {
                 float d[K], look[K];
@@ -507,14 +510,19 @@ __device__ __forceinline__ void produce_features_tma(const Enc0Args& a, const Gb
                 issue(q + 2);
             }
         }
-        nbar_arrive(1 + sb, kL0Threads);
+        nbar_arrive(1 + sb, kE0Threads);
     }
 }
 
 template <typename T, int kSrc>   // kSrc: 0 = features planes, 1 = G-buffer (LDG), 2 = G-buffer (TMA)
-__global__ void __launch_bounds__(kL0Threads, 1) enc0_kernel(const __grid_constant__ Enc0Args a,
-                                                             const __grid_constant__ GbufMaps tm, int total) {
+__global__ void __launch_bounds__(kSrc == 2 ? kE0Threads : kL0Threads, 1) enc0_kernel(
+    const __grid_constant__ Enc0Args a, const __grid_constant__ GbufMaps tm, int total) {
     constexpr int kProd = kSrc == 2 ? kE0Prod : kL0Prod;
+    constexpr int kThreads = kSrc == 2 ? kE0Threads : kL0Threads;
+    if (kSrc == 2) {
+        if (threadIdx.x < kProd) asm volatile("setmaxnreg.dec.sync.aligned.u32 88;");
+        else asm volatile("setmaxnreg.inc.sync.aligned.u32 128;");
+    }
     constexpr int kRows = kSrc == 2 ? 16 : 8;        // output rows per consumer warp
     if (threadIdx.x < kProd) {
         if (kSrc == 2) {
@@ -557,7 +565,7 @@ __global__ void __launch_bounds__(kL0Threads, 1) enc0_kernel(const __grid_consta
             }
     }
     T* out = reinterpret_cast<T*>(a.out);
-    l0_consume_loop(total, [&](uint8_t* buf, int tile) {
+    l0_consume_loop<kThreads>(total, [&](uint8_t* buf, int tile) {
             const L0Tile tl = l0_tile(tile, a.H0, a.W0);
             float pp[2][4];
             if (a.dbg & 2) return;
@@ -1403,7 +1411,7 @@ nsm_status run_l0(const Plan& p, const Bufs& b, const Enc0Args& e0, const GbufMa
     const int pgrid = std::min(total, num_sms());
     {
         NSM_PROF("enc0_fused", st);
-        if (src == 2) enc0_kernel<T, 2><<<pgrid, kL0Threads, ENC0_SMEM_TMA, st>>>(e0, tm, total);
+        if (src == 2) enc0_kernel<T, 2><<<pgrid, kE0Threads, ENC0_SMEM_TMA, st>>>(e0, tm, total);
         else if (src == 1) enc0_kernel<T, 1><<<pgrid, kL0Threads, 2 * E0_SMEM, st>>>(e0, tm, total);
         else enc0_kernel<T, 0><<<pgrid, kL0Threads, 2 * E0_SMEM, st>>>(e0, tm, total);
     }
