@@ -82,9 +82,10 @@ def full(path):
             try:
                 x = float(v.replace(",", ""))
                 if m.startswith("dram__bytes"):
-                    x = x / 1e6 if u == "byte" else (x * 1e3 if u == "Gbyte" else x)   # -> MB
+                    x = x * {"byte": 1e-6, "Kbyte": 1e-3, "Mbyte": 1.0, "Gbyte": 1e3}.get(u, 1.0)   # -> MB
                 if m == "gpu__time_duration.sum":
-                    x = x / 1e3 if u in ("nsecond", "ns") else (x * 1e3 if u in ("msecond", "ms") else x)  # -> us
+                    x = x * {"nsecond": 1e-3, "ns": 1e-3, "usecond": 1.0, "us": 1.0, "msecond": 1e3,
+                             "ms": 1e3}.get(u, 1.0)   # -> us
                 rec[k] = x
                 cells.append(f"{x:.3g}")
             except ValueError:
