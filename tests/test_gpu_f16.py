@@ -134,3 +134,63 @@ def test_fused_frustum_error():
     cfg, w = _weights()
     with pytest.raises(FrustumError):
         ShadowInference(network.Plan(w, cfg, "fp16"), [fr])(_inputs(r))
+
+
+@pytest.mark.parametrize("hw", [(600, 1000), (250, 333), (100, 64), (1080, 1920)])
+def test_odd_shapes_fp16_vs_oracle(hw):
+    """Partial level-0 tiles, level sizes not multiples of the level tiles,
+    widths not multiples of 4 (no TMA: the LDG producer variant) and the
+    1080 -> 1088 padding, all vs the oracle on the padded frame."""
+    from oracle import features as of
+    from oracle import network as on
+    from paper_2301_05262_b200 import network, producer, scenes
+    from paper_2301_05262_b200.infer import ShadowInference
+    h, w = hw
+    fr = scenes.make_frame(scenes.random_scene(16, seed=h + w, emitter_radius_m=0.1), (h, w), (700, 700))
+    inp = producer.render_inputs([fr])
+    cfg, wts = _weights(seed=5)
+    y = ShadowInference(network.Plan(wts, cfg, "fp16"), [fr])(inp)[0, 0].cpu().numpy()
+    hh = {k: v[0].cpu().numpy() for k, v in inp.items()}
+    feats, _ = of.features_from_planes(hh["d"], hh["normal"], hh["position"], hh["sm"], fr.camera, fr.view,
+                                       fr.scene.emitter_center, fr.size_index, fr.bias)
+    hp, wp = (h + 15) // 16 * 16, (w + 15) // 16 * 16
+    xp = np.zeros((4, hp, wp), np.float32)
+    xp[:, :h, :w] = feats
+    ref = on.forward({k: v.data for k, v in wts.items()}, xp)[0, :h, :w]
+    mx, mse = _err(y, ref)
+    print(f"{hw} fp16: max {mx:.3g} mse {mse:.3g}")
+    assert mx <= MAX_ABS and mse <= MAX_MSE
+
+
+def test_4k_bf16_and_fp16_vs_oracle():
+    """Config-5 frame size (3840x2160, 64 objects, 4096^2 map)."""
+    from oracle import features as of
+    from oracle import network as on
+    from paper_2301_05262_b200 import network, producer, scenes
+    from paper_2301_05262_b200.infer import ShadowInference
+    fr = scenes.config_frames(5, seed=0, n_frames=2)[1]          # the soft-light scene
+    inp = producer.render_inputs([fr])
+    cfg, wts = _weights()
+    hh = {k: v[0].cpu().numpy() for k, v in inp.items()}
+    feats, _ = of.features_from_planes(hh["d"], hh["normal"], hh["position"], hh["sm"], fr.camera, fr.view,
+                                       fr.scene.emitter_center, fr.size_index, fr.bias)
+    ref = on.forward({k: v.data for k, v in wts.items()}, feats)[0]
+    for dtype in ("fp16", "bf16"):
+        y = ShadowInference(network.Plan(wts, cfg, dtype), [fr])(inp)[0, 0].float().cpu().numpy()
+        mx, mse = _err(y, ref)
+        print(f"4K {dtype}: max {mx:.3g} mse {mse:.3g}")
+        assert mse <= MAX_MSE
+        if dtype == "fp16":
+            assert mx <= MAX_ABS
+
+
+def test_forward_fp16_batch_matches_infer_features():
+    """Plan.forward on a batch of feature planes == per-frame results."""
+    import torch
+    from paper_2301_05262_b200 import network
+    cfg, wts = _weights()
+    plan = network.Plan(wts, cfg, "fp16")
+    x = torch.randn(5, 4, 64, 96, device="cuda") * 0.5
+    yb = plan.forward(x).cpu().numpy()
+    for i in range(5):
+        np.testing.assert_array_equal(plan.forward(x[i:i + 1]).cpu().numpy()[0], yb[i])
