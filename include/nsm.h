@@ -141,6 +141,18 @@ nsm_status nsm_features(const nsm_gbuffer* g, const float* sm, int64_t sm_stride
                         float* out_planes, int32_t* texel_idx, int64_t* first_bad,
                         void* stream);
 
+/* ---- blocker-search penumbra plane (BASELINE configs 3/4 extension) ----
+ * No reference implementation (PCSS is out of the reference's scope,
+ * SPEC.md:14): per covered pixel the nearest texel of _shadow_lookup, a
+ * (2*radius)^2 texel window, blockers = finite depths < z_f - bias,
+ * (z_min, z_max) -> analysis.penumbra_extents (analysis.py:240-269) with
+ * r_e = size_index * 0.0625 m, width (x_a + x_b) * focal_px / d
+ * (analysis.py:319-320).  out: (n, h, w) fp32, the 5th input plane of a
+ * NetworkConfig(in_channels=5) net.  first_bad as nsm_features. */
+nsm_status nsm_blocker_plane(const nsm_gbuffer* g, const float* sm, int64_t sm_stride,
+                             const nsm_frame* frames, int32_t n, int32_t h, int32_t w,
+                             int32_t radius, float* out, int64_t* first_bad, void* stream);
+
 /* ---- stage 2: network.forward (network.py:165-209) ----
  * x: (n, in_channels, h, w) fp32 device, y: (n, 1, h, w) fp32 device.
  * h, w must be divisible by 2**(layers-1) (NSM_ERR_SHAPE otherwise). */

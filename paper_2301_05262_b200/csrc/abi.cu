@@ -338,6 +338,17 @@ nsm_status nsm_features(const nsm_gbuffer* g, const float* sm, int64_t sm_stride
                            first_bad, (cudaStream_t)stream);
 }
 
+nsm_status nsm_blocker_plane(const nsm_gbuffer* g, const float* sm, int64_t sm_stride,
+                             const nsm_frame* frames, int32_t n, int32_t h, int32_t w, int32_t radius,
+                             float* out, int64_t* first_bad, void* stream) {
+    clear_error();
+    if (!g || !sm || !frames || !out || !first_bad || !g->d || !g->position)
+        return fail(NSM_ERR_ARG, "nsm_blocker_plane: null argument");
+    if (n <= 0 || h <= 0 || w <= 0 || radius <= 0) return fail(NSM_ERR_ARG, "nsm_blocker_plane: bad size");
+    if (g->dtype != NSM_F32 && g->dtype != NSM_F64) return fail(NSM_ERR_ARG, "G-buffer planes must be F32 or F64");
+    return launch_blocker(g, sm, sm_stride, frames, n, h, w, radius, out, first_bad, (cudaStream_t)stream);
+}
+
 nsm_status nsm_forward(const nsm_plan* plan, const float* x, int32_t n, int32_t h, int32_t w,
                        float* y, void* workspace, size_t ws_bytes, void* stream) {
     clear_error();

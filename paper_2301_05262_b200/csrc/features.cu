@@ -164,3 +164,100 @@ nsm_status launch_features(const nsm_gbuffer* g, const float* sm, int64_t sm_str
 }
 
 }  // namespace nsm
+
+// ---------------------------------------------------------------------------
+// Blocker-search penumbra plane (BASELINE configs 3/4 extension; no reference
+// implementation -- parity is against oracle/blocker.py).  Per covered pixel:
+// the nearest texel exactly as _shadow_lookup, a (2R)x(2R) texel window,
+// blockers = finite depths < z_f - b, (z_min, z_max) -> the bounding-sphere
+// penumbra model of analysis.penumbra_extents (analysis.py:240-269) with the
+// emitter radius, and the screen-space width (x_a + x_b) * focal_px / d
+// (analysis.py:319-320).  0 where uncovered / no blockers / invalid geometry.
+namespace nsm {
+
+__device__ double penumbra_width(double zmin, double zmax, double zf, double re, double focal, double d) {
+    const double zm = (zmax + zmin) / 2.0, rs = (zmax - zmin) / 2.0;
+    const double hyp = sqrt(zm * zm + re * re);
+    if (!(zmin > 0.0 && zmax >= zmin && zf > zmax && zm > 0.0 && rs <= hyp && re > 0.0)) return 0.0;
+    const double td = asin(rs / hyp);
+    const double bq = re * (zf - zm) / zm;
+    const double th = atan((bq + re) / zf);
+    if (!(th + td < 1.5707963267948966)) return 0.0;
+    const double xa = zf * tan(th - td) - re, xb = zf * tan(th + td) - re;
+    return (xa + xb) * focal / d;
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256) blocker_kernel(GBufK g, const float* __restrict__ sm, int64_t sm_stride,
+                                                      FrameTable tab, int h, int w, int radius,
+                                                      float* __restrict__ out, int64_t* __restrict__ first_bad) {
+    const int x = blockIdx.x * blockDim.x + threadIdx.x;
+    const int y = blockIdx.y * blockDim.y + threadIdx.y;
+    const int fr = blockIdx.z;
+    if (x >= w || y >= h) return;
+    const FrameK& f = tab.f[fr];
+    const int64_t hw = (int64_t)h * w, pix = (int64_t)y * w + x, base = (int64_t)fr * g.frame_stride;
+    float* o = out + (int64_t)fr * hw + pix;
+    const double d = ldd<T>(g.d, base + pix);
+    if (!(d > 0.0)) {
+        *o = 0.f;
+        return;
+    }
+    const int64_t pb = 3 * base;
+    const double px = ldd<T>(g.position, pb + pix), py = ldd<T>(g.position, pb + hw + pix),
+                 pz = ldd<T>(g.position, pb + 2 * hw + pix);
+    const double tx = f.ec[0] - px, ty = f.ec[1] - py, tz = f.ec[2] - pz;
+    const double zf = sqrt(tx * tx + ty * ty + tz * tz);
+    int ri, ci;
+    if (!texel_of(f, px, py, pz, ri, ci)) atomic_min_i64(first_bad + fr, pix);
+    const double thr = zf - f.bias;
+    const float* smf = sm + fr * sm_stride;
+    float zmin = INFINITY, zmax = -INFINITY;
+    const int r0 = max(ri - radius, 0), r1 = min(ri + radius, f.hs);
+    const int c0 = max(ci - radius, 0), c1 = min(ci + radius, f.ws);
+    for (int r = r0; r < r1; ++r) {
+        const float* row = smf + (int64_t)r * f.ws;
+        for (int c = c0; c < c1; ++c) {
+            const float t = __ldg(row + c);
+            if ((double)t < thr) {          // +inf misses never pass
+                zmin = fminf(zmin, t);
+                zmax = fmaxf(zmax, t);
+            }
+        }
+    }
+    double wv = 0.0;
+    if (zmin <= zmax) {
+        const double re = f.size_index * (0.5 / 2.0 / 4.0);          // scene.emitter_radius
+        const double focal = (f.ch / 2.0) / f.half_h;                  // CameraPose.focal_px
+        wv = penumbra_width(zmin, zmax, zf, re, focal, d);
+    }
+    *o = (float)wv;
+}
+
+nsm_status launch_blocker(const nsm_gbuffer* g, const float* sm, int64_t sm_stride, const nsm_frame* frames,
+                          int32_t n, int32_t h, int32_t w, int32_t radius, float* out, int64_t* first_bad,
+                          cudaStream_t st) {
+    GBufK gk{g->d, g->normal, g->position, nullptr, nullptr, nullptr, nullptr, g->frame_stride};
+    launch_fill_i64(first_bad, n, INT64_MAX, st);
+    for (int32_t f0 = 0; f0 < n; f0 += NSM_MAX_FRAMES_PER_LAUNCH) {
+        const int nf = min(n - f0, NSM_MAX_FRAMES_PER_LAUNCH);
+        FrameTable tab;
+        make_frame_table(frames + f0, nf, tab);
+        GBufK gf = gk;
+        const int64_t es = g->dtype == NSM_F64 ? 8 : 4;
+        gf.d = (const char*)g->d + es * f0 * g->frame_stride;
+        gf.position = (const char*)g->position + es * 3 * f0 * g->frame_stride;
+        dim3 blk(32, 8), grd((w + 31) / 32, (h + 7) / 8, nf);
+        NSM_PROF("blocker_kernel", st);
+        if (g->dtype == NSM_F64)
+            blocker_kernel<double><<<grd, blk, 0, st>>>(gf, sm + f0 * sm_stride, sm_stride, tab, h, w, radius,
+                                                        out + (int64_t)f0 * h * w, first_bad + f0);
+        else
+            blocker_kernel<float><<<grd, blk, 0, st>>>(gf, sm + f0 * sm_stride, sm_stride, tab, h, w, radius,
+                                                       out + (int64_t)f0 * h * w, first_bad + f0);
+    }
+    NSM_CUDA_TRY(cudaGetLastError());
+    return NSM_OK;
+}
+
+}  // namespace nsm

@@ -56,6 +56,9 @@ nsm_status launch_features(const nsm_gbuffer* g, const float* sm, int64_t sm_str
                            int32_t wo, float* out, int32_t* tidx, int64_t* first_bad,
                            cudaStream_t st);
 void launch_fill_i64(int64_t* p, int n, int64_t v, cudaStream_t st);
+nsm_status launch_blocker(const nsm_gbuffer* g, const float* sm, int64_t sm_stride, const nsm_frame* frames,
+                          int32_t n, int32_t h, int32_t w, int32_t radius, float* out, int64_t* first_bad,
+                          cudaStream_t st);
 nsm_status launch_render_gbuffer(const double* prims, int32_t n_prims, const nsm_camera* cam,
                                  float* d, float* normal, float* position, cudaStream_t st);
 nsm_status launch_render_shadowmap(const double* prims, int32_t n_prims,

@@ -167,6 +167,31 @@ def assemble_features_batch(inputs, frames, want_idx=False, check=True):
     return out, idx, bad
 
 
+def blocker_penumbra_batch(inputs, frames, radius: int = 8, check=True):
+    """Blocker-search penumbra-width plane (N, H, W) fp32 -- the 5th input
+    plane of BASELINE configs 3/4 (a build extension: the reference has no
+    blocker search; see include/nsm.h nsm_blocker_plane and oracle/blocker.py).
+    ``frames`` as for :func:`assemble_features_batch`; size_index sets the
+    emitter radius (0.0625 m per unit, scene.py:54-58)."""
+    import torch
+    d = inputs["d"]
+    n, h, w = d.shape
+    hs, ws = inputs["sm"].shape[1:]
+    gb = _lib.GBufferC(_lib.NSM_F32, d.data_ptr(), inputs["normal"].data_ptr(),
+                       inputs["position"].data_ptr(), None, None, None, None, h * w)
+    out = torch.empty((n, h, w), dtype=torch.float32, device=d.device)
+    bad = torch.empty(n, dtype=torch.int64, device=d.device)
+    _lib.check(_lib.lib.nsm_blocker_plane(C.byref(gb), inputs["sm"].data_ptr(), hs * ws,
+                                          _lib.frames_c(frames), n, h, w, int(radius),
+                                          out.data_ptr(), bad.data_ptr(), _lib.stream_ptr()))
+    if check:
+        for v in bad.cpu().tolist():
+            if v != _lib.INT64_MAX:
+                y, x = divmod(int(v), w)
+                raise FrustumError(f"covered pixel ({y}, {x}) projects outside the emitter frustum")
+    return out
+
+
 def hard_shadow_mask(stack: FeatureStack) -> np.ndarray:
     """Point-light shadow test (raster.py:281-283)."""
     return (stack.data[0] < 0.0) & stack.coverage

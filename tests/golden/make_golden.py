@@ -210,7 +210,24 @@ def make_nets():
     print("nets:", len(NET_CASES), "cases")
 
 
+def make_penumbra():
+    """analysis.penumbra_extents on random valid geometry (pins the formula
+    the blocker-search extension reuses)."""
+    from shadowkit import analysis
+    rng = np.random.default_rng(11)
+    n = 4000
+    z_min = rng.uniform(0.5, 5.0, n)
+    z_max = z_min + rng.uniform(0.0, 1.0, n)
+    z_f = z_max + rng.uniform(0.01, 4.0, n)
+    r_e = rng.uniform(0.0, 0.5, n)
+    xa, xb = analysis.penumbra_extents(z_min, z_max, z_f, r_e)
+    np.savez_compressed(os.path.join(HERE, "penumbra.npz"), z_min=z_min, z_max=z_max, z_f=z_f,
+                        r_e=r_e, x_a=xa, x_b=xb)
+    print("penumbra:", n)
+
+
 if __name__ == "__main__":
+    make_penumbra()
     make_cfg1()
     make_variants()
     make_canon()

@@ -126,3 +126,28 @@ def test_spec_zero_weights_give_half():
     z = {k: np.zeros_like(v.data) for k, v in w.items()}
     y = on.forward(z, np.random.default_rng(0).normal(size=(4, 32, 32)).astype(np.float32))
     np.testing.assert_array_equal(y, 0.5)
+
+
+def test_penumbra_formula_pinned_to_reference():
+    """oracle.blocker.penumbra_widths reuses analysis.penumbra_extents
+    (analysis.py:240-269): pinned on 4000 reference evaluations."""
+    from oracle import blocker as ob
+    g = load_golden("penumbra")
+    w = ob.penumbra_widths(g["z_min"], g["z_max"], g["z_f"], g["r_e"], 1.0, 1.0)
+    ref = g["x_a"] + g["x_b"]
+    ref = np.where(g["r_e"] > 0, ref, 0.0)             # point lights: exact zero width
+    np.testing.assert_allclose(w, ref, rtol=1e-12, atol=1e-12)
+
+
+def test_blocker_plane_point_light_is_zero():
+    from oracle import blocker as ob
+    r = load_golden("cfg1")
+    cov = r["d"] > 0
+    z_f, _, _, cov = of.derive_planes(r["d"], r["normal"], r["position"], golden_camera(r),
+                                      r["emitter_center"])
+    p = ob.blocker_plane(r["d"], r["position"], z_f, cov, r["sm"], golden_view(r), float(r["bias"]),
+                         0.0, golden_camera(r).focal_px)
+    assert np.all(p == 0)
+    p2 = ob.blocker_plane(r["d"], r["position"], z_f, cov, r["sm"], golden_view(r), float(r["bias"]),
+                          4.0, golden_camera(r).focal_px)
+    assert np.all(p2[~cov] == 0) and np.all(p2 >= 0) and (p2 > 0).mean() > 0.05
