@@ -407,13 +407,29 @@ __device__ __forceinline__ void produce_features(const Enc0Args& a, uint8_t* buf
 // .inc can only claim what .dec released within the CTA (more deadlocks).
 constexpr int kE0Prod = 512, kE0Threads = 640;
 
+// Per-pixel producer state carried from the A to the B phase of a half-tile.
+template <int K>
+struct HalfRegs {
+    float izf[K], c2[K], c3[K], look[K];
+};
+
 template <typename T>
 __device__ __forceinline__ void produce_features_tma(const Enc0Args& a, const GbufMaps& tm, int total) {
+    // Software pipeline over half-tiles q (two per tile):
+    //   A(q): staged planes -> texel (fp64), 1/z_f, c_e + s, c_c / d in
+    //         registers, and the shadow-map gather issued (LDG in flight)
+    //   TMA(q+2) into the stage A(q) just released
+    //   B(q-1): gathered occluder depth -> ch0, ch1, pack, STS into the
+    //         tile's feature buffer
+    // so the gather latency of half q overlaps B(q-1) and A(q+1), and the
+    // G-buffer of half q+2 streams in meanwhile.
     extern __shared__ __align__(128) uint8_t smem[];
+    constexpr int K = (ST_PIX + kE0Prod - 1) / kE0Prod;
     uint8_t* stage = smem + 2 * E0_SMEM;
     uint64_t* full = reinterpret_cast<uint64_t*>(stage + 2 * ST_BYTES);
     const int ptid = threadIdx.x;
     const int mytiles = (int)blockIdx.x < total ? (total - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x : 0;
+    const int nh = 2 * mytiles;
     auto issue = [&](int q) {
         const L0Tile tl = l0_tile(blockIdx.x + (q >> 1) * gridDim.x, a.H0, a.W0);
         const int sidx = q & 1;
@@ -430,87 +446,98 @@ __device__ __forceinline__ void produce_features_tma(const Enc0Args& a, const Gb
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     nbar_sync(5, kE0Prod);
-    if (ptid == 0 && mytiles > 0) {
-        issue(0);
-        issue(1);
+    if (ptid == 0) {
+        if (nh > 0) issue(0);
+        if (nh > 1) issue(1);
     }
-    for (int k = 0; k < mytiles; ++k) {
-        const L0Tile tl = l0_tile(blockIdx.x + k * gridDim.x, a.H0, a.W0);
-        const int sb = k & 1;
-        if (k >= 2) nbar_sync(3 + sb, kE0Threads);
-        uint8_t* buf = smem + sb * E0_SMEM;
+    auto phaseA = [&](int q, HalfRegs<K>& R) {
+        const L0Tile tl = l0_tile(blockIdx.x + (q >> 1) * gridDim.x, a.H0, a.W0);
+        const int sidx = q & 1, hh = q & 1;
         const FrameK& F = a.tab.f[tl.f];
         const float* smf = a.sm + tl.f * a.sm_stride;
+        mbar_wait(&full[sidx], (q >> 1) & 1);
+        const float* sd = reinterpret_cast<const float*>(stage + sidx * ST_BYTES);
+        const float* sn = reinterpret_cast<const float*>(stage + sidx * ST_BYTES + ST_OFF_N);
+        const float* sp = reinterpret_cast<const float*>(stage + sidx * ST_BYTES + ST_OFF_P);
         const float ecx = F.fec[0], ecy = F.fec[1], ecz = F.fec[2];
-        const float bias = F.fbias, sidx_off = F.fsize;
-        for (int hh = 0; hh < 2; ++hh) {
-            const int q = 2 * k + hh, sidx = q & 1;
-            const int fy0 = 2 * tl.ty0 - 2 + ST_ROWS * hh, fx0 = 2 * tl.tx0 - 2;
-            mbar_wait(&full[sidx], (q >> 1) & 1);
-            const float* sd = reinterpret_cast<const float*>(stage + sidx * ST_BYTES);
-            const float* sn = reinterpret_cast<const float*>(stage + sidx * ST_BYTES + ST_OFF_N);
-            const float* sp = reinterpret_cast<const float*>(stage + sidx * ST_BYTES + ST_OFF_P);
-            constexpr int K = 5;
-#pragma unroll 1
-            for (int i0 = ptid; i0 < ((a.dbg & 1) ? 0 : ST_PIX); i0 += kE0Prod * K) {
-                float d[K], look[K];
-                int si[K];
 #pragma unroll
-                for (int j = 0; j < K; ++j) {
-                    const int i = i0 + j * kE0Prod;
-                    si[j] = i + 4 * (i / ST_COLS) + 2;      // staged index (136-wide rows)
-                    d[j] = i < ST_PIX ? sd[si[j]] : 0.f;
-                    look[j] = 0.f;
-                    if (d[j] > 0.f) {
-                        int ri, ci;
-                        if (!texel_fused(F, sp[si[j]], sp[ST_TPIX + si[j]], sp[2 * ST_TPIX + si[j]], ri, ci)) {
-                            const int ry = i / ST_COLS;
-                            atomic_min_i64(a.first_bad + tl.f,
-                                           (int64_t)(fy0 + ry) * a.w + (fx0 + i - ry * ST_COLS));
-                        }
-                        look[j] = __ldg(smf + (int64_t)ri * F.ws + ci);
-                    }
-                }
-#pragma unroll
-                for (int j = 0; j < K; ++j) {
-                    const int i = i0 + j * kE0Prod;
-                    if (i >= ST_PIX) continue;
-                    const int ry = i / ST_COLS, rx = i - ry * ST_COLS;
-                    float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-                    if (d[j] > 0.f) {
-                        const int o = si[j];
-                        const float px = sp[o], py = sp[ST_TPIX + o], pz = sp[2 * ST_TPIX + o];
-                        const float nx = sn[o], ny = sn[ST_TPIX + o], nz = sn[2 * ST_TPIX + o];
-                        const float tx = ecx - px, ty = ecy - py, tz = ecz - pz;
-                        const float izf = rsqrtf(tx * tx + ty * ty + tz * tz);
-                        const float ce = fminf(fmaxf((nx * tx + ny * ty + nz * tz) * izf, 0.f), 1.f);
-                        // c_c = clip(n . -ray): the pixel ray is the direction camera -> hit
-                        // point (render_gbuffer places p on it), fp32 is ample here
-                        const float dx = F.fcp[0] - px, dy = F.fcp[1] - py, dz = F.fcp[2] - pz;
-                        const float cc = fminf(fmaxf((nx * dx + ny * dy + nz * dz) *
-                                                         rsqrtf(dx * dx + dy * dy + dz * dz), 0.f), 1.f);
-                        float ch0 = 0.f, ch1 = 1.f;
-                        if (look[j] < INFINITY) {                  // raster.py:262 (finite lookup)
-                            const float zf = 1.f / izf;
-                            const float m = fminf(look[j], zf);
-                            ch0 = (m - zf) + bias;
-                            ch1 = (m + bias) * izf;
-                        }
-                        v = make_float4(ch0, ch1, ce + sidx_off, __fdividef(cc, d[j]));
-                    }
-                    const int trow = ST_ROWS * hh + ry;            // full-res row within the tile
-                    const int p = (trow >> 1) * E0_IC + (rx >> 1);
-                    *reinterpret_cast<uint2*>(buf + (trow & 1) * E0_PLANE + p * 16 + (rx & 1) * 8) =
-                        make_uint2(Elem<T>::pack(v.x, v.y), Elem<T>::pack(v.z, v.w));
-                }
+        for (int j = 0; j < K; ++j) {
+            const int i = ptid + j * kE0Prod;
+            R.izf[j] = 0.f;
+            R.c2[j] = 0.f;
+            R.c3[j] = 0.f;
+            R.look[j] = -1.f;                       // < 0: uncovered / outside
+            if (i >= ST_PIX) continue;
+            const int o = i + 4 * (i / ST_COLS) + 2;      // staged index (136-wide rows)
+            const float d = sd[o];
+            if (!(d > 0.f)) continue;
+            const float px = sp[o], py = sp[ST_TPIX + o], pz = sp[2 * ST_TPIX + o];
+            int ri, ci;
+            if (!texel_fused(F, px, py, pz, ri, ci)) {
+                const int ry = i / ST_COLS;
+                atomic_min_i64(a.first_bad + tl.f,
+                               (int64_t)(2 * tl.ty0 - 2 + ST_ROWS * hh + ry) * a.w + (2 * tl.tx0 - 2 + i - ry * ST_COLS));
             }
-            nbar_sync(5, kE0Prod);                 // everyone is done with stage sidx
-            if (ptid == 0 && q + 2 < 2 * mytiles) {
-                fence_proxy_async();
-                issue(q + 2);
-            }
+            R.look[j] = __ldg(smf + (int64_t)ri * F.ws + ci);   // consumed one phase later
+            const float nx = sn[o], ny = sn[ST_TPIX + o], nz = sn[2 * ST_TPIX + o];
+            const float tx = ecx - px, ty = ecy - py, tz = ecz - pz;
+            const float izf = rsqrtf(tx * tx + ty * ty + tz * tz);
+            // c_c = clip(n . -ray): the pixel ray is the direction camera -> hit
+            // point (render_gbuffer places p on it), fp32 is ample here
+            const float dx = F.fcp[0] - px, dy = F.fcp[1] - py, dz = F.fcp[2] - pz;
+            const float cc = fminf(fmaxf((nx * dx + ny * dy + nz * dz) * rsqrtf(dx * dx + dy * dy + dz * dz), 0.f), 1.f);
+            R.izf[j] = izf;
+            R.c2[j] = fminf(fmaxf((nx * tx + ny * ty + nz * tz) * izf, 0.f), 1.f) + F.fsize;
+            R.c3[j] = __fdividef(cc, d);
         }
-        nbar_arrive(1 + sb, kE0Threads);
+    };
+    auto phaseB = [&](int q, HalfRegs<K>& R) {
+        const L0Tile tl = l0_tile(blockIdx.x + (q >> 1) * gridDim.x, a.H0, a.W0);
+        const int hh = q & 1, sb = (q >> 1) & 1;
+        const float bias = a.tab.f[tl.f].fbias;
+        uint8_t* buf = smem + sb * E0_SMEM;
+#pragma unroll
+        for (int j = 0; j < K; ++j) {
+            const int i = ptid + j * kE0Prod;
+            if (i >= ST_PIX) continue;
+            const int ry = i / ST_COLS, rx = i - ry * ST_COLS;
+            float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+            const float look = R.look[j];
+            if (look >= 0.f) {
+                float ch0 = 0.f, ch1 = 1.f;
+                if (look < INFINITY) {                  // raster.py:262 (finite lookup)
+                    const float zf = 1.f / R.izf[j];
+                    const float m = fminf(look, zf);
+                    ch0 = (m - zf) + bias;
+                    ch1 = (m + bias) * R.izf[j];
+                }
+                v = make_float4(ch0, ch1, R.c2[j], R.c3[j]);
+            }
+            const int trow = ST_ROWS * hh + ry;            // full-res row within the tile
+            const int p = (trow >> 1) * E0_IC + (rx >> 1);
+            *reinterpret_cast<uint2*>(buf + (trow & 1) * E0_PLANE + p * 16 + (rx & 1) * 8) =
+                make_uint2(Elem<T>::pack(v.x, v.y), Elem<T>::pack(v.z, v.w));
+        }
+    };
+    auto step = [&](int q, HalfRegs<K>& RA, HalfRegs<K>& RB) {
+        if (q < nh && !(a.dbg & 1)) phaseA(q, RA);
+        else if (q < nh) mbar_wait(&full[q & 1], (q >> 1) & 1);
+        nbar_sync(5, kE0Prod);                     // stage q&1 fully consumed by A(q)
+        if (ptid == 0 && q + 2 < nh) {
+            fence_proxy_async();
+            issue(q + 2);
+        }
+        if (q >= 1) {
+            const int qb = q - 1, k = qb >> 1;
+            if (!(qb & 1) && k >= 2) nbar_sync(3 + (k & 1), kE0Threads);   // tile buffer free
+            if (!(a.dbg & 1)) phaseB(qb, RB);
+            if (qb & 1) nbar_arrive(1 + (k & 1), kE0Threads);               // tile k complete
+        }
+    };
+    HalfRegs<K> R0, R1;
+    for (int q = 0; q <= nh; q += 2) {
+        step(q, R0, R1);
+        if (q + 1 <= nh) step(q + 1, R1, R0);
     }
 }
 
