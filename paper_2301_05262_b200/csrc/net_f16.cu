@@ -36,7 +36,7 @@ int chunk_frames() {
     static int v = 0;
     if (!v) {
         const char* e = getenv("NSM_CHUNK_FRAMES");
-        v = e ? std::max(1, std::min(NSM_MAX_FRAMES_PER_LAUNCH, atoi(e))) : 4;
+        v = e ? std::max(1, std::min(NSM_MAX_FRAMES_PER_LAUNCH, atoi(e))) : NSM_MAX_FRAMES_PER_LAUNCH;
     }
     return v;
 }
