@@ -653,6 +653,7 @@ struct Dec0Args {
     const float* b1;
     const float* bh;
     float* y;             // head output, 4 fp32 planes per frame: (N, 4, H0, W0)
+    int dbg;              // experiments only: 1 skip upsample math, 2 skip convolutions
 };
 
 // Bilinear 2x of an NHWC 16-bit tensor at one output pixel, 8 channels
@@ -723,34 +724,63 @@ __global__ void __launch_bounds__(kL0Threads, 1) dec0_kernel(const __grid_consta
             mbar_wait(&full[sb], (k >> 1) & 1);
             const uint8_t* lo = stg + sb * D0_STG;
             const int ly0 = tl.ty0 / 2 - 1, lx0 = tl.tx0 / 2 - 1;
-            // up2(D1) over the halo'd tile (zero outside the frame: conv padding)
-            for (int i = ptid; i < E0_IR * E0_IC * 2; i += kL0Prod) {
-                const int c = i & 1, p = i >> 1;
-                const int ti = p / E0_IC, tj = p - ti * E0_IC;
-                const int oy = tl.ty0 - 1 + ti, ox = tl.tx0 - 1 + tj;
-                uint4 q = make_uint4(0u, 0u, 0u, 0u);
-                if (oy >= 0 && ox >= 0 && oy < a.H0 && ox < a.W0) {
-                    const float sy = fminf(fmaxf((oy + 0.5f) * 0.5f - 0.5f, 0.f), (float)(H1 - 1));
-                    const float sx = fminf(fmaxf((ox + 0.5f) * 0.5f - 0.5f, 0.f), (float)(W1 - 1));
-                    const int r0 = (int)sy, c0 = (int)sx;
-                    const int r1 = min(r0 + 1, H1 - 1), c1 = min(c0 + 1, W1 - 1);
-                    const float wy = sy - r0, wx = sx - c0;
-                    auto ld = [&](int r, int cc) {
-                        return *reinterpret_cast<const uint4*>(lo + (((r - ly0) * D0_LC + (cc - lx0)) * 16 + c * 8) * 2);
-                    };
-                    const uint4 q00 = ld(r0, c0), q10 = ld(r1, c0), q01 = ld(r0, c1), q11 = ld(r1, c1);
-                    const uint32_t *a00 = &q00.x, *a10 = &q10.x, *a01 = &q01.x, *a11 = &q11.x;
-                    uint32_t* qo = &q.x;
+            // up2(D1) over the halo'd tile (zero outside the frame: conv padding),
+            // one 2x2 output block per item: the block of D1 pixel (bi, bj) reads its
+            // 3x3 neighbourhood with fixed (1/4, 3/4) weights; clamping the source
+            // indices reproduces the reference's edge clamp (autodiff.py:258-264).
+            constexpr int BR = E0_IR / 2 + 1, BC = E0_IC / 2 + 1;     // 10 x 34 blocks
+            for (int it = ptid; it < ((a.dbg & 1) ? 0 : BR * BC * 2); it += kL0Prod) {
+                const int c = it & 1, blk = it >> 1;
+                const int bil = blk / BC, bjl = blk - bil * BC;
+                const int bi = ly0 + bil, bj = lx0 + bjl;          // D1 pixel of the block
+                int rs[3], cs[3];
 #pragma unroll
-                    for (int e = 0; e < 4; ++e) {
-                        const float2 p00 = Elem<T>::unpack(a00[e]), p10 = Elem<T>::unpack(a10[e]);
-                        const float2 p01 = Elem<T>::unpack(a01[e]), p11 = Elem<T>::unpack(a11[e]);
-                        const float c0x = p00.x * (1.f - wy) + p10.x * wy, c1x = p01.x * (1.f - wy) + p11.x * wy;
-                        const float c0y = p00.y * (1.f - wy) + p10.y * wy, c1y = p01.y * (1.f - wy) + p11.y * wy;
-                        qo[e] = Elem<T>::pack(c0x * (1.f - wx) + c1x * wx, c0y * (1.f - wx) + c1y * wx);
+                for (int u = 0; u < 3; ++u) {
+                    rs[u] = min(max(min(max(bi - 1 + u, 0), H1 - 1) - ly0, 0), D0_LR - 1);
+                    cs[u] = min(max(min(max(bj - 1 + u, 0), W1 - 1) - lx0, 0), D0_LC - 1);
+                }
+                float top[3][8], bot[3][8];
+#pragma unroll
+                for (int u = 0; u < 3; ++u) {
+                    float sv[3][8];
+#pragma unroll
+                    for (int v = 0; v < 3; ++v) {
+                        const uint4 q = *reinterpret_cast<const uint4*>(lo + ((rs[v] * D0_LC + cs[u]) * 16 + c * 8) * 2);
+                        const uint32_t* qw = &q.x;
+#pragma unroll
+                        for (int e = 0; e < 4; ++e) {
+                            const float2 f2 = Elem<T>::unpack(qw[e]);
+                            sv[v][2 * e] = f2.x;
+                            sv[v][2 * e + 1] = f2.y;
+                        }
+                    }
+#pragma unroll
+                    for (int e = 0; e < 8; ++e) {
+                        top[u][e] = 0.25f * sv[0][e] + 0.75f * sv[1][e];
+                        bot[u][e] = 0.75f * sv[1][e] + 0.25f * sv[2][e];
                     }
                 }
-                *reinterpret_cast<uint4*>(buf + c * E0_PLANE + p * 16) = q;
+#pragma unroll
+                for (int ab = 0; ab < 4; ++ab) {
+                    const int aa = ab >> 1, bb = ab & 1;
+                    const int oy = 2 * bi + aa, ox = 2 * bj + bb;        // level-0 pixel
+                    const int ti = oy - (tl.ty0 - 1), tj = ox - (tl.tx0 - 1);
+                    if (ti < 0 || ti >= E0_IR || tj < 0 || tj >= E0_IC) continue;
+                    uint4 q = make_uint4(0u, 0u, 0u, 0u);
+                    if (oy >= 0 && ox >= 0 && oy < a.H0 && ox < a.W0) {
+                        const float(&vr)[3][8] = aa ? bot : top;
+                        uint32_t* qo = &q.x;
+#pragma unroll
+                        for (int e = 0; e < 4; ++e) {
+                            const float x0 = bb ? 0.75f * vr[1][2 * e] + 0.25f * vr[2][2 * e]
+                                                : 0.25f * vr[0][2 * e] + 0.75f * vr[1][2 * e];
+                            const float x1 = bb ? 0.75f * vr[1][2 * e + 1] + 0.25f * vr[2][2 * e + 1]
+                                                : 0.25f * vr[0][2 * e + 1] + 0.75f * vr[1][2 * e + 1];
+                            qo[e] = Elem<T>::pack(x0, x1);
+                        }
+                    }
+                    *reinterpret_cast<uint4*>(buf + c * E0_PLANE + (ti * E0_IC + tj) * 16) = q;
+                }
             }
             nbar_sync(5, kL0Prod);                 // everyone is done with stage sb
             if (ptid == 0 && k + 2 < mytiles) issue(k + 2);
@@ -795,6 +825,7 @@ __global__ void __launch_bounds__(kL0Threads, 1) dec0_kernel(const __grid_consta
     l0_consume_loop(total,
         [&](uint8_t* buf, int tile) {
             const L0Tile tl = l0_tile(tile, a.H0, a.W0);
+            if (a.dbg & 2) return;
             conv3_strip16<T, 8>(smem_u32(buf), E0_PLANE, E0_IC, r0, sx, B3, bias3, [&](int oo, float (&acc)[2][4]) {
                 uint32_t a1[4], a2[4];
                 relu_pack_a<T>(acc, a1);
@@ -1445,8 +1476,9 @@ nsm_status run_l0(const Plan& p, const Bufs& b, const Enc0Args& e0, const GbufMa
     nsm_status s = run_levels<T>(p, b, nf, H0, W0, st);
     if (s != NSM_OK) return s;
     const Level& L0 = p.lev[0];
+    static const int d0dbg = getenv("NSM_DEC0_DBG") ? atoi(getenv("NSM_DEC0_DBG")) : 0;
     Dec0Args d{b.d1, H0, W0, (const uint2*)L0.dec3.wpk, (const uint2*)L0.dec1.wpk,
-               (const uint2*)p.head.wpk, L0.dec3.b32, L0.dec1.b32, p.head.b32, b.y};
+               (const uint2*)p.head.wpk, L0.dec3.b32, L0.dec1.b32, p.head.b32, b.y, d0dbg};
     {
         CUtensorMap dm;
         memset(&dm, 0, sizeof dm);
