@@ -179,6 +179,24 @@ nsm_status nsm_render_gbuffer(const double* prims, int32_t n_prims, const nsm_ca
 nsm_status nsm_render_shadowmap(const double* prims, int32_t n_prims,
                                 const nsm_emitter_view* view, float* depth, void* stream);
 
+/* ---- temporal consumers of the visibility ----
+ * nsm_motion_vectors: raster.motion_vectors (raster.py:330-358) for every
+ * consecutive pair of a t_frames sequence: pair k = (frame k, frame k+1),
+ * frame k+1's points reprojected with cams[k] (camera of frame k).  g holds
+ * t_frames frames (frame_stride as above; coverage NULL -> d > 0).
+ * vec: (t_frames-1, 2, h, w) fp64 (row, col) offsets, 0 on uncovered pixels;
+ * valid: (t_frames-1, h, w) uint8.
+ * nsm_temporal_instability: the per-pair sums of
+ * analysis.temporal_instability (analysis.py:350-377): vis (t_frames, h, w)
+ * fp32, acc (t_frames-1) fp64 sums of expm1(alpha |cur - prev[reproj]|) over
+ * valid pixels, count (t_frames-1) uint64 valid pixels.  E = sum(acc) /
+ * sum(count); the host raises NoValidPixels when sum(count) == 0. */
+nsm_status nsm_motion_vectors(const nsm_gbuffer* g, const nsm_camera* cams, int32_t t_frames,
+                              int32_t h, int32_t w, double* vec, uint8_t* valid, void* stream);
+nsm_status nsm_temporal_instability(const float* vis, const double* vec, const uint8_t* valid,
+                                    int32_t t_frames, int32_t h, int32_t w, double alpha,
+                                    double* acc, uint64_t* count, void* stream);
+
 /* ---- tracing / launch accounting (tracing) ----
  * nsm_launch_count: kernels launched by this library since load (graph
  * replays not included).  nsm_profile_enable(1): record a CUDA-event pair

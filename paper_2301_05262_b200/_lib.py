@@ -88,6 +88,10 @@ _EXPORTS = {
                                      C.c_void_p, C.c_void_p, C.c_void_p]),
     "nsm_render_shadowmap": (C.c_int, [C.c_void_p, C.c_int32, C.POINTER(EmitterViewC),
                                        C.c_void_p, C.c_void_p]),
+    "nsm_motion_vectors": (C.c_int, [C.POINTER(GBufferC), C.POINTER(CameraC), C.c_int32, C.c_int32,
+                                     C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p]),
+    "nsm_temporal_instability": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32, C.c_int32,
+                                           C.c_int32, C.c_double, C.c_void_p, C.c_void_p, C.c_void_p]),
     "nsm_launch_count": (C.c_int64, []),
     "nsm_profile_enable": (None, [C.c_int32]),
     "nsm_profile_report": (C.c_int32, [C.c_char_p, C.c_size_t]),

@@ -48,7 +48,7 @@ def _compile(src):
     # fast-math only where it is harmless: the parity kernels keep IEEE
     # division/sqrt (features.cu, net_f32.cu, producer.cu, abi.cu)
     flags = [f for f in FLAGS if f != "--use_fast_math"] if src in (
-        "features.cu", "net_f32.cu", "producer.cu", "abi.cu") else FLAGS
+        "features.cu", "net_f32.cu", "producer.cu", "abi.cu", "temporal.cu") else FLAGS
     cmd = [NVCC, *ARCH, *flags, "-c", path, "-o", obj]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:

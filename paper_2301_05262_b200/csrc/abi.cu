@@ -429,4 +429,29 @@ nsm_status nsm_render_shadowmap(const double* prims, int32_t n_prims, const nsm_
     return launch_render_shadowmap(prims, n_prims, view, depth, (cudaStream_t)stream);
 }
 
+nsm_status nsm_motion_vectors(const nsm_gbuffer* g, const nsm_camera* cams, int32_t t_frames,
+                              int32_t h, int32_t w, double* vec, uint8_t* valid, void* stream) {
+    clear_error();
+    if (!g || !cams || !vec || !valid || !g->d || !g->normal || !g->position)
+        return fail(NSM_ERR_ARG, "nsm_motion_vectors: null argument");
+    if (t_frames < 2 || h <= 0 || w <= 0) return fail(NSM_ERR_ARG, "nsm_motion_vectors: need >= 2 frames");
+    if (g->dtype != NSM_F32 && g->dtype != NSM_F64)
+        return fail(NSM_ERR_ARG, "G-buffer planes must be F32 or F64");
+    for (int k = 0; k < t_frames - 1; ++k)
+        if (cams[k].height != h || cams[k].width != w)  // raster.py:337-338
+            return fail(NSM_ERR_ARG, "motion vectors need equal resolutions");
+    return launch_motion(g, cams, t_frames, h, w, vec, valid, (cudaStream_t)stream);
+}
+
+nsm_status nsm_temporal_instability(const float* vis, const double* vec, const uint8_t* valid,
+                                    int32_t t_frames, int32_t h, int32_t w, double alpha, double* acc,
+                                    uint64_t* count, void* stream) {
+    clear_error();
+    if (!vis || !vec || !valid || !acc || !count) return fail(NSM_ERR_ARG, "nsm_temporal_instability: null argument");
+    if (t_frames < 2) return fail(NSM_ERR_ARG, "need at least two frames");  // analysis.py:353-354
+    if (h <= 0 || w <= 0) return fail(NSM_ERR_ARG, "nsm_temporal_instability: empty frames");
+    return launch_instability(vis, vec, valid, t_frames, h, w, alpha, acc, (unsigned long long*)count,
+                              (cudaStream_t)stream);
+}
+
 }  // extern "C"

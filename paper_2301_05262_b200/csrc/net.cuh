@@ -59,6 +59,11 @@ void launch_fill_i64(int64_t* p, int n, int64_t v, cudaStream_t st);
 nsm_status launch_blocker(const nsm_gbuffer* g, const float* sm, int64_t sm_stride, const nsm_frame* frames,
                           int32_t n, int32_t h, int32_t w, int32_t radius, float* out, int64_t* first_bad,
                           cudaStream_t st);
+nsm_status launch_motion(const nsm_gbuffer* g, const nsm_camera* cams, int t_frames, int h, int w,
+                         double* vec, uint8_t* valid, cudaStream_t st);
+nsm_status launch_instability(const float* vis, const double* vec, const uint8_t* valid, int t_frames,
+                              int h, int w, double alpha, double* acc, unsigned long long* cnt,
+                              cudaStream_t st);
 nsm_status launch_render_gbuffer(const double* prims, int32_t n_prims, const nsm_camera* cam,
                                  float* d, float* normal, float* position, cudaStream_t st);
 nsm_status launch_render_shadowmap(const double* prims, int32_t n_prims,

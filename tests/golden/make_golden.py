@@ -21,6 +21,10 @@ Fixtures (all ``np.savez_compressed``):
   soft light, explicit bias, size_index 3: features + indices.
 * ``canon.npz``  -- the reference test-suite's canonical scene fixture
   (conftest.small_buffers: 64x128, SM 256^2, size_index 2).
+* ``temporal.npz`` -- a 4-frame sequence (48x80, moving camera, light and
+  one object, as config 4 at small size): reference ``motion_vectors`` per
+  consecutive pair on the fp32-rounded G-buffers and reference
+  ``temporal_instability`` (alpha_t 3) of seeded smooth fp32 frames.
 * ``nets.npz``   -- ``network.forward`` on random planes for a spread of
   ``NetworkConfig``s (layers 2..6, in_channels 5, plain mode, channel cap,
   base 8) with random non-zero biases; weights included.
@@ -226,7 +230,51 @@ def make_penumbra():
     print("penumbra:", n)
 
 
+def make_temporal():
+    from shadowkit import analysis
+    rng = np.random.default_rng(np.random.SeedSequence([5, 0x7E]))
+    base = scenes.random_scene(16, seed=5, emitter_radius_m=0.2)
+    dirs = [scenes._unit(rng.normal(size=3)) for _ in range(3)]
+    mover = 3
+    t_frames, res = 4, (48, 80)
+    rec, gbufs, cams = {}, [], []
+    for t in range(t_frames):
+        step = 0.05 * t
+        objs = list(base.objects)
+        p = np.asarray(objs[mover].params, dtype=np.float64)
+        objs[mover] = (scenes.sphere(p[0:3] + step * dirs[1], p[3]) if objs[mover].kind == scenes.KIND_SPHERE
+                       else scenes.box(p[0:3] + step * dirs[1], p[3:6] + step * dirs[1]))
+        spec = scenes.SceneSpec(tuple(objs), base.emitter_center + step * dirs[0], 0.2)
+        fr = scenes.make_frame(spec, res, (128, 128),
+                               camera_pos=np.asarray(scenes.CAMERA_POS) + step * dirs[2])
+        sc = to_reference_scene(spec)
+        cam = to_reference_camera(fr.camera)
+        g = raster.render_gbuffer(sc, cam, sc.emitter)
+        d32, n32, p32 = (g.d.astype(np.float32), g.normal.astype(np.float32),
+                         g.position.astype(np.float32))
+        gbufs.append(raster.GBuffer(d=d32.astype(np.float64), normal=n32.astype(np.float64),
+                                    position=p32.astype(np.float64), n_e=g.n_e, z_f=g.z_f,
+                                    c_e=g.c_e, c_c=g.c_c, coverage=g.coverage, camera=cam))
+        cams.append(cam)
+        rec[f"d{t}"], rec[f"normal{t}"], rec[f"position{t}"] = d32, n32, p32
+        rec.update(camera_record(cam, f"cam{t}"))
+    motions = [raster.motion_vectors(gbufs[t], cams[t - 1], gbufs[t - 1]) for t in range(1, t_frames)]
+    ys, xs = np.mgrid[0:res[0], 0:res[1]]
+    frames = [(0.5 + 0.4 * np.sin(0.11 * xs + 0.07 * ys + 0.3 * t)
+               + rng.normal(0.0, 0.02, size=res)).astype(np.float32) for t in range(t_frames)]
+    rep = analysis.temporal_instability([f.astype(np.float64) for f in frames], motions, 3.0)
+    for k, m in enumerate(motions):
+        rec[f"vec{k}"], rec[f"valid{k}"] = m.vectors, m.valid
+    static = raster.motion_vectors(gbufs[0], cams[0], gbufs[0])
+    rec.update(frames=np.stack(frames), E=np.float64(rep.instability),
+               valid_pixels=np.int64(rep.valid_pixels), rejected=np.float64(rep.rejected_fraction),
+               static_vec=static.vectors, static_valid=static.valid, t_frames=np.int64(t_frames))
+    np.savez_compressed(os.path.join(HERE, "temporal.npz"), **rec)
+    print("temporal: valid", [int(m.valid.sum()) for m in motions], "E", rep.instability)
+
+
 if __name__ == "__main__":
+    make_temporal()
     make_penumbra()
     make_cfg1()
     make_variants()

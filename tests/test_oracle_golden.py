@@ -151,3 +151,27 @@ def test_blocker_plane_point_light_is_zero():
     p2 = ob.blocker_plane(r["d"], r["position"], z_f, cov, r["sm"], golden_view(r), float(r["bias"]),
                           4.0, golden_camera(r).focal_px)
     assert np.all(p2[~cov] == 0) and np.all(p2 >= 0) and (p2 > 0).mean() > 0.05
+
+
+def test_oracle_temporal_matches_reference():
+    """oracle.temporal vs reference motion_vectors / temporal_instability
+    (raster.py:330-358, analysis.py:350-377) on the golden sequence."""
+    from oracle import temporal as ot
+    g = load_golden("temporal")
+    t = int(g["t_frames"])
+    vs, oks = [], []
+    for k in range(1, t):
+        v, ok = ot.motion_vectors(g[f"position{k}"], g[f"normal{k}"], g[f"d{k}"] > 0, g[f"d{k - 1}"],
+                                  g[f"normal{k - 1}"], g[f"d{k - 1}"] > 0, golden_camera(g, f"cam{k - 1}"))
+        assert np.max(np.abs(v - g[f"vec{k - 1}"])) < 1e-12
+        np.testing.assert_array_equal(ok, g[f"valid{k - 1}"])
+        vs.append(v)
+        oks.append(ok)
+    E, n, rej = ot.temporal_instability(list(g["frames"]), vs, oks, 3.0)
+    assert n == int(g["valid_pixels"]) and rej == float(g["rejected"])
+    assert abs(E - float(g["E"])) <= 1e-13 * abs(float(g["E"]))
+    # static pair: identity vectors, valid == coverage (test_raster.py:219-223)
+    v, ok = ot.motion_vectors(g["position0"], g["normal0"], g["d0"] > 0, g["d0"], g["normal0"],
+                              g["d0"] > 0, golden_camera(g, "cam0"))
+    np.testing.assert_array_equal(ok, g["static_valid"])
+    assert np.max(np.abs(v - g["static_vec"])) < 1e-12
