@@ -25,6 +25,15 @@ Fixtures (all ``np.savez_compressed``):
   one object, as config 4 at small size): reference ``motion_vectors`` per
   consecutive pair on the fp32-rounded G-buffers and reference
   ``temporal_instability`` (alpha_t 3) of seeded smooth fp32 frames.
+* ``sensitivity.npz`` -- reference ``analysis.sensitivity_report`` (phi =
+  reference ``network.forward``, rng default_rng(7), repeats 2) on three
+  32x48 crops of the cfg1 feature stack, and ``training._eval_mse`` of the
+  same stacks against seeded targets.
+* ``dataset_small/`` + ``dataset_small_ref.npz`` -- a 3-frame dataset written
+  by the reference's own ``dataset.generate_dataset`` (32x48, moving camera,
+  1 perturbation, sizes 0/2, 4 spp) and the reference's readings of it:
+  ``load_feature_stack`` (size 2), ``load_gbuffer`` planes, the
+  ``cli._sequence_outputs`` visibility and the ``cmd_eval_temporal`` E.
 * ``nets.npz``   -- ``network.forward`` on random planes for a spread of
   ``NetworkConfig``s (layers 2..6, in_channels 5, plain mode, channel cap,
   base 8) with random non-zero biases; weights included.
@@ -273,7 +282,100 @@ def make_temporal():
     print("temporal: valid", [int(m.valid.sum()) for m in motions], "E", rep.instability)
 
 
+def make_sensitivity():
+    from shadowkit import analysis, training
+    feats = np.load(os.path.join(HERE, "cfg1.npz"))["features"]
+    stacks = [np.ascontiguousarray(feats[:, y:y + 32, x:x + 48]) for y, x in ((96, 80), (128, 144), (160, 40))]
+    cfg = network.NetworkConfig()
+    w = network.init_weights(cfg, np.random.default_rng(np.random.SeedSequence([0, 0x11])))
+
+    def phi(stack):
+        with ad.no_grad():
+            return network.forward(w, cfg, stack).data[0]
+
+    rep = analysis.sensitivity_report(phi, stacks, raster.FEATURE_CHANNELS, repeats=2,
+                                      rng=np.random.default_rng(7))
+    trng = np.random.default_rng(8)
+    targets = [trng.uniform(0, 1, size=(32, 48)).astype(np.float32) for _ in stacks]
+    samples = [training.TrainingSample((s,), t, 0.0) for s, t in zip(stacks, targets)]
+    m = training._eval_mse(w, cfg, samples)
+    np.savez_compressed(os.path.join(HERE, "sensitivity.npz"), stacks=np.stack(stacks),
+                        targets=np.stack(targets), absolute=rep.absolute, relative=rep.relative,
+                        heldout_mse=np.float64(m))
+    print("sensitivity:", rep.absolute, "mse", m)
+
+
+SMALL_SCENE = """
+[scene]
+objects = [
+  { type = "plane", point = [0, 0, 0], normal = [0, 1, 0], half_extent = [5, 5] },
+  { type = "sphere", center = [0.3, 0.6, 0.2], radius = 0.5 },
+  { type = "box", min = [-1.2, 0.0, -0.4], max = [-0.6, 0.9, 0.3] },
+]
+[emitter]
+center = [3.0, 5.0, 2.0]
+size_index = 2.0
+[camera]
+position = [0.0, 3.0, -6.0]
+look_at = [0.0, 0.0, 0.0]
+fov_deg = 60.0
+resolution = [32, 48]
+[perturbation]
+count = 1
+"""
+
+SMALL_TRAJ = """
+[[camera_keys]]
+time = 0.0
+position = [0.0, 3.0, -6.0]
+look_at = [0.0, 0.0, 0.0]
+[[camera_keys]]
+time = 1.0
+position = [0.3, 3.1, -5.9]
+look_at = [0.0, 0.0, 0.0]
+"""
+
+
+def make_dataset():
+    import shutil
+    import tempfile
+    from shadowkit import analysis, dataset
+    out = os.path.join(HERE, "dataset_small")
+    shutil.rmtree(out, ignore_errors=True)
+    with tempfile.TemporaryDirectory() as tmp:
+        sp, tp = os.path.join(tmp, "scene.toml"), os.path.join(tmp, "traj.toml")
+        open(sp, "w").write(SMALL_SCENE)
+        open(tp, "w").write(SMALL_TRAJ)
+        st = dataset.GenerateSettings(frames=3, spp=4, msaa=1, sizes=(0.0, 2.0), shadow_res=(128, 128),
+                                      perturbations=1, seed=0)
+        dataset.generate_dataset(sp, tp, out, st)
+    for root, _, files in os.walk(out):
+        for f in files:
+            if f.endswith(".png"):
+                os.remove(os.path.join(root, f))
+    m = dataset.load_manifest(out)
+    cfg = network.NetworkConfig()
+    w = network.init_weights(cfg, np.random.default_rng(np.random.SeedSequence([0, 0x11])))
+    vis = []
+    for fi in range(len(m.frames)):
+        stack = dataset.load_feature_stack(m, fi, 0, 2.0)
+        with ad.no_grad():
+            vis.append(network.forward(w, cfg, stack.data).data[0].astype(np.float64))
+    gb = [dataset.load_gbuffer(m, i) for i in range(len(vis))]
+    motions = [raster.motion_vectors(gb[t], gb[t - 1].camera, gb[t - 1]) for t in range(1, len(vis))]
+    rep = analysis.temporal_instability(vis, motions, 3.0)
+    fs = dataset.load_feature_stack(m, 1, 1, 2.0)
+    np.savez_compressed(os.path.join(HERE, "dataset_small_ref.npz"), vis=np.stack(vis).astype(np.float32),
+                        E=np.float64(rep.instability), valid_pixels=np.int64(rep.valid_pixels),
+                        stack_1_1_s2=fs.data, coverage_1=fs.coverage,
+                        gb_position_2=gb[2].position, gb_z_f_2=gb[2].z_f,
+                        target_2_s2=dataset.load_target(m, 2, 2.0))
+    print("dataset: frames", len(vis), "E", rep.instability, "valid", rep.valid_pixels)
+
+
 if __name__ == "__main__":
+    make_dataset()
+    make_sensitivity()
     make_temporal()
     make_penumbra()
     make_cfg1()

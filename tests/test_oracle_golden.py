@@ -175,3 +175,28 @@ def test_oracle_temporal_matches_reference():
                               g["d0"] > 0, golden_camera(g, "cam0"))
     np.testing.assert_array_equal(ok, g["static_valid"])
     assert np.max(np.abs(v - g["static_vec"])) < 1e-12
+
+
+def test_sensitivity_host_logic_with_oracle_phi():
+    """analysis.sensitivity_report / heldout_mse host logic (rng order,
+    normalisation) with the oracle forward as phi reproduces the reference's
+    report (analysis.py:100-139, training.py:179-189)."""
+    from paper_2301_05262_b200 import analysis
+    from paper_2301_05262_b200.raster import FEATURE_CHANNELS
+    g = load_golden("sensitivity")
+    _, w = _weights_for((5, 16, 4, 1, 256), [0, 0x11])
+    wd = {k: v.data for k, v in w.items()}
+
+    def phi(s):
+        return on.forward(wd, s)[0]
+
+    stacks = list(g["stacks"])
+    rep = analysis.sensitivity_report(phi, stacks, FEATURE_CHANNELS, repeats=2,
+                                      rng=np.random.default_rng(7))
+    np.testing.assert_allclose(rep.absolute, g["absolute"], rtol=1e-5)
+    np.testing.assert_allclose(rep.relative, g["relative"], rtol=1e-5)
+    m = analysis.heldout_mse(phi, stacks, list(g["targets"]))
+    assert abs(m - float(g["heldout_mse"])) <= 1e-6 * float(g["heldout_mse"])
+    with pytest.raises(analysis.ZeroVarianceChannel):
+        analysis.channel_sensitivity(phi, [np.zeros((4, 16, 16), np.float32)], 0)
+    assert math.isnan(analysis.heldout_mse(phi, [], []))
