@@ -15,6 +15,7 @@
 // upsampling, skip sums, the head and the sigmoid run in fp32 registers.
 #include <algorithm>
 #include <type_traits>
+#include <utility>
 #include <cmath>
 #include <vector>
 
@@ -40,6 +41,33 @@ int chunk_frames() {
     }
     return v;
 }
+// Kernel launches of the fused path go through launch_pdl: programmatic
+// stream serialisation lets each kernel's prologue overlap its predecessor's
+// tail (the kernels call pdl_trigger / pdl_wait).  NSM_PDL=0 disables it.
+bool pdl_enabled() {
+    static int v = -1;
+    if (v < 0) {
+        const char* e = getenv("NSM_PDL");
+        v = e ? atoi(e) : 1;
+    }
+    return v != 0;
+}
+
+template <typename... KArgs, typename... Args>
+void launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, Args&&... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl_enabled() ? 1 : 0;
+    cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
+
 constexpr int E0_TH = 16, E0_TW = 64;  // level-0 output tile (enc0 / dec0)
 constexpr int E0_IR = E0_TH + 2, E0_IC = E0_TW + 2;
 constexpr int E0_PLANE = plane_bytes(E0_IR * E0_IC, 2);
@@ -546,6 +574,8 @@ __global__ void __launch_bounds__(kSrc == 2 ? kE0Threads : kL0Threads, 1) enc0_k
     const __grid_constant__ Enc0Args a, const __grid_constant__ GbufMaps tm, int total) {
     constexpr int kProd = kSrc == 2 ? kE0Prod : kL0Prod;
     constexpr int kThreads = kSrc == 2 ? kE0Threads : kL0Threads;
+    if (threadIdx.x == 0) pdl_trigger();
+    pdl_wait();
     if (kSrc == 2) {
         if (threadIdx.x < kProd) asm volatile("setmaxnreg.dec.sync.aligned.u32 88;");
         else asm volatile("setmaxnreg.inc.sync.aligned.u32 128;");
@@ -695,6 +725,8 @@ template <typename T>
 __global__ void __launch_bounds__(kL0Threads, 1) dec0_kernel(const __grid_constant__ Dec0Args a,
                                                              const __grid_constant__ CUtensorMap tm, int total) {
     const int H1 = a.H0 / 2, W1 = a.W0 / 2;
+    if (threadIdx.x == 0) pdl_trigger();
+    pdl_wait();
     if (threadIdx.x < kL0Prod) {
         extern __shared__ __align__(128) uint8_t smem[];
         uint8_t* stg = smem + 2 * E0_SMEM;
@@ -863,6 +895,8 @@ __global__ void __launch_bounds__(kL0Threads, 1) dec0_kernel(const __grid_consta
 // reproduces the reference's edge clamp (_upsample_taps, autodiff.py:258-264).
 __global__ void __launch_bounds__(128) recon_kernel(const float* __restrict__ y, int H0, int W0, int h,
                                                      int w, int n, void* __restrict__ out, int f16) {
+    if (threadIdx.x == 0) pdl_trigger();
+    pdl_wait();
     const int X = blockIdx.x * blockDim.x + threadIdx.x;
     const int Y = blockIdx.y;
     const int f = blockIdx.z;
@@ -1024,6 +1058,7 @@ __global__ void __launch_bounds__((NPW + 9) * 32, 1) level_kernel(const __grid_c
         f = t / (ntx * nty);
     };
 
+    if (tid == 0) pdl_trigger();
     if (warp == EW0) tmem_alloc<G::TCOLS>(tptr);
     if (tid == 0) {
         for (int i = 0; i < 2; ++i) {
@@ -1051,6 +1086,7 @@ __global__ void __launch_bounds__((NPW + 9) * 32, 1) level_kernel(const __grid_c
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = *tptr;
+    pdl_wait();                      // prologue above overlaps the previous kernel's tail
 
     if (warp < NPW) {
         // ------------------------------------------------------------ producer
@@ -1364,7 +1400,7 @@ nsm_status launch_level(const LevelArgs& a, int nf, cudaStream_t st, const char*
     static const int dbg = getenv("NSM_LEVEL_DBG") ? atoi(getenv("NSM_LEVEL_DBG")) : 0;
     const_cast<LevelArgs&>(a).dbg = dbg;
     NSM_PROF(name, st);
-    k<<<grid, (NPW + 9) * 32, G::SMEM, st>>>(a, tin, tlo, total);
+    launch_pdl(k, dim3(grid), dim3((NPW + 9) * 32), G::SMEM, st, a, tin, tlo, total);
     return NSM_OK;
 }
 
@@ -1469,9 +1505,9 @@ nsm_status run_l0(const Plan& p, const Bufs& b, const Enc0Args& e0, const GbufMa
     const int pgrid = std::min(total, num_sms());
     {
         NSM_PROF("enc0_fused", st);
-        if (src == 2) enc0_kernel<T, 2><<<pgrid, kE0Threads, ENC0_SMEM_TMA, st>>>(e0, tm, total);
-        else if (src == 1) enc0_kernel<T, 1><<<pgrid, kL0Threads, 2 * E0_SMEM, st>>>(e0, tm, total);
-        else enc0_kernel<T, 0><<<pgrid, kL0Threads, 2 * E0_SMEM, st>>>(e0, tm, total);
+        if (src == 2) launch_pdl(enc0_kernel<T, 2>, dim3(pgrid), dim3(kE0Threads), ENC0_SMEM_TMA, st, e0, tm, total);
+        else if (src == 1) launch_pdl(enc0_kernel<T, 1>, dim3(pgrid), dim3(kL0Threads), 2 * E0_SMEM, st, e0, tm, total);
+        else launch_pdl(enc0_kernel<T, 0>, dim3(pgrid), dim3(kL0Threads), 2 * E0_SMEM, st, e0, tm, total);
     }
     nsm_status s = run_levels<T>(p, b, nf, H0, W0, st);
     if (s != NSM_OK) return s;
@@ -1485,12 +1521,12 @@ nsm_status run_l0(const Plan& p, const Bufs& b, const Enc0Args& e0, const GbufMa
         if (!encode_nhwc_map4(b.d1, std::is_same<T, __nv_bfloat16>::value, 16, H0 / 2, W0 / 2, nf, D0_LC, D0_LR, &dm))
             return fail(NSM_ERR_CUDA, "dec0: TMA tensor map encoding failed");
         NSM_PROF("dec0_fused", st);
-        dec0_kernel<T><<<pgrid, kL0Threads, DEC0_SMEM, st>>>(d, dm, total);
+        launch_pdl(dec0_kernel<T>, dim3(pgrid), dim3(kL0Threads), DEC0_SMEM, st, d, dm, total);
     }
     {
         dim3 g2((W0 + 127) / 128, H0, nf);
         NSM_PROF("recon", st);
-        recon_kernel<<<g2, 128, 0, st>>>(b.y, H0, W0, h, w, nf, y, y_f16);
+        launch_pdl(recon_kernel, g2, dim3(128), 0, st, (const float*)b.y, H0, W0, h, w, nf, y, y_f16);
     }
     return NSM_OK;
 }

@@ -124,6 +124,14 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
         : "memory");
 }
 
+// Programmatic dependent launch: let the next kernel of the stream start its
+// prologue while this grid drains (trigger), and block until the previous
+// grid has completed and its writes are visible (wait).  Every CTA of a
+// PDL-launched kernel must execute pdl_wait before touching data another
+// kernel of the chain reads or writes.
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 __device__ __forceinline__ void fence_proxy_async() {
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
