@@ -1,5 +1,5 @@
 """Summarise warp-stall samples of an ncu report's source page by SASS
-region: python tools/ncu_stalls.py report.ncu-rep [top_n]"""
+region: python tools/ncu_stalls.py report.ncu-rep [top_n] [kernel_regex]"""
 import csv
 import io
 import subprocess
@@ -8,11 +8,13 @@ from collections import Counter
 
 rep = sys.argv[1]
 top = int(sys.argv[2]) if len(sys.argv) > 2 else 40
-out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass"],
-                     capture_output=True, text=True).stdout
-lines = out.splitlines()
-rows = list(csv.reader(io.StringIO("\n".join(lines[1:]))))
-hdr, rows = rows[0], rows[1:]
+kfilt = ["-k", "regex:" + sys.argv[3]] if len(sys.argv) > 3 else []
+out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass",
+                      "--launch-count", "1"] + kfilt, capture_output=True, text=True).stdout
+lines = [ln for ln in out.splitlines() if not ln.startswith('"Kernel Name"')]
+rows = list(csv.reader(io.StringIO("\n".join(lines))))
+hdr = rows[0]
+rows = [r for r in rows[1:] if len(r) == len(hdr) and r[0] != "Address"]
 ix = {h: i for i, h in enumerate(hdr)}
 stall_cols = [h for h in hdr if h.startswith("stall_") and "Not Issued" not in h]
 tot = Counter()
