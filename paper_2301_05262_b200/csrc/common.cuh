@@ -114,10 +114,17 @@ __device__ __forceinline__ bool texel_fast(const FrameK& f, double px, double py
 // except within a few fp64 ulps of a half-texel tie (never observed).
 __device__ __forceinline__ bool texel_fused(const FrameK& f, float px, float py, float pz, int& ri,
                                             int& ci) {
-    const double x = px, y = py, z = pz;
-    const double zc = fma(f.kz[0], x, fma(f.kz[1], y, fma(f.kz[2], z, f.kz[3])));
-    const double xs = fma(f.kx[0], x, fma(f.kx[1], y, fma(f.kx[2], z, f.kx[3])));
-    const double ys = fma(f.ky[0], x, fma(f.ky[1], y, fma(f.ky[2], z, f.ky[3])));
+    // fp32 -> fp64 without the .ftz flush fast-math would add (G-buffer
+    // values are normal or zero)
+    double x, y, z;
+    asm("cvt.f64.f32 %0, %1;" : "=d"(x) : "f"(px));
+    asm("cvt.f64.f32 %0, %1;" : "=d"(y) : "f"(py));
+    asm("cvt.f64.f32 %0, %1;" : "=d"(z) : "f"(pz));
+    // one constant per DFMA (the second operand comes from a uniform
+    // register): the affine offsets k[3] are added last
+    const double zc = fma(f.kz[0], x, fma(f.kz[1], y, f.kz[2] * z)) + f.kz[3];
+    const double xs = fma(f.kx[0], x, fma(f.kx[1], y, f.kx[2] * z)) + f.kx[3];
+    const double ys = fma(f.ky[0], x, fma(f.ky[1], y, f.ky[2] * z)) + f.ky[3];
     double r;
     asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(zc));
     double e = fma(-zc, r, 1.0);

@@ -205,10 +205,16 @@ __device__ __forceinline__ float4 pixel_features(const FrameK& F, const GBufK& g
 // dx-shifted A fragments are loaded once and applied to the three output
 // rows that need them, so ldmatrix traffic is 3 instead of 9 loads per row.
 // Accumulators start at the conv bias (saves the epilogue's bias adds).
-template <typename T, int ROWS, class Epi>
+struct NoRowHook {
+    __device__ void operator()(int) const {}
+};
+
+// hook(ir) runs before input row ir is read (e.g. to wait for the producers
+// to finish the half of the tile that holds it).
+template <typename T, int ROWS, class Epi, class Hook = NoRowHook>
 __device__ __forceinline__ void conv3_strip16(uint32_t sbase, int plane, int rowpix, int r0, int sx,
                                               const uint32_t (&B3)[9][2][2], const float (&binit)[2][2],
-                                              Epi&& epi) {
+                                              Epi&& epi, Hook&& hook = Hook{}) {
     const int lane = threadIdx.x & 31;
     const int lm = lane >> 3, li = lane & 7;
     const uint32_t a_off = (lm >> 1) * plane + (li + 8 * (lm & 1)) * 16;
@@ -221,6 +227,7 @@ __device__ __forceinline__ void conv3_strip16(uint32_t sbase, int plane, int row
             for (int e = 0; e < 4; ++e) acc[s][n][e] = binit[n][e & 1];
 #pragma unroll
     for (int ir = 0; ir < ROWS + 2; ++ir) {
+        hook(ir);
         uint32_t A[3][4];
 #pragma unroll
         for (int dx = 0; dx < 3; ++dx)
@@ -430,34 +437,55 @@ __device__ __forceinline__ void produce_features(const Enc0Args& a, uint8_t* buf
 // TMA producer: one elected thread streams half-tiles of the seven G-buffer
 // planes into two SMEM stages (mbarrier complete_tx); the producer warps turn
 // each staged half into features while the next half is in flight.
-// 16 producer warps (features) + 4 tensor-core warps; setmaxnreg moves the
-// register budget from the producers (96 -> 88) to the MMA warps (96 -> 128);
-// .inc can only claim what .dec released within the CTA (more deadlocks).
-constexpr int kE0Prod = 512, kE0Threads = 640;
+// Each producer thread owns 4 pixels of one staged row of a half-tile:
+// threads 0-575 an interior quad (halo cols 4k-2 .. 4k+1, k = 1..32: level-0
+// pixels 2k-1 and 2k), warp 18 the row's two edge pairs (halo cols 0,1 and
+// 130,131: level-0 pixels 0 and 65).  A half is then one vectorised pass
+// (LDS.128 per plane) over 18 x 33 threads with all index math hoisted.
+// 19 producer warps + 4 tensor-core warps; setmaxnreg moves registers from
+// the producers (-> 72) to the MMA warps (-> 112); the budget is checked
+// against the kernel's launch register count on the host (run_l0).
+constexpr int kE0Prod = 608, kE0Threads = 736;
+constexpr int kE0ProdRegs = 72, kE0MmaRegs = 112;
+constexpr int ST_QC = E0_TW / 2;                     // interior quads per staged row (32)
+static_assert(ST_ROWS * (ST_QC + 1) <= kE0Prod, "one quad per producer thread per half-tile");
+static_assert(ST_ROWS * ST_QC % 32 == 0, "edge threads form their own warp");
+static_assert(ST_ROWS % 2 == 0, "a half-tile holds whole level-0 rows");
 
-// Per-pixel producer state carried from the A to the B phase of a half-tile.
-template <int K>
-struct HalfRegs {
-    float izf[K], c2[K], c3[K], look[K];
+// Per-quad producer state carried from the A to the B phase of a half-tile:
+// the gathered occluder depth (< 0: uncovered).  Phase A already writes
+// (ch2, ch3) into the tile and parks z_f (fp32) in the (ch0, ch1) slot.
+struct QuadRegs {
+    float look[4];
 };
 
 template <typename T>
 __device__ __forceinline__ void produce_features_tma(const Enc0Args& a, const GbufMaps& tm, int total) {
     // Software pipeline over half-tiles q (two per tile):
-    //   A(q): staged planes -> texel (fp64), 1/z_f, c_e + s, c_c / d in
-    //         registers, and the shadow-map gather issued (LDG in flight)
+    //   A(q): staged planes -> texel (fp64), z_f, (c_e + s, c_c / d) packed,
+    //         the shadow-map gather issued (LDG in flight)
     //   TMA(q+2) into the stage A(q) just released
     //   B(q-1): gathered occluder depth -> ch0, ch1, pack, STS into the
     //         tile's feature buffer
     // so the gather latency of half q overlaps B(q-1) and A(q+1), and the
     // G-buffer of half q+2 streams in meanwhile.
     extern __shared__ __align__(128) uint8_t smem[];
-    constexpr int K = (ST_PIX + kE0Prod - 1) / kE0Prod;
     uint8_t* stage = smem + 2 * E0_SMEM;
     uint64_t* full = reinterpret_cast<uint64_t*>(stage + 2 * ST_BYTES);
     const int ptid = threadIdx.x;
     const int mytiles = (int)blockIdx.x < total ? (total - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x : 0;
     const int nh = 2 * mytiles;
+    // tile-invariant geometry of this thread's 4 pixels: halo columns
+    // hc_lo + {0, 1} (level-0 halo pixel lo) and hc_hi + {0, 1} (pixel hi)
+    const bool edge = ptid >= ST_ROWS * ST_QC;
+    const bool active = ptid < ST_ROWS * (ST_QC + 1);
+    const int qy = edge ? ptid - ST_ROWS * ST_QC : ptid / ST_QC;
+    const int qk = edge ? 0 : ptid - qy * ST_QC + 1;
+    const int px_lo = edge ? 0 : 2 * qk - 1, px_hi = edge ? E0_IC - 1 : 2 * qk;
+    // staged col = halo col + 2; halo col of pixel e: 2 px + (e & 1)
+    const int lds_lo = qy * ST_TCOLS * 4 + 8 + 8 * px_lo, lds_hi = qy * ST_TCOLS * 4 + 8 + 8 * px_hi;
+    const int sts_row = (qy & 1) * E0_PLANE + (qy >> 1) * E0_IC * 16;
+    const int slot_lo = sts_row + px_lo * 16, slot_hi = sts_row + px_hi * 16;
     auto issue = [&](int q) {
         const L0Tile tl = l0_tile(blockIdx.x + (q >> 1) * gridDim.x, a.H0, a.W0);
         const int sidx = q & 1;
@@ -478,76 +506,96 @@ __device__ __forceinline__ void produce_features_tma(const Enc0Args& a, const Gb
         if (nh > 0) issue(0);
         if (nh > 1) issue(1);
     }
-    auto phaseA = [&](int q, HalfRegs<K>& R) {
+    auto phaseA = [&](int q, QuadRegs& R) {
         const L0Tile tl = l0_tile(blockIdx.x + (q >> 1) * gridDim.x, a.H0, a.W0);
-        const int sidx = q & 1, hh = q & 1;
-        const FrameK& F = a.tab.f[tl.f];
-        const float* smf = a.sm + tl.f * a.sm_stride;
+        const int sidx = q & 1;
         mbar_wait(&full[sidx], (q >> 1) & 1);
-        const float* sd = reinterpret_cast<const float*>(stage + sidx * ST_BYTES);
-        const float* sn = reinterpret_cast<const float*>(stage + sidx * ST_BYTES + ST_OFF_N);
-        const float* sp = reinterpret_cast<const float*>(stage + sidx * ST_BYTES + ST_OFF_P);
-        const float ecx = F.fec[0], ecy = F.fec[1], ecz = F.fec[2];
-#pragma unroll
-        for (int j = 0; j < K; ++j) {
-            const int i = ptid + j * kE0Prod;
-            R.izf[j] = 0.f;
-            R.c2[j] = 0.f;
-            R.c3[j] = 0.f;
-            R.look[j] = -1.f;                       // < 0: uncovered / outside
-            if (i >= ST_PIX) continue;
-            const int o = i + 4 * (i / ST_COLS) + 2;      // staged index (136-wide rows)
-            const float d = sd[o];
-            if (!(d > 0.f)) continue;
-            const float px = sp[o], py = sp[ST_TPIX + o], pz = sp[2 * ST_TPIX + o];
-            int ri, ci;
-            if (!texel_fused(F, px, py, pz, ri, ci)) {
-                const int ry = i / ST_COLS;
-                atomic_min_i64(a.first_bad + tl.f,
-                               (int64_t)(2 * tl.ty0 - 2 + ST_ROWS * hh + ry) * a.w + (2 * tl.tx0 - 2 + i - ry * ST_COLS));
+        if (!active) return;
+        const FrameK& F = a.tab.f[tl.f];
+        // 32-bit texel index: NSM_MAX_FRAMES_PER_LAUNCH maps of <= 2^26 texels
+        const int sm_off = tl.f * (int)a.sm_stride;
+        const uint8_t* sb = stage + sidx * ST_BYTES;
+        float dv[4], xv[4], yv[4], zv[4], nxv[4], nyv[4], nzv[4];
+        auto ld4 = [&](int off, float (&v)[4]) {
+            if (!edge) {                                   // warp-uniform
+                const float4 t = *reinterpret_cast<const float4*>(sb + off + lds_lo);
+                v[0] = t.x, v[1] = t.y, v[2] = t.z, v[3] = t.w;
+            } else {
+                const float2 l = *reinterpret_cast<const float2*>(sb + off + lds_lo);
+                const float2 r = *reinterpret_cast<const float2*>(sb + off + lds_hi);
+                v[0] = l.x, v[1] = l.y, v[2] = r.x, v[3] = r.y;
             }
-            R.look[j] = __ldg(smf + (int64_t)ri * F.ws + ci);   // consumed one phase later
-            const float nx = sn[o], ny = sn[ST_TPIX + o], nz = sn[2 * ST_TPIX + o];
+        };
+        ld4(0, dv);
+        uint8_t* tdst = smem + ((q >> 1) & 1) * E0_SMEM + (q & 1) * (ST_ROWS / 2) * E0_IC * 16;
+        if (!(dv[0] > 0.f || dv[1] > 0.f || dv[2] > 0.f || dv[3] > 0.f)) {   // nothing covered
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                R.look[e] = -1.f;
+                *reinterpret_cast<uint2*>(tdst + (e < 2 ? slot_lo : slot_hi) + (e & 1) * 8) = make_uint2(0u, 0u);
+            }
+            return;
+        }
+        ld4(ST_OFF_P, xv);
+        ld4(ST_OFF_P + ST_PLANE, yv);
+        ld4(ST_OFF_P + 2 * ST_PLANE, zv);
+        ld4(ST_OFF_N, nxv);
+        ld4(ST_OFF_N + ST_PLANE, nyv);
+        ld4(ST_OFF_N + 2 * ST_PLANE, nzv);
+        const float ecx = F.fec[0], ecy = F.fec[1], ecz = F.fec[2];
+        const float cpx = F.fcp[0], cpy = F.fcp[1], cpz = F.fcp[2];
+        const float size = F.fsize;
+        const int ws = F.ws;
+        int bad = 0;
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+            const float d = dv[e], px = xv[e], py = yv[e], pz = zv[e];
+            const bool cov = d > 0.f;
+            int ri, ci;
+            const bool ok = texel_fused(F, px, py, pz, ri, ci);
+            bad |= (cov && !ok) << e;
+            R.look[e] = cov ? __ldg(a.sm + (sm_off + ri * ws + ci)) : -1.f;   // consumed one phase later
             const float tx = ecx - px, ty = ecy - py, tz = ecz - pz;
-            const float izf = rsqrtf(tx * tx + ty * ty + tz * tz);
+            const float l2 = fmaf(tx, tx, fmaf(ty, ty, tz * tz));
+            const float izf = rsqrtf(l2);
             // c_c = clip(n . -ray): the pixel ray is the direction camera -> hit
             // point (render_gbuffer places p on it), fp32 is ample here
-            const float dx = F.fcp[0] - px, dy = F.fcp[1] - py, dz = F.fcp[2] - pz;
-            const float cc = fminf(fmaxf((nx * dx + ny * dy + nz * dz) * rsqrtf(dx * dx + dy * dy + dz * dz), 0.f), 1.f);
-            R.izf[j] = izf;
-            R.c2[j] = fminf(fmaxf((nx * tx + ny * ty + nz * tz) * izf, 0.f), 1.f) + F.fsize;
-            R.c3[j] = __fdividef(cc, d);
+            const float dx = cpx - px, dy = cpy - py, dz = cpz - pz;
+            const float nx = nxv[e], ny = nyv[e], nz = nzv[e];
+            const float cc = __saturatef(fmaf(nx, dx, fmaf(ny, dy, nz * dz)) *
+                                         rsqrtf(fmaf(dx, dx, fmaf(dy, dy, dz * dz))));
+            const float c2 = __saturatef(fmaf(nx, tx, fmaf(ny, ty, nz * tz)) * izf) + size;
+            *reinterpret_cast<uint2*>(tdst + (e < 2 ? slot_lo : slot_hi) + (e & 1) * 8) =
+                make_uint2(__float_as_uint(l2 * izf), cov ? Elem<T>::pack(c2, __fdividef(cc, d)) : 0u);
+        }
+        if (bad) {   // FrustumError: the quad's leftmost bad pixel (raster.py:251-255)
+            const int e = __ffs(bad) - 1;
+            atomic_min_i64(a.first_bad + tl.f, (int64_t)(2 * tl.ty0 - 2 + ST_ROWS * (q & 1) + qy) * a.w +
+                                                   (2 * tl.tx0 - 2 + 2 * (e < 2 ? px_lo : px_hi) + (e & 1)));
         }
     };
-    auto phaseB = [&](int q, HalfRegs<K>& R) {
+    auto phaseB = [&](int q, const QuadRegs& R) {
+        if (!active) return;
         const L0Tile tl = l0_tile(blockIdx.x + (q >> 1) * gridDim.x, a.H0, a.W0);
-        const int hh = q & 1, sb = (q >> 1) & 1;
         const float bias = a.tab.f[tl.f].fbias;
-        uint8_t* buf = smem + sb * E0_SMEM;
+        uint8_t* dst = smem + ((q >> 1) & 1) * E0_SMEM + (q & 1) * (ST_ROWS / 2) * E0_IC * 16;
 #pragma unroll
-        for (int j = 0; j < K; ++j) {
-            const int i = ptid + j * kE0Prod;
-            if (i >= ST_PIX) continue;
-            const int ry = i / ST_COLS, rx = i - ry * ST_COLS;
-            float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-            const float look = R.look[j];
-            if (look >= 0.f) {
-                float ch0 = 0.f, ch1 = 1.f;
-                if (look < INFINITY) {                  // raster.py:262 (finite lookup)
-                    const float zf = 1.f / R.izf[j];
-                    const float m = fminf(look, zf);
-                    ch0 = (m - zf) + bias;
-                    ch1 = (m + bias) * R.izf[j];
-                }
-                v = make_float4(ch0, ch1, R.c2[j], R.c3[j]);
+        for (int e = 0; e < 4; ++e) {
+            uint32_t* slot = reinterpret_cast<uint32_t*>(dst + (e < 2 ? slot_lo : slot_hi) + (e & 1) * 8);
+            const float look = R.look[e], zf = __uint_as_float(*slot);
+            float ch0 = 0.f, ch1 = look >= 0.f ? 1.f : 0.f;
+            if (look >= 0.f && look < INFINITY) {           // raster.py:262 (finite lookup)
+                const float m = fminf(look, zf);
+                ch0 = (m - zf) + bias;
+                ch1 = __fdividef(m + bias, zf);
             }
-            const int trow = ST_ROWS * hh + ry;            // full-res row within the tile
-            const int p = (trow >> 1) * E0_IC + (rx >> 1);
-            *reinterpret_cast<uint2*>(buf + (trow & 1) * E0_PLANE + p * 16 + (rx & 1) * 8) =
-                make_uint2(Elem<T>::pack(v.x, v.y), Elem<T>::pack(v.z, v.w));
+            *slot = Elem<T>::pack(ch0, ch1);
         }
     };
-    auto step = [&](int q, HalfRegs<K>& RA, HalfRegs<K>& RB) {
+    auto step = [&](int q, QuadRegs& RA, QuadRegs& RB) {
+        // phase A of a tile's first half already writes (ch2, ch3) into the
+        // tile buffer, so it waits for the consumers to release it
+        if (!(q & 1) && q < nh && (q >> 1) >= 2) nbar_sync(3 + ((q >> 1) & 1), kE0Threads);
         if (q < nh && !(a.dbg & 1)) phaseA(q, RA);
         else if (q < nh) mbar_wait(&full[q & 1], (q >> 1) & 1);
         nbar_sync(5, kE0Prod);                     // stage q&1 fully consumed by A(q)
@@ -557,15 +605,18 @@ __device__ __forceinline__ void produce_features_tma(const Enc0Args& a, const Gb
         }
         if (q >= 1) {
             const int qb = q - 1, k = qb >> 1;
-            if (!(qb & 1) && k >= 2) nbar_sync(3 + (k & 1), kE0Threads);   // tile buffer free
             if (!(a.dbg & 1)) phaseB(qb, RB);
-            if (qb & 1) nbar_arrive(1 + (k & 1), kE0Threads);               // tile k complete
+            // level-0 rows 0-8 (half 0) / 9-17 (half 1) of tile k complete
+            nbar_arrive((qb & 1) ? 1 + (k & 1) : 6 + (k & 1), kE0Threads);
         }
     };
-    HalfRegs<K> R0, R1;
-    for (int q = 0; q <= nh; q += 2) {
-        step(q, R0, R1);
-        if (q + 1 <= nh) step(q + 1, R1, R0);
+    QuadRegs RA, RB;
+#pragma unroll 1
+    for (int q = 0; q <= nh; ++q) {
+        step(q, RA, RB);
+        const QuadRegs t = RA;
+        RA = RB;
+        RB = t;
     }
 }
 
@@ -577,8 +628,9 @@ __global__ void __launch_bounds__(kSrc == 2 ? kE0Threads : kL0Threads, 1) enc0_k
     if (threadIdx.x == 0) pdl_trigger();
     pdl_wait();
     if (kSrc == 2) {
-        if (threadIdx.x < kProd) asm volatile("setmaxnreg.dec.sync.aligned.u32 88;");
-        else asm volatile("setmaxnreg.inc.sync.aligned.u32 128;");
+        static_assert(kE0ProdRegs == 72 && kE0MmaRegs == 112, "keep the asm immediates in sync");
+        if (threadIdx.x < kProd) asm volatile("setmaxnreg.dec.sync.aligned.u32 72;");
+        else asm volatile("setmaxnreg.inc.sync.aligned.u32 112;");
     }
     constexpr int kRows = kSrc == 2 ? 16 : 8;        // output rows per consumer warp
     if (threadIdx.x < kProd) {
@@ -622,10 +674,13 @@ __global__ void __launch_bounds__(kSrc == 2 ? kE0Threads : kL0Threads, 1) enc0_k
             }
     }
     T* out = reinterpret_cast<T*>(a.out);
-    l0_consume_loop<kThreads>(total, [&](uint8_t* buf, int tile) {
+    auto consume = [&](uint8_t* buf, int tile, auto&& hook) {
             const L0Tile tl = l0_tile(tile, a.H0, a.W0);
             float pp[2][4];
-            if (a.dbg & 2) return;
+            if (a.dbg & 2) {
+                hook(E0_IR / 2);
+                return;
+            }
             conv3_strip16<T, kRows>(smem_u32(buf), E0_PLANE, E0_IC, r0, sx, B3, bias3, [&](int oo, float (&acc)[2][4]) {
                 uint32_t a1[4];
                 relu_pack_a<T>(acc, a1);
@@ -669,8 +724,26 @@ __global__ void __launch_bounds__(kSrc == 2 ? kE0Threads : kL0Threads, 1) enc0_k
                         }
                     }
                 }
+            }, hook);
+    };
+    if constexpr (kSrc == 2) {
+        extern __shared__ __align__(128) uint8_t smem[];
+        // the producers signal each half of a tile: rows 0-8 (barrier 6/7)
+        // and rows 9-17 (barrier 1/2), so the convolution starts one
+        // half-tile earlier
+        for (int k = 0;; ++k) {
+            const int tile = blockIdx.x + k * gridDim.x;
+            if (tile >= total) break;
+            const int s = k & 1;
+            nbar_sync(6 + s, kThreads);
+            consume(smem + s * E0_SMEM, tile, [&](int ir) {
+                if (ir == E0_IR / 2) nbar_sync(1 + s, kThreads);
             });
-    });
+            if (tile + 2 * (int)gridDim.x < total) nbar_arrive(3 + s, kThreads);
+        }
+    } else {
+        l0_consume_loop<kThreads>(total, [&](uint8_t* buf, int tile) { consume(buf, tile, NoRowHook{}); });
+    }
 }
 
 struct Dec0Args {
@@ -1499,6 +1572,13 @@ nsm_status run_l0(const Plan& p, const Bufs& b, const Enc0Args& e0, const GbufMa
         cudaFuncSetAttribute(enc0_kernel<T, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * E0_SMEM);
         cudaFuncSetAttribute(enc0_kernel<T, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, ENC0_SMEM_TMA);
         cudaFuncSetAttribute(dec0_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, DEC0_SMEM);
+        // setmaxnreg.inc blocks until .dec released enough of the CTA's
+        // launch allocation: refuse to launch a budget that could hang
+        cudaFuncAttributes fa{};
+        cudaFuncGetAttributes(&fa, enc0_kernel<T, 2>);
+        if (kE0Prod * kE0ProdRegs + (kE0Threads - kE0Prod) * kE0MmaRegs > fa.numRegs * kE0Threads)
+            return fail(NSM_ERR_CUDA, "enc0: register budget %d x %d + %d x %d exceeds launch allocation %d x %d",
+                        kE0Prod, kE0ProdRegs, kE0Threads - kE0Prod, kE0MmaRegs, kE0Threads, fa.numRegs);
         attr = true;
     }
     const int total = ((W0 + E0_TW - 1) / E0_TW) * ((H0 + E0_TH - 1) / E0_TH) * nf;
@@ -1604,6 +1684,9 @@ nsm_status infer_f16(const Plan& p, const nsm_gbuffer* g, const float* sm, int64
         return fail(NSM_ERR_UNSUPPORTED, "16-bit path derives z_f/c_e/c_c from the planes");
     const int Hp = round16(h), Wp = round16(w), H0 = Hp / 2, W0 = Wp / 2;
     const int nfmax = std::min(n, chunk_frames());
+    if (sm_stride * nfmax > INT32_MAX)   // the fused feature pass indexes a chunk's maps in 32 bits
+        return fail(NSM_ERR_UNSUPPORTED, "shadow maps of %lld texels x %d frames per pass exceed 2^31",
+                    (long long)sm_stride, nfmax);
     Bufs b = carve(ws, nfmax, H0, W0, 2);
     if (ws_bytes < b.bytes) return fail(NSM_ERR_ARG, "workspace too small (%zu < %zu)", ws_bytes, b.bytes);
     launch_fill_i64(first_bad, n, INT64_MAX, st);
