@@ -100,6 +100,38 @@ def test_batch_equals_single_frames():
         np.testing.assert_array_equal(y1[0], yb[i])
 
 
+def test_host_pipeline_matches_device_path():
+    """HostPipeline (pinned host in/out, overlapped copies, two device slots)
+    returns bitwise the device-resident executor's visibility for every
+    batch, including slot reuse, and reports out-of-frustum batches."""
+    import torch
+    from paper_2301_05262_b200 import network, producer, scenes
+    from paper_2301_05262_b200._lib import FrustumError
+    from paper_2301_05262_b200.infer import HostPipeline, ShadowInference
+    cfg, w = _weights()
+    plan = network.Plan(w, cfg, "fp16")
+    frames = [scenes.make_frame(scenes.random_scene(8, seed=s), (96, 160), (256, 256)) for s in range(2)]
+    run = ShadowInference(plan, frames, out_dtype="fp16")
+    batches, refs = [], []
+    for b in range(3):   # three batches through two slots
+        inp = producer.render_inputs(frames)
+        inp["position"] = inp["position"] + 0.01 * b * (inp["d"] > 0)[:, None]
+        refs.append(run(inp).cpu().clone())
+        batches.append({k: v.cpu().pin_memory() for k, v in inp.items()})
+    pipe = HostPipeline(run)
+    outs = [torch.empty(run.y.shape, dtype=run.y.dtype, pin_memory=True) for _ in batches]
+    for hb, ho in zip(batches, outs):
+        pipe.submit(hb, ho)
+    pipe.synchronize()
+    for ho, ref in zip(outs, refs):
+        torch.testing.assert_close(ho, ref, rtol=0, atol=0)
+    bad = {k: v.clone() for k, v in batches[0].items()}
+    bad["position"][0, 0] += 1e4 * (bad["d"][0] > 0)      # far outside the emitter frustum
+    pipe.submit(bad, outs[0])
+    with pytest.raises(FrustumError):
+        pipe.synchronize()
+
+
 @pytest.mark.parametrize("config", [2, 3])
 def test_1080p_fp16_vs_oracle(config):
     from oracle import features as of

@@ -95,9 +95,28 @@ def full(path):
     return "\n".join(out), recs
 
 
+KMAP = {"enc0_kernel": "enc0_fused", "dec0_kernel": "dec0_fused", "recon_kernel": "recon"}
+
+
+def traffic(path, frames_per_launch, out, source):
+    """profiles/traffic.json for bench.py's roofline.traffic: DRAM bytes per
+    frame of each kernel's first launch in a --set full report."""
+    _, recs = full(path)
+    res = {}
+    for r in recs:
+        for k, name in KMAP.items():
+            if k in r["kernel"] and name not in res and "dram_read_MB" in r:
+                res[name] = {"dram_bytes_per_frame": (r["dram_read_MB"] + r["dram_write_MB"]) * 1e6 /
+                             frames_per_launch, "source": source}
+    json.dump(res, open(out, "w"), indent=1)
+    print(json.dumps(res, indent=1))
+
+
 if __name__ == "__main__":
     mode, path = sys.argv[1], sys.argv[2]
-    if mode == "launches":
+    if mode == "traffic":      # traffic <report> <frames_per_launch> <out.json> <source-label>
+        traffic(path, int(sys.argv[3]), sys.argv[4], sys.argv[5])
+    elif mode == "launches":
         print(launches(path))
     else:
         table, recs = full(path)
