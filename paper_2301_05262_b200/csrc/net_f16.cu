@@ -85,7 +85,7 @@ constexpr int round128(int v) { return (v + 127) / 128 * 128; }
 constexpr int ST_OFF_N = round128(ST_PLANE);              // TMA destinations 128-B aligned
 constexpr int ST_OFF_P = ST_OFF_N + round128(3 * ST_PLANE);
 constexpr int ST_BYTES = round128(ST_OFF_P + 3 * ST_PLANE);
-constexpr int ENC0_SMEM_TMA = 2 * E0_SMEM + 2 * ST_BYTES + 64;
+constexpr int ENC0_SMEM_TMA = 2 * E0_SMEM + 2 * ST_BYTES + 128;
 static_assert(E0_SMEM % 128 == 0, "stage base alignment");
 
 struct GbufMaps {
@@ -442,13 +442,21 @@ __device__ __forceinline__ void produce_features(const Enc0Args& a, uint8_t* buf
 // pixels 2k-1 and 2k), warp 18 the row's two edge pairs (halo cols 0,1 and
 // 130,131: level-0 pixels 0 and 65).  A half is then one vectorised pass
 // (LDS.128 per plane) over 18 x 33 threads with all index math hoisted.
-// 19 producer warps + 4 tensor-core warps; setmaxnreg moves registers from
-// the producers (-> 72) to the MMA warps (-> 112); the budget is checked
-// against the kernel's launch register count on the host (run_l0).
-constexpr int kE0Prod = 608, kE0Threads = 736;
+// Warp roles: 0-18 feature producers, 19 the TMA issuer, 20-23 tensor-core
+// consumers.  All hand-offs are mbarriers with one arrival per warp, so a
+// warp only ever waits for the data it needs, never for its peers:
+//   full[s]     TMA -> producers       (complete_tx: staged half-tile landed)
+//   empty[s]    producers -> TMA       (19 arrivals: stage s read by phase A)
+//   half[b][h]  producers -> consumers (19: rows of half h of tile buffer b)
+//   freed[b]    consumers -> producers (4: tile buffer b consumed)
+// setmaxnreg moves registers from the producer/TMA warps (-> 72) to the MMA
+// warps (-> 112); the budget is checked against the kernel's launch
+// register count on the host (run_l0).
+constexpr int kE0Feat = 608, kE0Prod = 640, kE0Threads = 768;
+constexpr int kE0FeatWarps = kE0Feat / 32, kE0MmaWarps = (kE0Threads - kE0Prod) / 32;
 constexpr int kE0ProdRegs = 72, kE0MmaRegs = 112;
 constexpr int ST_QC = E0_TW / 2;                     // interior quads per staged row (32)
-static_assert(ST_ROWS * (ST_QC + 1) <= kE0Prod, "one quad per producer thread per half-tile");
+static_assert(ST_ROWS * (ST_QC + 1) <= kE0Feat, "one quad per producer thread per half-tile");
 static_assert(ST_ROWS * ST_QC % 32 == 0, "edge threads form their own warp");
 static_assert(ST_ROWS % 2 == 0, "a half-tile holds whole level-0 rows");
 
@@ -472,9 +480,29 @@ __device__ __forceinline__ void produce_features_tma(const Enc0Args& a, const Gb
     extern __shared__ __align__(128) uint8_t smem[];
     uint8_t* stage = smem + 2 * E0_SMEM;
     uint64_t* full = reinterpret_cast<uint64_t*>(stage + 2 * ST_BYTES);
+    uint64_t* empty = full + 2;
+    uint64_t* half = full + 4;     // [buffer][half]
+    uint64_t* freed = full + 8;
     const int ptid = threadIdx.x;
+    const int lane = ptid & 31;
     const int mytiles = (int)blockIdx.x < total ? (total - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x : 0;
     const int nh = 2 * mytiles;
+    if (ptid >= kE0Feat) {                         // TMA warp
+        if (lane == 0) {
+            for (int q = 0; q < nh; ++q) {
+                const int sidx = q & 1;
+                if (q >= 2) mbar_wait(&empty[sidx], ((q - 2) >> 1) & 1);
+                const L0Tile tl = l0_tile(blockIdx.x + (q >> 1) * gridDim.x, a.H0, a.W0);
+                const uint32_t dst = smem_u32(stage + sidx * ST_BYTES);
+                const int x = 2 * tl.tx0 - 4, y = 2 * tl.ty0 - 2 + ST_ROWS * (q & 1);
+                mbar_expect_tx(&full[sidx], ST_TX);
+                tma_load_3d(dst, &tm.d, x, y, tl.f, &full[sidx]);
+                tma_load_4d(dst + ST_OFF_N, &tm.n, x, y, 0, tl.f, &full[sidx]);
+                tma_load_4d(dst + ST_OFF_P, &tm.p, x, y, 0, tl.f, &full[sidx]);
+            }
+        }
+        return;
+    }
     // tile-invariant geometry of this thread's 4 pixels: halo columns
     // hc_lo + {0, 1} (level-0 halo pixel lo) and hc_hi + {0, 1} (pixel hi)
     const bool edge = ptid >= ST_ROWS * ST_QC;
@@ -486,30 +514,9 @@ __device__ __forceinline__ void produce_features_tma(const Enc0Args& a, const Gb
     const int lds_lo = qy * ST_TCOLS * 4 + 8 + 8 * px_lo, lds_hi = qy * ST_TCOLS * 4 + 8 + 8 * px_hi;
     const int sts_row = (qy & 1) * E0_PLANE + (qy >> 1) * E0_IC * 16;
     const int slot_lo = sts_row + px_lo * 16, slot_hi = sts_row + px_hi * 16;
-    auto issue = [&](int q) {
-        const L0Tile tl = l0_tile(blockIdx.x + (q >> 1) * gridDim.x, a.H0, a.W0);
-        const int sidx = q & 1;
-        const uint32_t dst = smem_u32(stage + sidx * ST_BYTES);
-        const int x = 2 * tl.tx0 - 4, y = 2 * tl.ty0 - 2 + ST_ROWS * (q & 1);
-        mbar_expect_tx(&full[sidx], ST_TX);
-        tma_load_3d(dst, &tm.d, x, y, tl.f, &full[sidx]);
-        tma_load_4d(dst + ST_OFF_N, &tm.n, x, y, 0, tl.f, &full[sidx]);
-        tma_load_4d(dst + ST_OFF_P, &tm.p, x, y, 0, tl.f, &full[sidx]);
-    };
-    if (ptid == 0) {
-        mbar_init(&full[0], 1);
-        mbar_init(&full[1], 1);
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    nbar_sync(5, kE0Prod);
-    if (ptid == 0) {
-        if (nh > 0) issue(0);
-        if (nh > 1) issue(1);
-    }
     auto phaseA = [&](int q, QuadRegs& R) {
         const L0Tile tl = l0_tile(blockIdx.x + (q >> 1) * gridDim.x, a.H0, a.W0);
         const int sidx = q & 1;
-        mbar_wait(&full[sidx], (q >> 1) & 1);
         if (!active) return;
         const FrameK& F = a.tab.f[tl.f];
         // 32-bit texel index: NSM_MAX_FRAMES_PER_LAUNCH maps of <= 2^26 texels
@@ -593,21 +600,21 @@ __device__ __forceinline__ void produce_features_tma(const Enc0Args& a, const Gb
         }
     };
     auto step = [&](int q, QuadRegs& RA, QuadRegs& RB) {
-        // phase A of a tile's first half already writes (ch2, ch3) into the
-        // tile buffer, so it waits for the consumers to release it
-        if (!(q & 1) && q < nh && (q >> 1) >= 2) nbar_sync(3 + ((q >> 1) & 1), kE0Threads);
-        if (q < nh && !(a.dbg & 1)) phaseA(q, RA);
-        else if (q < nh) mbar_wait(&full[q & 1], (q >> 1) & 1);
-        nbar_sync(5, kE0Prod);                     // stage q&1 fully consumed by A(q)
-        if (ptid == 0 && q + 2 < nh) {
-            fence_proxy_async();
-            issue(q + 2);
+        if (q < nh) {
+            // phase A of a tile's first half already writes (ch2, ch3) into
+            // the tile buffer, so it waits for the consumers to release it
+            const int k = q >> 1;
+            if (!(q & 1) && k >= 2) mbar_wait(&freed[k & 1], ((k - 2) >> 1) & 1);
+            mbar_wait(&full[q & 1], (q >> 1) & 1);
+            if (!(a.dbg & 1)) phaseA(q, RA);
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[q & 1]);                   // stage read
         }
         if (q >= 1) {
             const int qb = q - 1, k = qb >> 1;
             if (!(a.dbg & 1)) phaseB(qb, RB);
-            // level-0 rows 0-8 (half 0) / 9-17 (half 1) of tile k complete
-            nbar_arrive((qb & 1) ? 1 + (k & 1) : 6 + (k & 1), kE0Threads);
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&half[(k & 1) * 2 + (qb & 1)]);   // rows of half qb&1 done
         }
     };
     QuadRegs RA, RB;
@@ -626,6 +633,19 @@ __global__ void __launch_bounds__(kSrc == 2 ? kE0Threads : kL0Threads, 1) enc0_k
     constexpr int kProd = kSrc == 2 ? kE0Prod : kL0Prod;
     constexpr int kThreads = kSrc == 2 ? kE0Threads : kL0Threads;
     if (threadIdx.x == 0) pdl_trigger();
+    if constexpr (kSrc == 2) {
+        extern __shared__ __align__(128) uint8_t smem[];
+        uint64_t* bars = reinterpret_cast<uint64_t*>(smem + 2 * E0_SMEM + 2 * ST_BYTES);
+        if (threadIdx.x == 0) {
+            mbar_init(&bars[0], 1);                 // full[2]
+            mbar_init(&bars[1], 1);
+            for (int i = 2; i < 8; ++i) mbar_init(&bars[i], kE0FeatWarps);   // empty[2], half[2][2]
+            mbar_init(&bars[8], kE0MmaWarps);      // freed[2]
+            mbar_init(&bars[9], kE0MmaWarps);
+            asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        }
+        __syncthreads();
+    }
     pdl_wait();
     if (kSrc == 2) {
         static_assert(kE0ProdRegs == 72 && kE0MmaRegs == 112, "keep the asm immediates in sync");
@@ -728,18 +748,22 @@ __global__ void __launch_bounds__(kSrc == 2 ? kE0Threads : kL0Threads, 1) enc0_k
     };
     if constexpr (kSrc == 2) {
         extern __shared__ __align__(128) uint8_t smem[];
-        // the producers signal each half of a tile: rows 0-8 (barrier 6/7)
-        // and rows 9-17 (barrier 1/2), so the convolution starts one
-        // half-tile earlier
+        uint64_t* bars = reinterpret_cast<uint64_t*>(smem + 2 * E0_SMEM + 2 * ST_BYTES);
+        uint64_t* half = bars + 4;
+        uint64_t* freed = bars + 8;
+        // the producers signal each half of a tile (level-0 rows 0-8 and
+        // 9-17), so the convolution starts one half-tile earlier
         for (int k = 0;; ++k) {
             const int tile = blockIdx.x + k * gridDim.x;
             if (tile >= total) break;
             const int s = k & 1;
-            nbar_sync(6 + s, kThreads);
+            const uint32_t par = (k >> 1) & 1;
+            mbar_wait(&half[s * 2], par);
             consume(smem + s * E0_SMEM, tile, [&](int ir) {
-                if (ir == E0_IR / 2) nbar_sync(1 + s, kThreads);
+                if (ir == E0_IR / 2) mbar_wait(&half[s * 2 + 1], par);
             });
-            if (tile + 2 * (int)gridDim.x < total) nbar_arrive(3 + s, kThreads);
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&freed[s]);
         }
     } else {
         l0_consume_loop<kThreads>(total, [&](uint8_t* buf, int tile) { consume(buf, tile, NoRowHook{}); });
@@ -1079,10 +1103,6 @@ __device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t
     asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
                  "l"(src), "r"(bytes), "r"(smem_u32(bar))
                  : "memory");
-}
-
-__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
-    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 
 // Persistent, warp-specialised level kernel (levels 1-3):
