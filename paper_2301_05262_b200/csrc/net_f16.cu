@@ -210,14 +210,16 @@ struct NoRowHook {
 };
 
 // hook(ir) runs before input row ir is read (e.g. to wait for the producers
-// to finish the half of the tile that holds it).
-template <typename T, int ROWS, class Epi, class Hook = NoRowHook>
+// to finish the half of the tile that holds it).  kPairRows maps MMA row r
+// to strip pixel 2r (r < 8) / 2(r-8)+1, so each thread's accumulator holds
+// the horizontal neighbours 2g, 2g+1 (a 2x2 pool needs no shuffles).
+template <typename T, int ROWS, bool kPairRows = false, class Epi, class Hook = NoRowHook>
 __device__ __forceinline__ void conv3_strip16(uint32_t sbase, int plane, int rowpix, int r0, int sx,
                                               const uint32_t (&B3)[9][2][2], const float (&binit)[2][2],
                                               Epi&& epi, Hook&& hook = Hook{}) {
     const int lane = threadIdx.x & 31;
     const int lm = lane >> 3, li = lane & 7;
-    const uint32_t a_off = (lm >> 1) * plane + (li + 8 * (lm & 1)) * 16;
+    const uint32_t a_off = (lm >> 1) * plane + (kPairRows ? 2 * li + (lm & 1) : li + 8 * (lm & 1)) * 16;
     float acc[3][2][4];
 #pragma unroll
     for (int s = 0; s < 3; ++s)
@@ -696,12 +698,12 @@ __global__ void __launch_bounds__(kSrc == 2 ? kE0Threads : kL0Threads, 1) enc0_k
     T* out = reinterpret_cast<T*>(a.out);
     auto consume = [&](uint8_t* buf, int tile, auto&& hook) {
             const L0Tile tl = l0_tile(tile, a.H0, a.W0);
-            float pp[2][4];
+            float pp[2][2];
             if (a.dbg & 2) {
                 hook(E0_IR / 2);
                 return;
             }
-            conv3_strip16<T, kRows>(smem_u32(buf), E0_PLANE, E0_IC, r0, sx, B3, bias3, [&](int oo, float (&acc)[2][4]) {
+            conv3_strip16<T, kRows, true>(smem_u32(buf), E0_PLANE, E0_IC, r0, sx, B3, bias3, [&](int oo, float (&acc)[2][4]) {
                 uint32_t a1[4];
                 relu_pack_a<T>(acc, a1);
                 float u[2][4];
@@ -711,37 +713,24 @@ __global__ void __launch_bounds__(kSrc == 2 ? kE0Threads : kL0Threads, 1) enc0_k
                     for (int e = 0; e < 4; ++e) u[n][e] = bias1[n][e & 1];
                     mma16816<T>(u[n], a1, B1[n][0], B1[n][1]);
                 }
-                // avg_pool2: rows oo-1, oo summed in registers, then the
-                // x-neighbour (lane ^ 4) once per row pair
+                // avg_pool2: rows oo-1, oo summed in registers; the x
+                // neighbours are this thread's e and e + 2 (kPairRows)
 #pragma unroll
                 for (int n = 0; n < 2; ++n)
 #pragma unroll
-                    for (int e = 0; e < 4; ++e) {
-                        const float v = fmaxf(u[n][e], 0.f);
+                    for (int e = 0; e < 2; ++e) {
+                        const float v = fmaxf(u[n][e], 0.f) + fmaxf(u[n][e + 2], 0.f);
                         if (oo & 1) pp[n][e] += v;
                         else pp[n][e] = v;
                     }
-                if (oo & 1) {
-#pragma unroll
-                    for (int n = 0; n < 2; ++n)
-#pragma unroll
-                        for (int e = 0; e < 4; ++e) pp[n][e] += __shfl_xor_sync(0xffffffffu, pp[n][e], 4);
-                }
                 if (oo & 1) {                                           // avg_pool2 of rows oo-1, oo
                     const int py = (tl.ty0 + r0 + oo) >> 1;
-                    const int pxb = (tl.tx0 + sx) >> 1;
-                    if (!(g & 1) && py < H1) {
-                        T* orow = out + ((int64_t)tl.f * H1 + py) * W1 * 16;
+                    const int px = ((tl.tx0 + sx) >> 1) + g;
+                    if (py < H1 && px < W1) {
+                        T* o = out + (((int64_t)tl.f * H1 + py) * W1 + px) * 16 + 2 * t;
 #pragma unroll
-                        for (int hlf = 0; hlf < 2; ++hlf) {
-                            const int px = pxb + (g >> 1) + 4 * hlf;
-                            if (px < W1) {
-#pragma unroll
-                                for (int n = 0; n < 2; ++n)
-                                    *reinterpret_cast<uint32_t*>(orow + px * 16 + n * 8 + 2 * t) =
-                                        Elem<T>::pack(pp[n][2 * hlf] * 0.25f, pp[n][2 * hlf + 1] * 0.25f);
-                            }
-                        }
+                        for (int n = 0; n < 2; ++n)
+                            *reinterpret_cast<uint32_t*>(o + n * 8) = Elem<T>::pack(pp[n][0] * 0.25f, pp[n][1] * 0.25f);
                     }
                 }
             }, hook);
