@@ -979,52 +979,81 @@ __global__ void __launch_bounds__(kL0Threads, 1) dec0_kernel(const __grid_consta
 // The 2x half-pixel bilinear of y0 at the 4 outputs of L0 pixel (Y, X) uses
 // rows/cols Y-1..Y+1 with weights (1/4, 3/4); clamping the neighbour indices
 // reproduces the reference's edge clamp (_upsample_taps, autodiff.py:258-264).
+__device__ __forceinline__ float sigmoid_fast(float v) {
+    // stable logistic (autodiff.py:200-209): e = exp(-|v|) in (0, 1]
+    const float e = __expf(-fabsf(v));
+    const float r = __fdividef(1.f, 1.f + e);
+    return v >= 0.f ? r : e * r;
+}
+
+// Each thread reconstructs 4 consecutive level-0 pixels (8 x 2 outputs):
+// ch0 of rows Y-1..Y+1 at columns X0-1..X0+4 (float4 + 2 edge loads per
+// row), the 3 detail channels as float4, two 16-B rows of fp16 out.
+constexpr int kReconPx = 4;
 __global__ void __launch_bounds__(128) recon_kernel(const float* __restrict__ y, int H0, int W0, int h,
                                                      int w, int n, void* __restrict__ out, int f16) {
     if (threadIdx.x == 0) pdl_trigger();
     pdl_wait();
-    const int X = blockIdx.x * blockDim.x + threadIdx.x;
+    const int X0 = (blockIdx.x * blockDim.x + threadIdx.x) * kReconPx;
     const int Y = blockIdx.y;
     const int f = blockIdx.z;
-    if (X >= W0) return;
-    const int64_t hw0 = (int64_t)H0 * W0;
+    if (X0 >= W0) return;
+    const int hw0 = H0 * W0;
     const float* y0 = y + (int64_t)f * 4 * hw0;
-    const int xm = max(X - 1, 0), xp = min(X + 1, W0 - 1);
-    const int ym = max(Y - 1, 0), yp = min(Y + 1, H0 - 1);
-    float r[3][3];
-    const int rows[3] = {ym, Y, yp}, cols[3] = {xm, X, xp};
+    const int rows[3] = {max(Y - 1, 0), Y, min(Y + 1, H0 - 1)};
+    const int xm = max(X0 - 1, 0), xp = min(X0 + kReconPx, W0 - 1);
+    float r[3][kReconPx + 2];
 #pragma unroll
-    for (int i = 0; i < 3; ++i)
+    for (int i = 0; i < 3; ++i) {
+        const float* row = y0 + rows[i] * W0;
+        const float4 c = __ldg(reinterpret_cast<const float4*>(row + X0));
+        r[i][0] = __ldg(row + xm);
+        r[i][1] = c.x, r[i][2] = c.y, r[i][3] = c.z, r[i][4] = c.w;
+        r[i][5] = __ldg(row + xp);
+    }
+    float det[3][kReconPx];
 #pragma unroll
-        for (int j = 0; j < 3; ++j) r[i][j] = __ldg(y0 + (int64_t)rows[i] * W0 + cols[j]);
-    const int64_t me = (int64_t)Y * W0 + X;
-    const float det[4] = {0.f, __ldg(y0 + hw0 + me), __ldg(y0 + 2 * hw0 + me), __ldg(y0 + 3 * hw0 + me)};
+    for (int c = 0; c < 3; ++c) {
+        const float4 v = __ldg(reinterpret_cast<const float4*>(y0 + (c + 1) * hw0 + Y * W0 + X0));
+        det[c][0] = v.x, det[c][1] = v.y, det[c][2] = v.z, det[c][3] = v.w;
+    }
 #pragma unroll
     for (int sy = 0; sy < 2; ++sy) {
         const int oy = 2 * Y + sy;
-        if (oy >= h) continue;
+        if (oy >= h) break;
         // rows: sy = 0 -> (Y-1, Y) weights (1/4, 3/4); sy = 1 -> (Y, Y+1) weights (3/4, 1/4)
-        float cr[3];
+        float cr[kReconPx + 2];
 #pragma unroll
-        for (int j = 0; j < 3; ++j) cr[j] = sy ? r[1][j] * 0.75f + r[2][j] * 0.25f : r[0][j] * 0.25f + r[1][j] * 0.75f;
-        float o2[2];
+        for (int j = 0; j < kReconPx + 2; ++j)
+            cr[j] = sy ? r[1][j] * 0.75f + r[2][j] * 0.25f : r[0][j] * 0.25f + r[1][j] * 0.75f;
+        float o[2 * kReconPx];
 #pragma unroll
-        for (int sx = 0; sx < 2; ++sx) {
-            const float base = sx ? cr[1] * 0.75f + cr[2] * 0.25f : cr[0] * 0.25f + cr[1] * 0.75f;
-            const float v = base + det[2 * sy + sx];
-            const float e = __expf(-fabsf(v));
-            o2[sx] = v >= 0.f ? __frcp_rn(1.f + e) : __fdividef(e, 1.f + e);
-        }
-        const int64_t o = ((int64_t)f * h + oy) * w + 2 * X;
-        if (2 * X + 1 < w && !(w & 1)) {
-            if (f16) *reinterpret_cast<__half2*>(reinterpret_cast<__half*>(out) + o) = __floats2half2_rn(o2[0], o2[1]);
-            else *reinterpret_cast<float2*>(reinterpret_cast<float*>(out) + o) = make_float2(o2[0], o2[1]);
-        } else {
+        for (int k = 0; k < kReconPx; ++k)
 #pragma unroll
             for (int sx = 0; sx < 2; ++sx) {
-                if (2 * X + sx >= w) break;
-                if (f16) reinterpret_cast<__half*>(out)[o + sx] = __float2half_rn(o2[sx]);
-                else reinterpret_cast<float*>(out)[o + sx] = o2[sx];
+                const float base = sx ? cr[k + 1] * 0.75f + cr[k + 2] * 0.25f : cr[k] * 0.25f + cr[k + 1] * 0.75f;
+                // depth_to_space detail: channel 2sy + sx, zero for (0, 0)
+                const float d = (sy | sx) ? det[2 * sy + sx - 1][k] : 0.f;
+                o[2 * k + sx] = sigmoid_fast(base + d);
+            }
+        const int64_t ob = ((int64_t)f * h + oy) * w + 2 * X0;
+        if (2 * X0 + 2 * kReconPx <= w && !(w & 7)) {
+            if (f16) {
+                uint4 v;
+                v.x = Elem<__half>::pack(o[0], o[1]), v.y = Elem<__half>::pack(o[2], o[3]);
+                v.z = Elem<__half>::pack(o[4], o[5]), v.w = Elem<__half>::pack(o[6], o[7]);
+                *reinterpret_cast<uint4*>(reinterpret_cast<__half*>(out) + ob) = v;
+            } else {
+                float4* po = reinterpret_cast<float4*>(reinterpret_cast<float*>(out) + ob);
+                po[0] = make_float4(o[0], o[1], o[2], o[3]);
+                po[1] = make_float4(o[4], o[5], o[6], o[7]);
+            }
+        } else {
+#pragma unroll
+            for (int k = 0; k < 2 * kReconPx; ++k) {
+                if (2 * X0 + k >= w) break;
+                if (f16) reinterpret_cast<__half*>(out)[ob + k] = __float2half_rn(o[k]);
+                else reinterpret_cast<float*>(out)[ob + k] = o[k];
             }
         }
     }
@@ -1613,7 +1642,8 @@ nsm_status run_l0(const Plan& p, const Bufs& b, const Enc0Args& e0, const GbufMa
         launch_pdl(dec0_kernel<T>, dim3(pgrid), dim3(kL0Threads), DEC0_SMEM, st, d, dm, total);
     }
     {
-        dim3 g2((W0 + 127) / 128, H0, nf);
+        static_assert(8 % kReconPx == 0, "W0 = round16(w) / 2 is a multiple of 8: float4 rows");
+        dim3 g2((W0 / kReconPx + 127) / 128, H0, nf);
         NSM_PROF("recon", st);
         launch_pdl(recon_kernel, g2, dim3(128), 0, st, (const float*)b.y, H0, W0, h, w, nf, y, y_f16);
     }

@@ -119,12 +119,15 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 
+// try_wait with a suspend-time hint: a waiting warp sleeps in hardware until
+// the phase completes (or ~0.1 ms pass) instead of spinning on try_wait and
+// stealing issue slots from the warps it is waiting for.
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
     asm volatile(
         "{\n\t.reg .pred P1;\n\tWAIT_%=:\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n\t"
         "@!P1 bra WAIT_%=;\n\t}\n" ::"r"(smem_u32(bar)),
-        "r"(phase)
+        "r"(phase), "n"(100000)
         : "memory");
 }
 
