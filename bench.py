@@ -42,6 +42,11 @@ METRIC = "1080p soft-shadow frames/sec"
 UNIT = "frames/s"
 
 
+def metric_name(config):
+    return {2: "1080p hard-shadow frames/sec", 3: METRIC, 4: METRIC,
+            5: "4K hard/soft-shadow frames/sec (64-scene sweep)"}[config]
+
+
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -185,7 +190,7 @@ def kernel_models(frames, inputs, cfg, dtype):
     return models, step_bytes, step_flops
 
 
-def ncu_traffic(kernel, algo_bytes, frames_per_launch):
+def ncu_traffic(kernel, algo_bytes, frames_per_launch, workload):
     """dram__bytes_read.sum + dram__bytes_write.sum per launch of ``kernel``,
     scaled from the committed ncu --set full capture (profiles/traffic.json,
     written by tools/ncu_summary.py traffic) to this run's frames per launch."""
@@ -194,7 +199,7 @@ def ncu_traffic(kernel, algo_bytes, frames_per_launch):
         return None
     with open(p) as f:
         t = json.load(f).get(kernel)
-    if not t:
+    if not t or t.get("workload") != workload:
         return None
     bpf = t["dram_bytes_per_frame"]
     return {"bytes": int(bpf * frames_per_launch), "algorithmic_bytes": int(algo_bytes),
@@ -279,7 +284,7 @@ def run_ours(args):
         ach = mb / (avg_ms / 1e3) / 1e9
         roof = {"bound": "hbm", "kernel": dom, "achieved": round(ach, 1), "peak": hbm,
                 "unit": "GB/s", "frac": round(ach / hbm, 4),
-                "traffic": ncu_traffic(dom, mb, n // max(1, cnt // args.steps)),
+                "traffic": ncu_traffic(dom, mb, n // max(1, cnt // args.steps), workload_name(args.config)),
                 "avg_launch_ms": round(avg_ms, 5), "peak_source": src,
                 "share_of_step": round(tot / args.steps / step_prof_ms, 3)}
     elif dom is not None:
@@ -329,7 +334,7 @@ def run_ours(args):
     if rank == 0:
         mpix = value * h * wd / 1e6
         line = {
-            "metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": world,
+            "metric": metric_name(args.config), "value": round(value, 3), "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": max(args.warmup, 3), "ms_per_step": round(ms_max, 5),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": {"fp16": "f16", "bf16": "bf16", "fp32": "f32"}[args.dtype],
@@ -413,7 +418,7 @@ def run_reference(args):
     value = steps / el
     h, wd = frames[0].camera.resolution
     print(json.dumps({
-        "metric": METRIC, "value": round(value, 4), "unit": UNIT, "impl": "reference",
+        "metric": metric_name(args.config), "value": round(value, 4), "unit": UNIT, "impl": "reference",
         "n_gpus": int(os.environ.get("WORLD_SIZE", "1")), "steps": steps, "warmup": warm,
         "ms_per_step": round(el / steps * 1e3, 2), "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f32", "data": "synthetic (same scenes/weights as ours)",

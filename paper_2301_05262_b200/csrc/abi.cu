@@ -316,11 +316,12 @@ size_t nsm_workspace_size(const nsm_plan* plan, int32_t n, int32_t h, int32_t w)
     if (!p || n <= 0 || h <= 0 || w <= 0) return 0;
     const int m = 1 << (p->cfg.layers - 1);
     const int hp = round_up(h, m), wp = round_up(w, m);
+    // 16-bit plans run every entry point on the chunked 16-bit kernels, whose
+    // workspace is bounded by the chunk, not by n
+    if (p->act != NSM_F32 && f16_supported(*p)) return infer_f16_workspace(*p, n, h, w);
     size_t a = forward_f32_workspace(*p, n, hp, wp);
     size_t b = infer_f32_workspace(*p, n, h, w);
-    size_t c = 0;
-    if (p->act != NSM_F32 && f16_supported(*p)) c = infer_f16_workspace(*p, n, h, w);
-    return std::max(a, std::max(b, c));
+    return std::max(a, b);
 }
 
 nsm_status nsm_features(const nsm_gbuffer* g, const float* sm, int64_t sm_stride,

@@ -98,7 +98,7 @@ def full(path):
 KMAP = {"enc0_kernel": "enc0_fused", "dec0_kernel": "dec0_fused", "recon_kernel": "recon"}
 
 
-def traffic(path, frames_per_launch, out, source):
+def traffic(path, frames_per_launch, out, source, workload="cfg4-1080p-soft-window8"):
     """profiles/traffic.json for bench.py's roofline.traffic: DRAM bytes per
     frame of each kernel's first launch in a --set full report."""
     _, recs = full(path)
@@ -107,7 +107,7 @@ def traffic(path, frames_per_launch, out, source):
         for k, name in KMAP.items():
             if k in r["kernel"] and name not in res and "dram_read_MB" in r:
                 res[name] = {"dram_bytes_per_frame": (r["dram_read_MB"] + r["dram_write_MB"]) * 1e6 /
-                             frames_per_launch, "source": source}
+                             frames_per_launch, "source": source, "workload": workload}
     json.dump(res, open(out, "w"), indent=1)
     print(json.dumps(res, indent=1))
 
