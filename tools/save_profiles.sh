@@ -10,3 +10,4 @@ grep '^{' gpurun_out/bench.log | tail -1 > profiles/${t}_bench.json
 grep '^{' gpurun_out/bench_ref.log | tail -1 > profiles/${t}_bench_ref.json
 tail -3 gpurun_out/pytest_gpu.log > profiles/${t}_pytest_gpu.txt
 cp gpurun_out/smoke.log profiles/${t}_smoke.txt
+cp gpurun_out/traffic.json profiles/traffic.json
