@@ -234,17 +234,19 @@ __device__ __forceinline__ void conv3_strip16(uint32_t sbase, int plane, int row
 #pragma unroll
         for (int dx = 0; dx < 3; ++dx)
             ldsm_x4(sbase + a_off + ((r0 + ir) * rowpix + sx + dx) * 16, A[dx]);
+        // dx outer, (ky, n) inner: consecutive MMAs go to up to 6 different
+        // accumulators, so no MMA waits on the one just issued
 #pragma unroll
-        for (int ky = 0; ky < 3; ++ky) {
-            const int oo = ir - ky;
-            if (oo >= 0 && oo < ROWS) {
+        for (int dx = 0; dx < 3; ++dx)
 #pragma unroll
-                for (int dx = 0; dx < 3; ++dx)
+            for (int ky = 0; ky < 3; ++ky) {
+                const int oo = ir - ky;
+                if (oo >= 0 && oo < ROWS) {
 #pragma unroll
                     for (int n = 0; n < 2; ++n)
                         mma16816<T>(acc[oo % 3][n], A[dx], B3[ky * 3 + dx][n][0], B3[ky * 3 + dx][n][1]);
+                }
             }
-        }
         if (ir >= 2) {
             const int oo = ir - 2;
             epi(oo, acc[oo % 3]);
@@ -1094,7 +1096,7 @@ struct LvGeom {
     static constexpr int SKB = STG ? IR * IC * CIN * 2 : 0, LOB = STG ? LR * LC * CIN * 2 : 0;
     static constexpr int OFF_SK = round128(OFF_W1 + W1B);
     static constexpr int OFF_LO = round128(OFF_SK + SKB);
-    static constexpr int OFF_B = round128(OFF_LO + LOB);
+    static constexpr int OFF_B = round128(OFF_LO + 2 * LOB);   // low-res staging double-buffered
     static constexpr int OFF_BAR = (OFF_B + (C3 + C1) * 4 + 15) / 16 * 16;
     static constexpr int SMEM = OFF_BAR + 192;
     static constexpr int ACC3 = 0, ACC1 = 2 * NB * C3;         // TMEM columns (both double-buffered)
@@ -1152,8 +1154,9 @@ __global__ void __launch_bounds__((NPW + 9) * 32, 1) level_kernel(const __grid_c
     uint64_t* a1_full = bar + 12;
     uint64_t* a1_empty = bar + 14;
     uint64_t* wbar = bar + 16;        // weights landed
-    uint64_t* stg_full = bar + 17;    // SRC_UP staging landed
-    uint32_t* tptr = reinterpret_cast<uint32_t*>(smem + G::OFF_BAR + 144);
+    uint64_t* skf = bar + 17;         // SRC_UP: skip rows 0-8 / 9-17 of the tile landed [2]
+    uint64_t* lof = bar + 19;         // SRC_UP: low-res tile landed, double-buffered [2]
+    uint32_t* tptr = reinterpret_cast<uint32_t*>(smem + G::OFF_BAR + 176);
     float* sb3 = reinterpret_cast<float*>(smem + G::OFF_B);
     float* sb1 = sb3 + C3;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -1183,7 +1186,10 @@ __global__ void __launch_bounds__((NPW + 9) * 32, 1) level_kernel(const __grid_c
             mbar_init(&a1_empty[i], 256);
         }
         mbar_init(wbar, 1);
-        mbar_init(stg_full, 1);
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(&skf[i], 1);
+            mbar_init(&lof[i], 1);
+        }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         // resident weights: two async bulk copies, waited on by the MMA warp only
         mbar_expect_tx(wbar, G::W3B + G::W1B);
@@ -1214,61 +1220,94 @@ __global__ void __launch_bounds__((NPW + 9) * 32, 1) level_kernel(const __grid_c
             }
         } else {
             // up2(low) + skip from TMA-staged pixel-major tiles (skip: the halo'd
-            // tile; low: (TH/2+2) x (TW/2+2) source pixels, edge-clamped indices)
+            // tile; low: (TH/2+2) x (TW/2+2) source pixels, edge-clamped indices).
+            // The skip tile streams in two row halves and the low-res tile is
+            // double-buffered, so the next tile's staging lands while this one
+            // is computed: skip rows 0-8 of tile k+1 are issued as soon as the
+            // producers finish rows 0-8 of tile k, the low tile of k+2 when
+            // tile k is done.
             const int hl = a.H / 2, wl = a.W / 2;
             const uint8_t* sk = smem + G::OFF_SK;
-            const uint8_t* lo = smem + G::OFF_LO;
-            auto stage = [&](int k) {          // thread 0 only
+            // (NIN = 1: the input buffer is single, the producers wait for the
+            // MMA anyway, so the skip tile is one piece issued per tile)
+            constexpr int NH = NIN == 2 ? 2 : 1;                // skip pieces per tile
+            constexpr int HR = G::IR / NH;                      // rows per skip piece
+            constexpr int SKH = HR * G::IC * CIN * 2;           // bytes per skip piece
+            static_assert(G::IR % NH == 0, "skip halves");
+            auto stage_skip = [&](int k, int h) {               // thread 0 only
                 int f, y0, x0;
                 tile_of(k, f, y0, x0);
-                mbar_expect_tx(stg_full, (a.skip ? G::SKB : 0) + G::LOB);
-                if (a.skip) tma_load_4d(sbase + G::OFF_SK, &tin, 0, x0 - 1, y0 - 1, f, stg_full);
-                tma_load_4d(sbase + G::OFF_LO, &tlo, 0, x0 / 2 - 1, y0 / 2 - 1, f, stg_full);
+                mbar_expect_tx(&skf[h], SKH);
+                tma_load_4d(sbase + G::OFF_SK + h * SKH, &tin, 0, x0 - 1, y0 - 1 + h * HR, f, &skf[h]);
             };
-            if (tid == 0 && mytiles > 0) stage(0);
+            auto stage_lo = [&](int k) {                        // thread 0 only
+                int f, y0, x0;
+                tile_of(k, f, y0, x0);
+                mbar_expect_tx(&lof[k & 1], G::LOB);
+                tma_load_4d(sbase + G::OFF_LO + (k & 1) * G::LOB, &tlo, 0, x0 / 2 - 1, y0 / 2 - 1, f, &lof[k & 1]);
+            };
+            if (tid == 0) {
+                if (mytiles > 0) {
+                    for (int h = 0; h < NH; ++h)
+                        if (a.skip) stage_skip(0, h);
+                    stage_lo(0);
+                }
+                if (mytiles > 1) stage_lo(1);
+            }
             for (int k = 0; k < mytiles; ++k) {
                 const int s = k % NIN;
                 int f, y0, x0;
                 tile_of(k, f, y0, x0);
                 const int ly0 = y0 / 2 - 1, lx0 = x0 / 2 - 1;
+                const uint8_t* lo = smem + G::OFF_LO + (k & 1) * G::LOB;
                 mbar_wait(&in_empty[s], ((k / NIN) & 1) ^ 1);
-                mbar_wait(stg_full, k & 1);
+                mbar_wait(&lof[k & 1], (k >> 1) & 1);
                 uint8_t* in = smem + s * G::INB;
-                for (int i = tid; i < ((a.dbg & 1) ? 0 : G::NPI * G::NCI); i += NPT) {
-                    const int c = i % G::NCI, p = i / G::NCI;
-                    const int ti = p / G::IC, tj = p - ti * G::IC;
-                    const int yy = y0 - 1 + ti, xx = x0 - 1 + tj;
-                    uint4 q = make_uint4(0u, 0u, 0u, 0u);
-                    if (yy >= 0 && xx >= 0 && yy < a.H && xx < a.W) {
-                        const float sy = fminf(fmaxf((yy + 0.5f) * 0.5f - 0.5f, 0.f), (float)(hl - 1));
-                        const float sx = fminf(fmaxf((xx + 0.5f) * 0.5f - 0.5f, 0.f), (float)(wl - 1));
-                        const int r0 = (int)sy, c0 = (int)sx;
-                        const int r1 = min(r0 + 1, hl - 1), c1 = min(c0 + 1, wl - 1);
-                        const float wy = sy - r0, wx = sx - c0;
-                        auto ld = [&](int r, int cc) {
-                            return *reinterpret_cast<const uint4*>(lo + (((r - ly0) * G::LC + (cc - lx0)) * CIN + c * 8) * 2);
-                        };
-                        const uint4 q00 = ld(r0, c0), q10 = ld(r1, c0), q01 = ld(r0, c1), q11 = ld(r1, c1);
-                        uint4 qs = make_uint4(0u, 0u, 0u, 0u);
-                        if (a.skip) qs = *reinterpret_cast<const uint4*>(sk + (p * CIN + c * 8) * 2);
-                        const uint32_t *a00 = &q00.x, *a10 = &q10.x, *a01 = &q01.x, *a11 = &q11.x, *as = &qs.x;
-                        uint32_t* qo = &q.x;
+#pragma unroll 1
+                for (int h = 0; h < NH; ++h) {
+                    if (a.skip) mbar_wait(&skf[h], k & 1);
+                    constexpr int HI = HR * G::IC * G::NCI;     // items per half
+                    for (int i = h * HI + tid; i < ((a.dbg & 1) ? 0 : (h + 1) * HI); i += NPT) {
+                        const int c = i % G::NCI, p = i / G::NCI;
+                        const int ti = p / G::IC, tj = p - ti * G::IC;
+                        const int yy = y0 - 1 + ti, xx = x0 - 1 + tj;
+                        uint4 q = make_uint4(0u, 0u, 0u, 0u);
+                        if (yy >= 0 && xx >= 0 && yy < a.H && xx < a.W) {
+                            const float sy = fminf(fmaxf((yy + 0.5f) * 0.5f - 0.5f, 0.f), (float)(hl - 1));
+                            const float sx = fminf(fmaxf((xx + 0.5f) * 0.5f - 0.5f, 0.f), (float)(wl - 1));
+                            const int r0 = (int)sy, c0 = (int)sx;
+                            const int r1 = min(r0 + 1, hl - 1), c1 = min(c0 + 1, wl - 1);
+                            const float wy = sy - r0, wx = sx - c0;
+                            auto ld = [&](int r, int cc) {
+                                return *reinterpret_cast<const uint4*>(lo + (((r - ly0) * G::LC + (cc - lx0)) * CIN + c * 8) * 2);
+                            };
+                            const uint4 q00 = ld(r0, c0), q10 = ld(r1, c0), q01 = ld(r0, c1), q11 = ld(r1, c1);
+                            uint4 qs = make_uint4(0u, 0u, 0u, 0u);
+                            if (a.skip) qs = *reinterpret_cast<const uint4*>(sk + (p * CIN + c * 8) * 2);
+                            const uint32_t *a00 = &q00.x, *a10 = &q10.x, *a01 = &q01.x, *a11 = &q11.x, *as = &qs.x;
+                            uint32_t* qo = &q.x;
 #pragma unroll
-                        for (int e = 0; e < 4; ++e) {
-                            const float2 p00 = Elem<T>::unpack(a00[e]), p10 = Elem<T>::unpack(a10[e]);
-                            const float2 p01 = Elem<T>::unpack(a01[e]), p11 = Elem<T>::unpack(a11[e]);
-                            const float2 ps = Elem<T>::unpack(as[e]);
-                            const float c0x = p00.x * (1.f - wy) + p10.x * wy, c1x = p01.x * (1.f - wy) + p11.x * wy;
-                            const float c0y = p00.y * (1.f - wy) + p10.y * wy, c1y = p01.y * (1.f - wy) + p11.y * wy;
-                            qo[e] = Elem<T>::pack(c0x * (1.f - wx) + c1x * wx + ps.x, c0y * (1.f - wx) + c1y * wx + ps.y);
+                            for (int e = 0; e < 4; ++e) {
+                                const float2 p00 = Elem<T>::unpack(a00[e]), p10 = Elem<T>::unpack(a10[e]);
+                                const float2 p01 = Elem<T>::unpack(a01[e]), p11 = Elem<T>::unpack(a11[e]);
+                                const float2 ps = Elem<T>::unpack(as[e]);
+                                const float c0x = p00.x * (1.f - wy) + p10.x * wy, c1x = p01.x * (1.f - wy) + p11.x * wy;
+                                const float c0y = p00.y * (1.f - wy) + p10.y * wy, c1y = p01.y * (1.f - wy) + p11.y * wy;
+                                qo[e] = Elem<T>::pack(c0x * (1.f - wx) + c1x * wx + ps.x, c0y * (1.f - wx) + c1y * wx + ps.y);
+                            }
                         }
+                        *reinterpret_cast<uint4*>(in + c * G::PIN + p * 16) = q;
                     }
-                    *reinterpret_cast<uint4*>(in + c * G::PIN + p * 16) = q;
+                    if (h == NH - 1) {
+                        fence_proxy_async();
+                        mbar_arrive(&in_full[s]);
+                    }
+                    nbar_sync(1, NPT);             // all producers done with skip piece h (and, last, the low tile)
+                    if (tid == 0) {
+                        if (a.skip && k + 1 < mytiles) stage_skip(k + 1, h);
+                        if (h == NH - 1 && k + 2 < mytiles) stage_lo(k + 2);
+                    }
                 }
-                fence_proxy_async();
-                mbar_arrive(&in_full[s]);
-                nbar_sync(1, NPT);                 // all producers done with the staging tiles
-                if (tid == 0 && k + 1 < mytiles) stage(k + 1);
             }
         }
     } else if (warp == MW) {
@@ -1487,6 +1526,7 @@ bool encode_nhwc_map4(const void* base, bool bf16, int C, int H, int W, int nf, 
 template <typename T, int CIN, int C3, int C1, int SRC, int DST, int NB, int NIN, int NMID>
 nsm_status launch_level(const LevelArgs& a, int nf, cudaStream_t st, const char* name) {
     using G = LvGeom<CIN, C3, C1, NB, NIN, NMID, SRC == SRC_UP>;
+    static_assert(G::SMEM <= 232448, "level kernel exceeds 227 KB of shared memory");
     constexpr int NPW = SRC == SRC_TENSOR ? 1 : 8;
     auto k = level_kernel<T, CIN, C3, C1, SRC, DST, NB, NIN, NMID, NPW>;
     static bool attr = false;
@@ -1503,7 +1543,7 @@ nsm_status launch_level(const LevelArgs& a, int nf, cudaStream_t st, const char*
         ok = encode_nhwc_map(a.x, bf, CIN, a.H, a.W, nf, G::IC, G::IR, &tin);
     } else {
         ok = encode_nhwc_map4(a.x, bf, CIN, a.H / 2, a.W / 2, nf, G::LC, G::LR, &tlo);
-        if (a.skip) ok = ok && encode_nhwc_map4(a.skip, bf, CIN, a.H, a.W, nf, G::IC, G::IR, &tin);
+        if (a.skip) ok = ok && encode_nhwc_map4(a.skip, bf, CIN, a.H, a.W, nf, G::IC, NIN == 2 ? G::IR / 2 : G::IR, &tin);
     }
     if (!ok) return fail(NSM_ERR_CUDA, "%s: TMA tensor map encoding failed", name);
     const int total = ((a.W + G::TW - 1) / G::TW) * ((a.H + G::TH - 1) / G::TH) * nf;
