@@ -1527,7 +1527,7 @@ template <typename T, int CIN, int C3, int C1, int SRC, int DST, int NB, int NIN
 nsm_status launch_level(const LevelArgs& a, int nf, cudaStream_t st, const char* name) {
     using G = LvGeom<CIN, C3, C1, NB, NIN, NMID, SRC == SRC_UP>;
     static_assert(G::SMEM <= 232448, "level kernel exceeds 227 KB of shared memory");
-    constexpr int NPW = SRC == SRC_TENSOR ? 1 : 8;
+    constexpr int NPW = SRC == SRC_TENSOR ? 1 : 16;
     auto k = level_kernel<T, CIN, C3, C1, SRC, DST, NB, NIN, NMID, NPW>;
     static bool attr = false;
     if (!attr) {
