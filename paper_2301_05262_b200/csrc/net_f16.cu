@@ -1266,37 +1266,73 @@ __global__ void __launch_bounds__((NPW + 9) * 32, 1) level_kernel(const __grid_c
 #pragma unroll 1
                 for (int h = 0; h < NH; ++h) {
                     if (a.skip) mbar_wait(&skf[h], k & 1);
-                    constexpr int HI = HR * G::IC * G::NCI;     // items per half
-                    for (int i = h * HI + tid; i < ((a.dbg & 1) ? 0 : (h + 1) * HI); i += NPT) {
-                        const int c = i % G::NCI, p = i / G::NCI;
-                        const int ti = p / G::IC, tj = p - ti * G::IC;
-                        const int yy = y0 - 1 + ti, xx = x0 - 1 + tj;
-                        uint4 q = make_uint4(0u, 0u, 0u, 0u);
-                        if (yy >= 0 && xx >= 0 && yy < a.H && xx < a.W) {
-                            const float sy = fminf(fmaxf((yy + 0.5f) * 0.5f - 0.5f, 0.f), (float)(hl - 1));
-                            const float sx = fminf(fmaxf((xx + 0.5f) * 0.5f - 0.5f, 0.f), (float)(wl - 1));
-                            const int r0 = (int)sy, c0 = (int)sx;
-                            const int r1 = min(r0 + 1, hl - 1), c1 = min(c0 + 1, wl - 1);
-                            const float wy = sy - r0, wx = sx - c0;
-                            auto ld = [&](int r, int cc) {
-                                return *reinterpret_cast<const uint4*>(lo + (((r - ly0) * G::LC + (cc - lx0)) * CIN + c * 8) * 2);
-                            };
-                            const uint4 q00 = ld(r0, c0), q10 = ld(r1, c0), q01 = ld(r0, c1), q11 = ld(r1, c1);
-                            uint4 qs = make_uint4(0u, 0u, 0u, 0u);
-                            if (a.skip) qs = *reinterpret_cast<const uint4*>(sk + (p * CIN + c * 8) * 2);
-                            const uint32_t *a00 = &q00.x, *a10 = &q10.x, *a01 = &q01.x, *a11 = &q11.x, *as = &qs.x;
-                            uint32_t* qo = &q.x;
+                    // one item = one 2x2 block of outputs (the children of low-res
+                    // pixel (bi, bj)) x one 8-channel chunk: the block reads its 3x3
+                    // low-res neighbourhood once with the fixed (1/4, 3/4) weights
+                    // (autodiff.py:258-287); clamping the source indices reproduces
+                    // the reference's edge clamp.  Block rows 5h .. 5h+4 hold the
+                    // tile's halo rows 9h .. 9h+8.
+                    constexpr int BR = G::IR / 2 + 1, BC = G::IC / 2 + 1;
+                    constexpr int BRH = BR / NH;                // block rows per piece
+                    static_assert(BR % NH == 0 && (NH == 1 || BRH * 2 == HR + 1), "block rows per skip piece");
+                    constexpr int HI = BRH * BC * G::NCI;       // items per piece
+                    for (int it = h * HI + tid; it < ((a.dbg & 1) ? 0 : (h + 1) * HI); it += NPT) {
+                        const int c = it % G::NCI, blk = it / G::NCI;
+                        const int bil = blk / BC, bjl = blk - bil * BC;
+                        const int bi = ly0 + bil, bj = lx0 + bjl;      // low-res pixel of the block
+                        int rs[3], cs[3];
 #pragma unroll
-                            for (int e = 0; e < 4; ++e) {
-                                const float2 p00 = Elem<T>::unpack(a00[e]), p10 = Elem<T>::unpack(a10[e]);
-                                const float2 p01 = Elem<T>::unpack(a01[e]), p11 = Elem<T>::unpack(a11[e]);
-                                const float2 ps = Elem<T>::unpack(as[e]);
-                                const float c0x = p00.x * (1.f - wy) + p10.x * wy, c1x = p01.x * (1.f - wy) + p11.x * wy;
-                                const float c0y = p00.y * (1.f - wy) + p10.y * wy, c1y = p01.y * (1.f - wy) + p11.y * wy;
-                                qo[e] = Elem<T>::pack(c0x * (1.f - wx) + c1x * wx + ps.x, c0y * (1.f - wx) + c1y * wx + ps.y);
+                        for (int u = 0; u < 3; ++u) {
+                            rs[u] = min(max(min(max(bi - 1 + u, 0), hl - 1) - ly0, 0), G::LR - 1);
+                            cs[u] = min(max(min(max(bj - 1 + u, 0), wl - 1) - lx0, 0), G::LC - 1);
+                        }
+                        float top[3][8], bot[3][8];
+#pragma unroll
+                        for (int u = 0; u < 3; ++u) {
+                            float sv[3][8];
+#pragma unroll
+                            for (int v = 0; v < 3; ++v) {
+                                const uint4 q = *reinterpret_cast<const uint4*>(lo + ((rs[v] * G::LC + cs[u]) * CIN + c * 8) * 2);
+                                const uint32_t* qw = &q.x;
+#pragma unroll
+                                for (int e = 0; e < 4; ++e) {
+                                    const float2 f2 = Elem<T>::unpack(qw[e]);
+                                    sv[v][2 * e] = f2.x;
+                                    sv[v][2 * e + 1] = f2.y;
+                                }
+                            }
+#pragma unroll
+                            for (int e = 0; e < 8; ++e) {
+                                top[u][e] = 0.25f * sv[0][e] + 0.75f * sv[1][e];
+                                bot[u][e] = 0.75f * sv[1][e] + 0.25f * sv[2][e];
                             }
                         }
-                        *reinterpret_cast<uint4*>(in + c * G::PIN + p * 16) = q;
+#pragma unroll
+                        for (int ab = 0; ab < 4; ++ab) {
+                            const int aa = ab >> 1, bb = ab & 1;
+                            const int yy = 2 * bi + aa, xx = 2 * bj + bb;       // output pixel
+                            const int ti = yy - (y0 - 1), tj = xx - (x0 - 1);
+                            if (ti < 0 || ti >= G::IR || tj < 0 || tj >= G::IC) continue;
+                            const int p = ti * G::IC + tj;
+                            uint4 q = make_uint4(0u, 0u, 0u, 0u);
+                            if (yy >= 0 && xx >= 0 && yy < a.H && xx < a.W) {
+                                uint4 qs = make_uint4(0u, 0u, 0u, 0u);
+                                if (a.skip) qs = *reinterpret_cast<const uint4*>(sk + (p * CIN + c * 8) * 2);
+                                const uint32_t* as = &qs.x;
+                                const float(&vr)[3][8] = aa ? bot : top;
+                                uint32_t* qo = &q.x;
+#pragma unroll
+                                for (int e = 0; e < 4; ++e) {
+                                    const float2 ps = Elem<T>::unpack(as[e]);
+                                    const float x0v = bb ? 0.75f * vr[1][2 * e] + 0.25f * vr[2][2 * e]
+                                                         : 0.25f * vr[0][2 * e] + 0.75f * vr[1][2 * e];
+                                    const float x1v = bb ? 0.75f * vr[1][2 * e + 1] + 0.25f * vr[2][2 * e + 1]
+                                                         : 0.25f * vr[0][2 * e + 1] + 0.75f * vr[1][2 * e + 1];
+                                    qo[e] = Elem<T>::pack(x0v + ps.x, x1v + ps.y);
+                                }
+                            }
+                            *reinterpret_cast<uint4*>(in + c * G::PIN + p * 16) = q;
+                        }
                     }
                     if (h == NH - 1) {
                         fence_proxy_async();
@@ -1527,7 +1563,7 @@ template <typename T, int CIN, int C3, int C1, int SRC, int DST, int NB, int NIN
 nsm_status launch_level(const LevelArgs& a, int nf, cudaStream_t st, const char* name) {
     using G = LvGeom<CIN, C3, C1, NB, NIN, NMID, SRC == SRC_UP>;
     static_assert(G::SMEM <= 232448, "level kernel exceeds 227 KB of shared memory");
-    constexpr int NPW = SRC == SRC_TENSOR ? 1 : 16;
+    constexpr int NPW = SRC == SRC_TENSOR ? 1 : 12;
     auto k = level_kernel<T, CIN, C3, C1, SRC, DST, NB, NIN, NMID, NPW>;
     static bool attr = false;
     if (!attr) {
