@@ -1098,7 +1098,7 @@ struct LvGeom {
     static constexpr int OFF_LO = round128(OFF_SK + SKB);
     static constexpr int OFF_B = round128(OFF_LO + 2 * LOB);   // low-res staging double-buffered
     static constexpr int OFF_BAR = (OFF_B + (C3 + C1) * 4 + 15) / 16 * 16;
-    static constexpr int SMEM = OFF_BAR + 192;
+    static constexpr int SMEM = OFF_BAR + 256;
     static constexpr int ACC3 = 0, ACC1 = 2 * NB * C3;         // TMEM columns (both double-buffered)
     static constexpr int TCOLS = tmem_cols(2 * NB * (C3 + C1));
     static constexpr int TX_BYTES = NCI * PIN;
@@ -1145,18 +1145,19 @@ __global__ void __launch_bounds__((NPW + 9) * 32, 1) level_kernel(const __grid_c
     using G = LvGeom<CIN, C3, C1, NB, NIN, NMID, SRC == SRC_UP>;
     extern __shared__ __align__(128) uint8_t smem[];
     uint64_t* bar = reinterpret_cast<uint64_t*>(smem + G::OFF_BAR);
-    uint64_t* in_full = bar + 0;      // [2]
-    uint64_t* in_empty = bar + 2;     // [2]
-    uint64_t* a3_full = bar + 4;
-    uint64_t* a3_empty = bar + 6;
-    uint64_t* mid_full = bar + 8;
-    uint64_t* mid_empty = bar + 10;
-    uint64_t* a1_full = bar + 12;
-    uint64_t* a1_empty = bar + 14;
-    uint64_t* wbar = bar + 16;        // weights landed
-    uint64_t* skf = bar + 17;         // SRC_UP: skip rows 0-8 / 9-17 of the tile landed [2]
-    uint64_t* lof = bar + 19;         // SRC_UP: low-res tile landed, double-buffered [2]
-    uint32_t* tptr = reinterpret_cast<uint32_t*>(smem + G::OFF_BAR + 176);
+    static_assert(NIN <= 4 && NMID <= 2, "barrier slots");
+    uint64_t* in_full = bar + 0;      // [NIN]
+    uint64_t* in_empty = bar + 4;     // [NIN]
+    uint64_t* a3_full = bar + 8;
+    uint64_t* a3_empty = bar + 10;
+    uint64_t* mid_full = bar + 12;
+    uint64_t* mid_empty = bar + 14;
+    uint64_t* a1_full = bar + 16;
+    uint64_t* a1_empty = bar + 18;
+    uint64_t* wbar = bar + 20;        // weights landed
+    uint64_t* skf = bar + 21;         // SRC_UP: skip rows 0-8 / 9-17 of the tile landed [2]
+    uint64_t* lof = bar + 23;         // SRC_UP: low-res tile landed, double-buffered [2]
+    uint32_t* tptr = reinterpret_cast<uint32_t*>(smem + G::OFF_BAR + 208);
     float* sb3 = reinterpret_cast<float*>(smem + G::OFF_B);
     float* sb1 = sb3 + C3;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -1175,9 +1176,11 @@ __global__ void __launch_bounds__((NPW + 9) * 32, 1) level_kernel(const __grid_c
     if (tid == 0) pdl_trigger();
     if (warp == EW0) tmem_alloc<G::TCOLS>(tptr);
     if (tid == 0) {
-        for (int i = 0; i < 2; ++i) {
+        for (int i = 0; i < NIN; ++i) {
             mbar_init(&in_full[i], SRC == SRC_TENSOR ? 1 : NPT);
             mbar_init(&in_empty[i], 1);
+        }
+        for (int i = 0; i < 2; ++i) {
             mbar_init(&a3_full[i], 1);
             mbar_init(&a3_empty[i], 256);
             mbar_init(&mid_full[i], 256);
