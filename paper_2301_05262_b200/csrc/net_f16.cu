@@ -148,6 +148,23 @@ void pack_umma(const float* w, int cout, int cin, int k, std::vector<uint16_t>& 
                     }
 }
 
+// Tile decode without integer division: q = (n * ceil(2^32 / d)) >> 32 is
+// floor(n / d) whenever n * d < 2^32 (tiles and tiles-per-frame < 2^16);
+// the multiplier is 2^32 itself for d = 1, hence 64-bit.
+struct TileDiv {
+    int nx, nxy;
+    uint64_t mnx, mnxy;
+};
+
+__host__ __device__ inline TileDiv tile_div(int H0, int W0) {
+    TileDiv d;
+    d.nx = (W0 + E0_TW - 1) / E0_TW;
+    d.nxy = d.nx * ((H0 + E0_TH - 1) / E0_TH);
+    d.mnx = 0xFFFFFFFFull / (uint64_t)d.nx + 1ull;
+    d.mnxy = 0xFFFFFFFFull / (uint64_t)d.nxy + 1ull;
+    return d;
+}
+
 // ------------------------------------------------------------- level 0 (mma.sync)
 struct Enc0Args {
     GBufK g;
@@ -164,6 +181,7 @@ struct Enc0Args {
     void* out;            // pooled (N, H0/2, W0/2, 16)
     int64_t* first_bad;
     int dbg;              // experiments only: 1 skip feature math, 2 skip convolutions
+    TileDiv td;           // tile decode constants (host-computed, read from the param bank)
 };
 
 // Stage-1 per-pixel math of the fused kernel: fp64 projection for the texel
@@ -222,12 +240,6 @@ __device__ __forceinline__ void conv3_strip16(uint32_t sbase, int plane, int row
     const uint32_t a_off = (lm >> 1) * plane + (kPairRows ? 2 * li + (lm & 1) : li + 8 * (lm & 1)) * 16;
     float acc[3][2][4];
 #pragma unroll
-    for (int s = 0; s < 3; ++s)
-#pragma unroll
-        for (int n = 0; n < 2; ++n)
-#pragma unroll
-            for (int e = 0; e < 4; ++e) acc[s][n][e] = binit[n][e & 1];
-#pragma unroll
     for (int ir = 0; ir < ROWS + 2; ++ir) {
         hook(ir);
         uint32_t A[3][4];
@@ -243,17 +255,18 @@ __device__ __forceinline__ void conv3_strip16(uint32_t sbase, int plane, int row
                 const int oo = ir - ky;
                 if (oo >= 0 && oo < ROWS) {
 #pragma unroll
-                    for (int n = 0; n < 2; ++n)
-                        mma16816<T>(acc[oo % 3][n], A[dx], B3[ky * 3 + dx][n][0], B3[ky * 3 + dx][n][1]);
+                    for (int n = 0; n < 2; ++n) {
+                        if (ky == 0 && dx == 0)          // first tap of output row oo: C = bias
+                            mma16816_c<T>(acc[oo % 3][n], A[dx], B3[ky * 3 + dx][n][0], B3[ky * 3 + dx][n][1],
+                                          binit[n][0], binit[n][1], binit[n][0], binit[n][1]);
+                        else
+                            mma16816<T>(acc[oo % 3][n], A[dx], B3[ky * 3 + dx][n][0], B3[ky * 3 + dx][n][1]);
+                    }
                 }
             }
         if (ir >= 2) {
             const int oo = ir - 2;
             epi(oo, acc[oo % 3]);
-#pragma unroll
-            for (int n = 0; n < 2; ++n)
-#pragma unroll
-                for (int e = 0; e < 4; ++e) acc[oo % 3][n][e] = binit[n][e & 1];
         }
     }
 }
@@ -336,6 +349,16 @@ __device__ __forceinline__ L0Tile l0_tile(int tile, int H0, int W0) {
     t.tx0 = (tile % nx) * E0_TW;
     t.ty0 = ((tile / nx) % ny) * E0_TH;
     t.f = tile / (nx * ny);
+    return t;
+}
+
+__device__ __forceinline__ L0Tile l0_tile(int tile, const TileDiv& d) {
+    L0Tile t;
+    t.f = (int)(((uint64_t)(uint32_t)tile * d.mnxy) >> 32);
+    const int r = tile - t.f * d.nxy;
+    const int ty = (int)(((uint64_t)(uint32_t)r * d.mnx) >> 32);
+    t.ty0 = ty * E0_TH;
+    t.tx0 = (r - ty * d.nx) * E0_TW;
     return t;
 }
 
@@ -471,6 +494,13 @@ struct QuadRegs {
     float look[4];
 };
 
+// Phase-A results bound for the tile buffer: (z_f, (ch2, ch3)) per pixel.
+// A tile's first half parks them in registers until the consumers release
+// the buffer, so that waiting never delays the previous tile's last half.
+struct QuadPark {
+    uint2 v[4];
+};
+
 template <typename T>
 __device__ __forceinline__ void produce_features_tma(const Enc0Args& a, const GbufMaps& tm, int total) {
     // Software pipeline over half-tiles q (two per tile):
@@ -496,7 +526,7 @@ __device__ __forceinline__ void produce_features_tma(const Enc0Args& a, const Gb
             for (int q = 0; q < nh; ++q) {
                 const int sidx = q & 1;
                 if (q >= 2) mbar_wait(&empty[sidx], ((q - 2) >> 1) & 1);
-                const L0Tile tl = l0_tile(blockIdx.x + (q >> 1) * gridDim.x, a.H0, a.W0);
+                const L0Tile tl = l0_tile(blockIdx.x + (q >> 1) * gridDim.x, a.td);
                 const uint32_t dst = smem_u32(stage + sidx * ST_BYTES);
                 const int x = 2 * tl.tx0 - 4, y = 2 * tl.ty0 - 2 + ST_ROWS * (q & 1);
                 mbar_expect_tx(&full[sidx], ST_TX);
@@ -518,8 +548,15 @@ __device__ __forceinline__ void produce_features_tma(const Enc0Args& a, const Gb
     const int lds_lo = qy * ST_TCOLS * 4 + 8 + 8 * px_lo, lds_hi = qy * ST_TCOLS * 4 + 8 + 8 * px_hi;
     const int sts_row = (qy & 1) * E0_PLANE + (qy >> 1) * E0_IC * 16;
     const int slot_lo = sts_row + px_lo * 16, slot_hi = sts_row + px_hi * 16;
-    auto phaseA = [&](int q, QuadRegs& R) {
-        const L0Tile tl = l0_tile(blockIdx.x + (q >> 1) * gridDim.x, a.H0, a.W0);
+    auto park = [&](int q, const QuadPark& P) {
+        if (!active) return;
+        uint8_t* tdst = smem + ((q >> 1) & 1) * E0_SMEM + (q & 1) * (ST_ROWS / 2) * E0_IC * 16;
+#pragma unroll
+        for (int e = 0; e < 4; ++e)
+            *reinterpret_cast<uint2*>(tdst + (e < 2 ? slot_lo : slot_hi) + (e & 1) * 8) = P.v[e];
+    };
+    auto phaseA = [&](int q, QuadRegs& R, QuadPark& P) {
+        const L0Tile tl = l0_tile(blockIdx.x + (q >> 1) * gridDim.x, a.td);
         const int sidx = q & 1;
         if (!active) return;
         const FrameK& F = a.tab.f[tl.f];
@@ -538,12 +575,11 @@ __device__ __forceinline__ void produce_features_tma(const Enc0Args& a, const Gb
             }
         };
         ld4(0, dv);
-        uint8_t* tdst = smem + ((q >> 1) & 1) * E0_SMEM + (q & 1) * (ST_ROWS / 2) * E0_IC * 16;
         if (!(dv[0] > 0.f || dv[1] > 0.f || dv[2] > 0.f || dv[3] > 0.f)) {   // nothing covered
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
                 R.look[e] = -1.f;
-                *reinterpret_cast<uint2*>(tdst + (e < 2 ? slot_lo : slot_hi) + (e & 1) * 8) = make_uint2(0u, 0u);
+                P.v[e] = make_uint2(0u, 0u);
             }
             return;
         }
@@ -576,8 +612,7 @@ __device__ __forceinline__ void produce_features_tma(const Enc0Args& a, const Gb
             const float cc = __saturatef(fmaf(nx, dx, fmaf(ny, dy, nz * dz)) *
                                          rsqrtf(fmaf(dx, dx, fmaf(dy, dy, dz * dz))));
             const float c2 = __saturatef(fmaf(nx, tx, fmaf(ny, ty, nz * tz)) * izf) + size;
-            *reinterpret_cast<uint2*>(tdst + (e < 2 ? slot_lo : slot_hi) + (e & 1) * 8) =
-                make_uint2(__float_as_uint(l2 * izf), cov ? Elem<T>::pack(c2, __fdividef(cc, d)) : 0u);
+            P.v[e] = make_uint2(__float_as_uint(l2 * izf), cov ? Elem<T>::pack(c2, __fdividef(cc, d)) : 0u);
         }
         if (bad) {   // FrustumError: the quad's leftmost bad pixel (raster.py:251-255)
             const int e = __ffs(bad) - 1;
@@ -587,7 +622,7 @@ __device__ __forceinline__ void produce_features_tma(const Enc0Args& a, const Gb
     };
     auto phaseB = [&](int q, const QuadRegs& R) {
         if (!active) return;
-        const L0Tile tl = l0_tile(blockIdx.x + (q >> 1) * gridDim.x, a.H0, a.W0);
+        const L0Tile tl = l0_tile(blockIdx.x + (q >> 1) * gridDim.x, a.td);
         const float bias = a.tab.f[tl.f].fbias;
         uint8_t* dst = smem + ((q >> 1) & 1) * E0_SMEM + (q & 1) * (ST_ROWS / 2) * E0_IC * 16;
 #pragma unroll
@@ -604,21 +639,27 @@ __device__ __forceinline__ void produce_features_tma(const Enc0Args& a, const Gb
         }
     };
     auto step = [&](int q, QuadRegs& RA, QuadRegs& RB) {
+        QuadPark P;
         if (q < nh) {
-            // phase A of a tile's first half already writes (ch2, ch3) into
-            // the tile buffer, so it waits for the consumers to release it
-            const int k = q >> 1;
-            if (!(q & 1) && k >= 2) mbar_wait(&freed[k & 1], ((k - 2) >> 1) & 1);
             mbar_wait(&full[q & 1], (q >> 1) & 1);
-            if (!(a.dbg & 1)) phaseA(q, RA);
+            if (!(a.dbg & 1)) phaseA(q, RA, P);
+            else for (int e = 0; e < 4; ++e) RA.look[e] = -1.f, P.v[e] = make_uint2(0u, 0u);
             __syncwarp();
             if (lane == 0) mbar_arrive(&empty[q & 1]);                   // stage read
+            if (q & 1) park(q, P);            // second half: the buffer is ours already
         }
         if (q >= 1) {
             const int qb = q - 1, k = qb >> 1;
-            if (!(a.dbg & 1)) phaseB(qb, RB);
+            phaseB(qb, RB);
             __syncwarp();
             if (lane == 0) mbar_arrive(&half[(k & 1) * 2 + (qb & 1)]);   // rows of half qb&1 done
+        }
+        if (q < nh && !(q & 1)) {
+            // a tile's first half: wait for the consumers to release the
+            // buffer (after finishing the previous tile above), then park
+            const int k = q >> 1;
+            if (k >= 2) mbar_wait(&freed[k & 1], ((k - 2) >> 1) & 1);
+            park(q, P);
         }
     };
     QuadRegs RA, RB;
@@ -662,7 +703,7 @@ __global__ void __launch_bounds__(kSrc == 2 ? kE0Threads : kL0Threads, 1) enc0_k
             produce_features_tma<T>(a, tm, total);
         } else {
             l0_produce_loop(total, [&](uint8_t* buf, int tile) {
-                produce_features<T, kSrc == 1>(a, buf, l0_tile(tile, a.H0, a.W0));
+                produce_features<T, kSrc == 1>(a, buf, l0_tile(tile, a.td));
             });
         }
         return;
@@ -699,7 +740,7 @@ __global__ void __launch_bounds__(kSrc == 2 ? kE0Threads : kL0Threads, 1) enc0_k
     }
     T* out = reinterpret_cast<T*>(a.out);
     auto consume = [&](uint8_t* buf, int tile, auto&& hook) {
-            const L0Tile tl = l0_tile(tile, a.H0, a.W0);
+            const L0Tile tl = l0_tile(tile, a.td);
             float pp[2][2];
             if (a.dbg & 2) {
                 hook(E0_IR / 2);
@@ -711,9 +752,7 @@ __global__ void __launch_bounds__(kSrc == 2 ? kE0Threads : kL0Threads, 1) enc0_k
                 float u[2][4];
 #pragma unroll
                 for (int n = 0; n < 2; ++n) {
-#pragma unroll
-                    for (int e = 0; e < 4; ++e) u[n][e] = bias1[n][e & 1];
-                    mma16816<T>(u[n], a1, B1[n][0], B1[n][1]);
+                    mma16816_c<T>(u[n], a1, B1[n][0], B1[n][1], bias1[n][0], bias1[n][1], bias1[n][0], bias1[n][1]);
                 }
                 // avg_pool2: rows oo-1, oo summed in registers; the x
                 // neighbours are this thread's e and e + 2 (kPairRows)
@@ -772,6 +811,7 @@ struct Dec0Args {
     const float* bh;
     float* y;             // head output, 4 fp32 planes per frame: (N, 4, H0, W0)
     int dbg;              // experiments only: 1 skip upsample math, 2 skip convolutions
+    TileDiv td;
 };
 
 // Bilinear 2x of an NHWC 16-bit tensor at one output pixel, 8 channels
@@ -822,7 +862,7 @@ __global__ void __launch_bounds__(kL0Threads, 1) dec0_kernel(const __grid_consta
         const int ptid = threadIdx.x;
         const int mytiles = (int)blockIdx.x < total ? (total - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x : 0;
         auto issue = [&](int k) {
-            const L0Tile tl = l0_tile(blockIdx.x + k * gridDim.x, a.H0, a.W0);
+            const L0Tile tl = l0_tile(blockIdx.x + k * gridDim.x, a.td);
             mbar_expect_tx(&full[k & 1], D0_LR * D0_LC * 32);
             tma_load_4d(smem_u32(stg + (k & 1) * D0_STG), &tm, 0, tl.tx0 / 2 - 1, tl.ty0 / 2 - 1, tl.f, &full[k & 1]);
         };
@@ -837,7 +877,7 @@ __global__ void __launch_bounds__(kL0Threads, 1) dec0_kernel(const __grid_consta
             if (mytiles > 1) issue(1);
         }
         for (int k = 0; k < mytiles; ++k) {
-            const L0Tile tl = l0_tile(blockIdx.x + k * gridDim.x, a.H0, a.W0);
+            const L0Tile tl = l0_tile(blockIdx.x + k * gridDim.x, a.td);
             const int sb = k & 1;
             if (k >= 2) nbar_sync(3 + sb, kL0Threads);
             uint8_t* buf = smem + sb * E0_SMEM;
@@ -944,7 +984,7 @@ __global__ void __launch_bounds__(kL0Threads, 1) dec0_kernel(const __grid_consta
     }
     l0_consume_loop(total,
         [&](uint8_t* buf, int tile) {
-            const L0Tile tl = l0_tile(tile, a.H0, a.W0);
+            const L0Tile tl = l0_tile(tile, a.td);
             if (a.dbg & 2) return;
             conv3_strip16<T, 8>(smem_u32(buf), E0_PLANE, E0_IC, r0, sx, B3, bias3, [&](int oo, float (&acc)[2][4]) {
                 uint32_t a1[4], a2[4];
@@ -952,13 +992,11 @@ __global__ void __launch_bounds__(kL0Threads, 1) dec0_kernel(const __grid_consta
                 float u[2][4];
 #pragma unroll
                 for (int n = 0; n < 2; ++n) {
-#pragma unroll
-                    for (int e = 0; e < 4; ++e) u[n][e] = bias1[n][e & 1];
-                    mma16816<T>(u[n], a1, B1[n][0], B1[n][1]);
+                    mma16816_c<T>(u[n], a1, B1[n][0], B1[n][1], bias1[n][0], bias1[n][1], bias1[n][0], bias1[n][1]);
                 }
                 relu_pack_a<T>(u, a2);
-                float yh[4] = {biash[0], biash[1], biash[0], biash[1]};
-                mma16816<T>(yh, a2, BH[0], BH[1]);
+                float yh[4];
+                mma16816_c<T>(yh, a2, BH[0], BH[1], biash[0], biash[1], biash[0], biash[1]);
                 const int oy = tl.ty0 + r0 + oo;
                 if (t < 2 && oy < a.H0) {
                     const int64_t hw0 = (int64_t)a.H0 * a.W0;
@@ -1711,7 +1749,8 @@ nsm_status run_l0(const Plan& p, const Bufs& b, const Enc0Args& e0, const GbufMa
     const Level& L0 = p.lev[0];
     static const int d0dbg = getenv("NSM_DEC0_DBG") ? atoi(getenv("NSM_DEC0_DBG")) : 0;
     Dec0Args d{b.d1, H0, W0, (const uint2*)L0.dec3.wpk, (const uint2*)L0.dec1.wpk,
-               (const uint2*)p.head.wpk, L0.dec3.b32, L0.dec1.b32, p.head.b32, b.y, d0dbg};
+               (const uint2*)p.head.wpk, L0.dec3.b32, L0.dec1.b32, p.head.b32, b.y, d0dbg,
+               tile_div(H0, W0)};
     {
         CUtensorMap dm;
         memset(&dm, 0, sizeof dm);
@@ -1822,6 +1861,7 @@ nsm_status infer_f16(const Plan& p, const nsm_gbuffer* g, const float* sm, int64
         e.w = w;
         e.H0 = H0;
         e.W0 = W0;
+        e.td = tile_div(H0, W0);
         e.wb3 = (const uint2*)p.lev[0].enc3.wpk;
         e.wb1 = (const uint2*)p.lev[0].enc1.wpk;
         e.b3 = p.lev[0].enc3.b32;
@@ -1858,6 +1898,7 @@ nsm_status forward_f16(const Plan& p, const float* x, int n, int h, int w, float
         e.w = w;
         e.H0 = H0;
         e.W0 = W0;
+        e.td = tile_div(H0, W0);
         e.wb3 = (const uint2*)p.lev[0].enc3.wpk;
         e.wb1 = (const uint2*)p.lev[0].enc1.wpk;
         e.b3 = p.lev[0].enc3.b32;

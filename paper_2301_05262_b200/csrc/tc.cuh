@@ -82,6 +82,32 @@ __device__ __forceinline__ void mma16816<__nv_bfloat16>(float c[4], const uint32
         : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
 }
 
+// d = a * b + c with a separate C operand (the accumulator starts at c, e.g.
+// a bias, without register copies).
+template <typename T>
+__device__ __forceinline__ void mma16816_c(float d[4], const uint32_t a[4], uint32_t b0, uint32_t b1, float c0,
+                                           float c1, float c2, float c3);
+
+template <>
+__device__ __forceinline__ void mma16816_c<__half>(float d[4], const uint32_t a[4], uint32_t b0, uint32_t b1,
+                                                   float c0, float c1, float c2, float c3) {
+    asm volatile(
+        "mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+        "{%10,%11,%12,%13};\n"
+        : "=f"(d[0]), "=f"(d[1]), "=f"(d[2]), "=f"(d[3])
+        : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1), "f"(c0), "f"(c1), "f"(c2), "f"(c3));
+}
+
+template <>
+__device__ __forceinline__ void mma16816_c<__nv_bfloat16>(float d[4], const uint32_t a[4], uint32_t b0,
+                                                          uint32_t b1, float c0, float c1, float c2, float c3) {
+    asm volatile(
+        "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+        "{%10,%11,%12,%13};\n"
+        : "=f"(d[0]), "=f"(d[1]), "=f"(d[2]), "=f"(d[3])
+        : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1), "f"(c0), "f"(c1), "f"(c2), "f"(c3));
+}
+
 // ---------------------------------------------------------------- tcgen05
 // SMEM matrix descriptor, SWIZZLE_NONE, K-major canonical layout
 // ((8, m), (8 elems, k)) : ((16 B, SBO), (2 B, LBO)); version bits = 1.
