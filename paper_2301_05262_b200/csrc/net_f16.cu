@@ -239,13 +239,19 @@ __device__ __forceinline__ void conv3_strip16(uint32_t sbase, int plane, int row
     const int lm = lane >> 3, li = lane & 7;
     const uint32_t a_off = (lm >> 1) * plane + (kPairRows ? 2 * li + (lm & 1) : li + 8 * (lm & 1)) * 16;
     float acc[3][2][4];
-#pragma unroll
-    for (int ir = 0; ir < ROWS + 2; ++ir) {
+    // A fragments double-buffered: row ir+1 is loaded before row ir's MMAs
+    uint32_t Ab[2][3][4];
+    auto load_row = [&](int ir, uint32_t (&A)[3][4]) {
         hook(ir);
-        uint32_t A[3][4];
 #pragma unroll
         for (int dx = 0; dx < 3; ++dx)
             ldsm_x4(sbase + a_off + ((r0 + ir) * rowpix + sx + dx) * 16, A[dx]);
+    };
+    load_row(0, Ab[0]);
+#pragma unroll
+    for (int ir = 0; ir < ROWS + 2; ++ir) {
+        if (ir + 1 < ROWS + 2) load_row(ir + 1, Ab[(ir + 1) & 1]);
+        uint32_t (&A)[3][4] = Ab[ir & 1];
         // dx outer, (ky, n) inner: consecutive MMAs go to up to 6 different
         // accumulators, so no MMA waits on the one just issued
 #pragma unroll
