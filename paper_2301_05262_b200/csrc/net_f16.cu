@@ -849,6 +849,75 @@ __device__ __forceinline__ void up2_chunk(const T* x, int hl, int wl, int C, int
     }
 }
 
+// 2x bilinear upsampling of one 8-channel chunk for the 2x2 output block of
+// a low-res pixel: q[u][v] = the chunk at column u, row v of its clamped 3x3
+// neighbourhood; out[2 aa + bb] = the output (2i + aa, 2j + bb), packed.
+// Rows then columns with weights (1/4, 3/4) like _upsample_taps
+// (autodiff.py:258-287).  fp16: packed half2 arithmetic (each FMA rounds to
+// fp16, the result is stored as fp16 anyway); bf16: fp32 arithmetic, one
+// rounding at the end (bf16 has too few mantissa bits to round twice).
+template <typename T>
+__device__ __forceinline__ void up2_block(const uint4 (&q)[3][3], uint4 (&out)[4]) {
+    if constexpr (std::is_same<T, __half>::value) {
+        const __half2 w1 = __float2half2_rn(0.25f), w3 = __float2half2_rn(0.75f);
+        __half2 top[3][4], bot[3][4];
+#pragma unroll
+        for (int u = 0; u < 3; ++u) {
+            const __half2* s0 = reinterpret_cast<const __half2*>(&q[u][0]);
+            const __half2* s1 = reinterpret_cast<const __half2*>(&q[u][1]);
+            const __half2* s2 = reinterpret_cast<const __half2*>(&q[u][2]);
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                top[u][e] = __hfma2(s1[e], w3, __hmul2(s0[e], w1));
+                bot[u][e] = __hfma2(s1[e], w3, __hmul2(s2[e], w1));
+            }
+        }
+#pragma unroll
+        for (int ab = 0; ab < 4; ++ab) {
+            const __half2(&vr)[3][4] = (ab >> 1) ? bot : top;
+            __half2* o = reinterpret_cast<__half2*>(&out[ab]);
+#pragma unroll
+            for (int e = 0; e < 4; ++e)
+                o[e] = (ab & 1) ? __hfma2(vr[1][e], w3, __hmul2(vr[2][e], w1))
+                                : __hfma2(vr[1][e], w3, __hmul2(vr[0][e], w1));
+        }
+    } else {
+        float top[3][8], bot[3][8];
+#pragma unroll
+        for (int u = 0; u < 3; ++u) {
+            float sv[3][8];
+#pragma unroll
+            for (int v = 0; v < 3; ++v) {
+                const uint32_t* qw = &q[u][v].x;
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    const float2 f2 = Elem<T>::unpack(qw[e]);
+                    sv[v][2 * e] = f2.x;
+                    sv[v][2 * e + 1] = f2.y;
+                }
+            }
+#pragma unroll
+            for (int e = 0; e < 8; ++e) {
+                top[u][e] = 0.25f * sv[0][e] + 0.75f * sv[1][e];
+                bot[u][e] = 0.75f * sv[1][e] + 0.25f * sv[2][e];
+            }
+        }
+#pragma unroll
+        for (int ab = 0; ab < 4; ++ab) {
+            const float(&vr)[3][8] = (ab >> 1) ? bot : top;
+            uint32_t* qo = &out[ab].x;
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                const float x0 = (ab & 1) ? 0.75f * vr[1][2 * e] + 0.25f * vr[2][2 * e]
+                                          : 0.25f * vr[0][2 * e] + 0.75f * vr[1][2 * e];
+                const float x1 = (ab & 1) ? 0.75f * vr[1][2 * e + 1] + 0.25f * vr[2][2 * e + 1]
+                                          : 0.25f * vr[0][2 * e + 1] + 0.75f * vr[1][2 * e + 1];
+                qo[e] = Elem<T>::pack(x0, x1);
+            }
+        }
+    }
+}
+
 // dec0 source staging: the D1 (level-1, 16 ch) pixels a level-0 tile's
 // up2 reads, (TH/2 + 2) x (TW/2 + 2), pixel-major, double-buffered by TMA.
 constexpr int D0_LR = E0_TH / 2 + 2, D0_LC = E0_TW / 2 + 2;
@@ -905,46 +974,21 @@ __global__ void __launch_bounds__(kL0Threads, 1) dec0_kernel(const __grid_consta
                     rs[u] = min(max(min(max(bi - 1 + u, 0), H1 - 1) - ly0, 0), D0_LR - 1);
                     cs[u] = min(max(min(max(bj - 1 + u, 0), W1 - 1) - lx0, 0), D0_LC - 1);
                 }
-                float top[3][8], bot[3][8];
+                uint4 qn[3][3], ob[4];
 #pragma unroll
-                for (int u = 0; u < 3; ++u) {
-                    float sv[3][8];
+                for (int u = 0; u < 3; ++u)
 #pragma unroll
-                    for (int v = 0; v < 3; ++v) {
-                        const uint4 q = *reinterpret_cast<const uint4*>(lo + ((rs[v] * D0_LC + cs[u]) * 16 + c * 8) * 2);
-                        const uint32_t* qw = &q.x;
-#pragma unroll
-                        for (int e = 0; e < 4; ++e) {
-                            const float2 f2 = Elem<T>::unpack(qw[e]);
-                            sv[v][2 * e] = f2.x;
-                            sv[v][2 * e + 1] = f2.y;
-                        }
-                    }
-#pragma unroll
-                    for (int e = 0; e < 8; ++e) {
-                        top[u][e] = 0.25f * sv[0][e] + 0.75f * sv[1][e];
-                        bot[u][e] = 0.75f * sv[1][e] + 0.25f * sv[2][e];
-                    }
-                }
+                    for (int v = 0; v < 3; ++v)
+                        qn[u][v] = *reinterpret_cast<const uint4*>(lo + ((rs[v] * D0_LC + cs[u]) * 16 + c * 8) * 2);
+                up2_block<T>(qn, ob);
 #pragma unroll
                 for (int ab = 0; ab < 4; ++ab) {
                     const int aa = ab >> 1, bb = ab & 1;
                     const int oy = 2 * bi + aa, ox = 2 * bj + bb;        // level-0 pixel
                     const int ti = oy - (tl.ty0 - 1), tj = ox - (tl.tx0 - 1);
                     if (ti < 0 || ti >= E0_IR || tj < 0 || tj >= E0_IC) continue;
-                    uint4 q = make_uint4(0u, 0u, 0u, 0u);
-                    if (oy >= 0 && ox >= 0 && oy < a.H0 && ox < a.W0) {
-                        const float(&vr)[3][8] = aa ? bot : top;
-                        uint32_t* qo = &q.x;
-#pragma unroll
-                        for (int e = 0; e < 4; ++e) {
-                            const float x0 = bb ? 0.75f * vr[1][2 * e] + 0.25f * vr[2][2 * e]
-                                                : 0.25f * vr[0][2 * e] + 0.75f * vr[1][2 * e];
-                            const float x1 = bb ? 0.75f * vr[1][2 * e + 1] + 0.25f * vr[2][2 * e + 1]
-                                                : 0.25f * vr[0][2 * e + 1] + 0.75f * vr[1][2 * e + 1];
-                            qo[e] = Elem<T>::pack(x0, x1);
-                        }
-                    }
+                    const bool in = oy >= 0 && ox >= 0 && oy < a.H0 && ox < a.W0;
+                    const uint4 q = in ? ob[ab] : make_uint4(0u, 0u, 0u, 0u);
                     *reinterpret_cast<uint4*>(buf + c * E0_PLANE + (ti * E0_IC + tj) * 16) = q;
                 }
             }
