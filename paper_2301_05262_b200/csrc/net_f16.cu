@@ -918,6 +918,26 @@ __device__ __forceinline__ void up2_block(const uint4 (&q)[3][3], uint4 (&out)[4
     }
 }
 
+// a + b of two packed 8-channel chunks (the decoder skip sum): half2 adds on
+// fp16 plans, fp32 with one rounding on bf16.
+template <typename T>
+__device__ __forceinline__ uint4 add_packed(uint4 a, uint4 b) {
+    uint4 r;
+    const uint32_t *pa = &a.x, *pb = &b.x;
+    uint32_t* pr = &r.x;
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+        if constexpr (std::is_same<T, __half>::value) {
+            const __half2 v = __hadd2(*reinterpret_cast<const __half2*>(&pa[e]), *reinterpret_cast<const __half2*>(&pb[e]));
+            pr[e] = *reinterpret_cast<const uint32_t*>(&v);
+        } else {
+            const float2 x = Elem<T>::unpack(pa[e]), y = Elem<T>::unpack(pb[e]);
+            pr[e] = Elem<T>::pack(x.x + y.x, x.y + y.y);
+        }
+    }
+    return r;
+}
+
 // dec0 source staging: the D1 (level-1, 16 ch) pixels a level-0 tile's
 // up2 reads, (TH/2 + 2) x (TW/2 + 2), pixel-major, double-buffered by TMA.
 constexpr int D0_LR = E0_TH / 2 + 2, D0_LC = E0_TW / 2 + 2;
@@ -1377,27 +1397,13 @@ __global__ void __launch_bounds__((NPW + 9) * 32, 1) level_kernel(const __grid_c
                             rs[u] = min(max(min(max(bi - 1 + u, 0), hl - 1) - ly0, 0), G::LR - 1);
                             cs[u] = min(max(min(max(bj - 1 + u, 0), wl - 1) - lx0, 0), G::LC - 1);
                         }
-                        float top[3][8], bot[3][8];
+                        uint4 qn[3][3], ob[4];
 #pragma unroll
-                        for (int u = 0; u < 3; ++u) {
-                            float sv[3][8];
+                        for (int u = 0; u < 3; ++u)
 #pragma unroll
-                            for (int v = 0; v < 3; ++v) {
-                                const uint4 q = *reinterpret_cast<const uint4*>(lo + ((rs[v] * G::LC + cs[u]) * CIN + c * 8) * 2);
-                                const uint32_t* qw = &q.x;
-#pragma unroll
-                                for (int e = 0; e < 4; ++e) {
-                                    const float2 f2 = Elem<T>::unpack(qw[e]);
-                                    sv[v][2 * e] = f2.x;
-                                    sv[v][2 * e + 1] = f2.y;
-                                }
-                            }
-#pragma unroll
-                            for (int e = 0; e < 8; ++e) {
-                                top[u][e] = 0.25f * sv[0][e] + 0.75f * sv[1][e];
-                                bot[u][e] = 0.75f * sv[1][e] + 0.25f * sv[2][e];
-                            }
-                        }
+                            for (int v = 0; v < 3; ++v)
+                                qn[u][v] = *reinterpret_cast<const uint4*>(lo + ((rs[v] * G::LC + cs[u]) * CIN + c * 8) * 2);
+                        up2_block<T>(qn, ob);
 #pragma unroll
                         for (int ab = 0; ab < 4; ++ab) {
                             const int aa = ab >> 1, bb = ab & 1;
@@ -1407,19 +1413,10 @@ __global__ void __launch_bounds__((NPW + 9) * 32, 1) level_kernel(const __grid_c
                             const int p = ti * G::IC + tj;
                             uint4 q = make_uint4(0u, 0u, 0u, 0u);
                             if (yy >= 0 && xx >= 0 && yy < a.H && xx < a.W) {
-                                uint4 qs = make_uint4(0u, 0u, 0u, 0u);
-                                if (a.skip) qs = *reinterpret_cast<const uint4*>(sk + (p * CIN + c * 8) * 2);
-                                const uint32_t* as = &qs.x;
-                                const float(&vr)[3][8] = aa ? bot : top;
-                                uint32_t* qo = &q.x;
-#pragma unroll
-                                for (int e = 0; e < 4; ++e) {
-                                    const float2 ps = Elem<T>::unpack(as[e]);
-                                    const float x0v = bb ? 0.75f * vr[1][2 * e] + 0.25f * vr[2][2 * e]
-                                                         : 0.25f * vr[0][2 * e] + 0.75f * vr[1][2 * e];
-                                    const float x1v = bb ? 0.75f * vr[1][2 * e + 1] + 0.25f * vr[2][2 * e + 1]
-                                                         : 0.25f * vr[0][2 * e + 1] + 0.75f * vr[1][2 * e + 1];
-                                    qo[e] = Elem<T>::pack(x0v + ps.x, x1v + ps.y);
+                                q = ob[ab];
+                                if (a.skip) {          // up2(low) + skip (network.py:189-194)
+                                    const uint4 qs = *reinterpret_cast<const uint4*>(sk + (p * CIN + c * 8) * 2);
+                                    q = add_packed<T>(q, qs);
                                 }
                             }
                             *reinterpret_cast<uint4*>(in + c * G::PIN + p * 16) = q;
