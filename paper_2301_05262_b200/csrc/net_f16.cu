@@ -748,6 +748,11 @@ __global__ void __launch_bounds__(kSrc == 2 ? kE0Threads : kL0Threads, 1) enc0_k
     auto consume = [&](uint8_t* buf, int tile, auto&& hook) {
             const L0Tile tl = l0_tile(tile, a.td);
             float pp[2][2];
+            // pooled pixel ((ty0 + r0) / 2 + oo / 2, (tx0 + sx) / 2 + g): one 64-bit
+            // base per tile, 32-bit row offsets
+            const int px = ((tl.tx0 + sx) >> 1) + g;
+            const bool px_ok = px < W1;
+            T* obase = out + (((int64_t)tl.f * H1 + ((tl.ty0 + r0) >> 1)) * W1 + px) * 16 + 2 * t;
             if (a.dbg & 2) {
                 hook(E0_IR / 2);
                 return;
@@ -771,10 +776,8 @@ __global__ void __launch_bounds__(kSrc == 2 ? kE0Threads : kL0Threads, 1) enc0_k
                         else pp[n][e] = v;
                     }
                 if (oo & 1) {                                           // avg_pool2 of rows oo-1, oo
-                    const int py = (tl.ty0 + r0 + oo) >> 1;
-                    const int px = ((tl.tx0 + sx) >> 1) + g;
-                    if (py < H1 && px < W1) {
-                        T* o = out + (((int64_t)tl.f * H1 + py) * W1 + px) * 16 + 2 * t;
+                    if (((tl.ty0 + r0 + oo) >> 1) < H1 && px_ok) {
+                        T* o = obase + (oo >> 1) * W1 * 16;
 #pragma unroll
                         for (int n = 0; n < 2; ++n)
                             *reinterpret_cast<uint32_t*>(o + n * 8) = Elem<T>::pack(pp[n][0] * 0.25f, pp[n][1] * 0.25f);
@@ -1056,6 +1059,9 @@ __global__ void __launch_bounds__(kL0Threads, 1) dec0_kernel(const __grid_consta
         [&](uint8_t* buf, int tile) {
             const L0Tile tl = l0_tile(tile, a.td);
             if (a.dbg & 2) return;
+            const int hw0 = a.H0 * a.W0;
+            const bool full_w = tl.tx0 + sx + 16 <= a.W0;
+            float* ybase = a.y + ((int64_t)tl.f * 4 + 2 * t) * hw0 + (int64_t)(tl.ty0 + r0) * a.W0 + tl.tx0 + sx + g;
             conv3_strip16<T, 8>(smem_u32(buf), E0_PLANE, E0_IC, r0, sx, B3, bias3, [&](int oo, float (&acc)[2][4]) {
                 uint32_t a1[4], a2[4];
                 relu_pack_a<T>(acc, a1);
@@ -1067,17 +1073,22 @@ __global__ void __launch_bounds__(kL0Threads, 1) dec0_kernel(const __grid_consta
                 relu_pack_a<T>(u, a2);
                 float yh[4];
                 mma16816_c<T>(yh, a2, BH[0], BH[1], biash[0], biash[1], biash[0], biash[1]);
-                const int oy = tl.ty0 + r0 + oo;
-                if (t < 2 && oy < a.H0) {
-                    const int64_t hw0 = (int64_t)a.H0 * a.W0;
-                    float* yp = a.y + ((int64_t)tl.f * 4 + 2 * t) * hw0 + (int64_t)oy * a.W0;
+                // head channels 2t, 2t+1 (t < 2) of pixels g, g+8: one 64-bit base
+                // per tile, 32-bit row offsets (planes and the +8 are immediates)
+                if (t < 2 && tl.ty0 + r0 + oo < a.H0) {
+                    float* yp = ybase + oo * a.W0;
+                    if (full_w) {
+                        yp[0] = yh[0];
+                        yp[8] = yh[2];
+                        yp[hw0] = yh[1];
+                        yp[hw0 + 8] = yh[3];
+                    } else {
 #pragma unroll
-                    for (int hlf = 0; hlf < 2; ++hlf) {
-                        const int ox = tl.tx0 + sx + g + 8 * hlf;
-                        if (ox < a.W0) {
-                            yp[ox] = yh[2 * hlf];
-                            yp[hw0 + ox] = yh[2 * hlf + 1];
-                        }
+                        for (int hlf = 0; hlf < 2; ++hlf)
+                            if (tl.tx0 + sx + g + 8 * hlf < a.W0) {
+                                yp[8 * hlf] = yh[2 * hlf];
+                                yp[hw0 + 8 * hlf] = yh[2 * hlf + 1];
+                            }
                     }
                 }
             });
