@@ -664,7 +664,7 @@ __device__ __forceinline__ void produce_features_tma(const Enc0Args& a, const Gb
             // a tile's first half: wait for the consumers to release the
             // buffer (after finishing the previous tile above), then park
             const int k = q >> 1;
-            if (k >= 2) mbar_wait(&freed[k & 1], ((k - 2) >> 1) & 1);
+            if (k >= 2) mbar_wait_backoff(&freed[k & 1], ((k - 2) >> 1) & 1);
             park(q, P);
         }
     };

@@ -141,6 +141,30 @@ __device__ __forceinline__ void mbar_init(uint64_t* bar, int count) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
 }
 
+// Non-blocking probe of an mbarrier phase.
+__device__ __forceinline__ bool mbar_test(uint64_t* bar, uint32_t phase) {
+    uint32_t ok;
+    asm volatile(
+        "{\n\t.reg .pred P1;\n\t"
+        "mbarrier.test_wait.parity.shared::cta.b64 P1, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, P1;\n\t}\n"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(phase)
+        : "memory");
+    return ok != 0;
+}
+
+// Wait for a phase that is usually far away (a warp that is ahead of its
+// consumer): exponential __nanosleep backoff, so the waiting warp does not
+// steal issue slots from the warps it waits for.
+__device__ __forceinline__ void mbar_wait_backoff(uint64_t* bar, uint32_t phase) {
+    uint32_t ns = 64;
+    while (!mbar_test(bar, phase)) {
+        __nanosleep(ns);
+        ns = ns < 1024 ? 2 * ns : 1024;
+    }
+}
+
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
