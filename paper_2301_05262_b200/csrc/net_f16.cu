@@ -1205,7 +1205,12 @@ struct LvGeom {
     static constexpr int PIN = NPI * 16;                       // dense: the TMA box layout
     static constexpr int INB = round128(NCI * PIN);
     static constexpr int PMID = plane_bytes(TH * TW, NC3);
-    static constexpr int MIDB = round128(NC3 * PMID);
+    // conv1's A operand (relu(conv3) packed to 16 bits) lives in TMEM when the
+    // columns allow (the accumulators of both convs are double-buffered):
+    // lane = pixel, 2 channels per column; otherwise in a chunk-planar SMEM tile
+    static constexpr int ACCM = 2 * NB * (C3 + C1), MIDC = NB * C3 / 2;
+    static constexpr bool MIDT = ACCM + NMID * MIDC <= 512;
+    static constexpr int MIDB = MIDT ? 0 : round128(NC3 * PMID);
     static constexpr int W3B = 9 * CIN * C3 * 2, W1B = C3 * C1 * 2;
     static constexpr int OFF_MID = NIN * INB;
     static constexpr int OFF_W3 = OFF_MID + NMID * MIDB;
@@ -1219,7 +1224,7 @@ struct LvGeom {
     static constexpr int OFF_BAR = (OFF_B + (C3 + C1) * 4 + 15) / 16 * 16;
     static constexpr int SMEM = OFF_BAR + 256;
     static constexpr int ACC3 = 0, ACC1 = 2 * NB * C3;         // TMEM columns (both double-buffered)
-    static constexpr int TCOLS = tmem_cols(2 * NB * (C3 + C1));
+    static constexpr int TCOLS = tmem_cols(ACCM + (MIDT ? NMID * MIDC : 0));
     static constexpr int TX_BYTES = NCI * PIN;
 };
 
@@ -1460,9 +1465,14 @@ __global__ void __launch_bounds__((NPW + 9) * 32, 1) level_kernel(const __grid_c
                 for (int b = 0; b < NB; ++b)
 #pragma unroll
                     for (int kk = 0; kk < C3 / 16; ++kk) {
-                        const uint64_t da = umma_desc(mid + (2 * kk) * G::PMID + (b * 8) * 16, G::PMID, G::TW * 16);
                         const uint64_t db = umma_desc(sbase + G::OFF_W1 + kk * C1 * 32, C1 * 16, 128);
-                        umma_f16(tmem + G::ACC1 + (a1 * NB + b) * C1, da, db, idesc1, kk ? 1u : 0u);
+                        if constexpr (G::MIDT) {
+                            umma_f16_ts(tmem + G::ACC1 + (a1 * NB + b) * C1,
+                                        tmem + G::ACCM + (m * NB + b) * G::MIDC / NB + kk * 8, db, idesc1, kk ? 1u : 0u);
+                        } else {
+                            const uint64_t da = umma_desc(mid + (2 * kk) * G::PMID + (b * 8) * 16, G::PMID, G::TW * 16);
+                            umma_f16(tmem + G::ACC1 + (a1 * NB + b) * C1, da, db, idesc1, kk ? 1u : 0u);
+                        }
                     }
                 umma_commit(&mid_empty[m]);
                 umma_commit(&a1_full[a1]);
@@ -1519,11 +1529,16 @@ __global__ void __launch_bounds__((NPW + 9) * 32, 1) level_kernel(const __grid_c
                     for (int e = 0; e < 8; ++e)
                         qp[e] = Elem<T>::pack(fmaxf(v[2 * e] + sb3[c0 + 2 * e], 0.f),
                                               fmaxf(v[2 * e + 1] + sb3[c0 + 2 * e + 1], 0.f));
-                    const int p = pi * G::TW + b * 8 + pj;
-                    *reinterpret_cast<uint4*>(mid + (c0 / 8) * G::PMID + p * 16) = qv[0];
-                    *reinterpret_cast<uint4*>(mid + (c0 / 8 + 1) * G::PMID + p * 16) = qv[1];
+                    if constexpr (G::MIDT) {
+                        tmem_st8(tmem + tl + G::ACCM + (mm * NB + b) * G::MIDC / NB + c0 / 2, qp);
+                    } else {
+                        const int p = pi * G::TW + b * 8 + pj;
+                        *reinterpret_cast<uint4*>(mid + (c0 / 8) * G::PMID + p * 16) = qv[0];
+                        *reinterpret_cast<uint4*>(mid + (c0 / 8 + 1) * G::PMID + p * 16) = qv[1];
+                    }
                 }
             }
+            if constexpr (G::MIDT) tmem_st_wait();
             fence_proxy_async();
             tc_fence_before();
             mbar_arrive(&a3_empty[a3]);
