@@ -1750,11 +1750,11 @@ nsm_status run_levels(const Plan& p, const Bufs& b, int nf, int H0, int W0, cuda
     if (s != NSM_OK) return s;
     // l3 bottleneck: P3 (64) -> 128 -> B3 (64)
     a = LevelArgs{b.p3, nullptr, H3, W3, L3.enc3.wpk, L3.enc3.b32, L3.enc1.wpk, L3.enc1.b32, b.b3, nullptr};
-    s = launch_level<T, 64, 128, 64, SRC_TENSOR, DST_STORE, 1, 1, 1>(a, nf, st, "lv3_bott");
+    s = launch_level<T, 64, 128, 64, SRC_TENSOR, DST_STORE, 1, 2, 2>(a, nf, st, "lv3_bott");
     if (s != NSM_OK) return s;
     // l2 decoder: up(B3) + S2 -> 64 -> D2 (32)
     a = LevelArgs{b.b3, b.s2, H2, W2, L2.dec3.wpk, L2.dec3.b32, L2.dec1.wpk, L2.dec1.b32, b.d2, nullptr};
-    s = launch_level<T, 64, 64, 32, SRC_UP, DST_STORE, 2, 1, 1>(a, nf, st, "lv2_dec");
+    s = launch_level<T, 64, 64, 32, SRC_UP, DST_STORE, 2, 2, 2>(a, nf, st, "lv2_dec");
     if (s != NSM_OK) return s;
     // l1 decoder: up(D2) + S1 -> 32 -> D1 (16)
     a = LevelArgs{b.d2, b.s1, H1, W1, L1.dec3.wpk, L1.dec3.b32, L1.dec1.wpk, L1.dec1.b32, b.d1, nullptr};
