@@ -1195,6 +1195,7 @@ struct LevelArgs {
     void* out;           // (N, H, W, C1)
     void* pool;          // (N, H/2, W/2, C1)
     int dbg;             // experiments only: 1 skip producer math, 2 skip epilogue math, 4 skip MMAs
+    long long* trace;    // experiments only (NSM_LEVEL_TRACE=<name>): CTA 0 per-tile clock64 events
 };
 
 template <int CIN, int C3, int C1, int NB, int NIN, int NMID, int STG>
@@ -1290,6 +1291,9 @@ __global__ void __launch_bounds__((NPW + 9) * 32, 1) level_kernel(const __grid_c
     const uint32_t sbase = smem_u32(smem);
     const int ntx = (a.W + G::TW - 1) / G::TW, nty = (a.H + G::TH - 1) / G::TH;
     const int mytiles = (int)blockIdx.x < total ? (total - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x : 0;
+    auto tr = [&](int k, int ev) {     // experiments: CTA 0's per-tile timeline
+        if (a.trace && blockIdx.x == 0 && k < 32) a.trace[k * 8 + ev] = clock64();
+    };
     auto tile_of = [&](int k, int& f, int& y0, int& x0) {
         const int t = blockIdx.x + k * gridDim.x;
         x0 = (t % ntx) * G::TW;
@@ -1389,6 +1393,7 @@ __global__ void __launch_bounds__((NPW + 9) * 32, 1) level_kernel(const __grid_c
                 const uint8_t* lo = smem + G::OFF_LO + (k & 1) * G::LOB;
                 mbar_wait(&in_empty[s], ((k / NIN) & 1) ^ 1);
                 mbar_wait(&lof[k & 1], (k >> 1) & 1);
+                if (tid == 0) tr(k, 0);
                 uint8_t* in = smem + s * G::INB;
 #pragma unroll 1
                 for (int h = 0; h < NH; ++h) {
@@ -1441,6 +1446,7 @@ __global__ void __launch_bounds__((NPW + 9) * 32, 1) level_kernel(const __grid_c
                     if (h == NH - 1) {
                         fence_proxy_async();
                         mbar_arrive(&in_full[s]);
+                        if (tid == 0) tr(k, 1);
                     }
                     nbar_sync(1, NPT);             // all producers done with skip piece h (and, last, the low tile)
                     if (tid == 0) {
@@ -1460,22 +1466,24 @@ __global__ void __launch_bounds__((NPW + 9) * 32, 1) level_kernel(const __grid_c
                 mbar_wait(&mid_full[m], (j / NMID) & 1);
                 mbar_wait(&a1_empty[a1], ((j >> 1) & 1) ^ 1);
                 tc_fence_after();
-                const uint32_t mid = sbase + G::OFF_MID + m * G::MIDB;
+                const uint64_t db0 = umma_desc(sbase + G::OFF_W1, C1 * 16, 128);
+                const uint64_t dm0 = umma_desc(sbase + G::OFF_MID + m * G::MIDB, G::PMID, G::TW * 16);
 #pragma unroll
                 for (int b = 0; b < NB; ++b)
 #pragma unroll
                     for (int kk = 0; kk < C3 / 16; ++kk) {
-                        const uint64_t db = umma_desc(sbase + G::OFF_W1 + kk * C1 * 32, C1 * 16, 128);
+                        const uint64_t db = db0 + (uint64_t)((kk * C1 * 32) >> 4);
                         if constexpr (G::MIDT) {
                             umma_f16_ts(tmem + G::ACC1 + (a1 * NB + b) * C1,
                                         tmem + G::ACCM + (m * NB + b) * G::MIDC / NB + kk * 8, db, idesc1, kk ? 1u : 0u);
                         } else {
-                            const uint64_t da = umma_desc(mid + (2 * kk) * G::PMID + (b * 8) * 16, G::PMID, G::TW * 16);
+                            const uint64_t da = dm0 + (uint64_t)(((2 * kk) * G::PMID + (b * 8) * 16) >> 4);
                             umma_f16(tmem + G::ACC1 + (a1 * NB + b) * C1, da, db, idesc1, kk ? 1u : 0u);
                         }
                     }
                 umma_commit(&mid_empty[m]);
                 umma_commit(&a1_full[a1]);
+                tr(j, 3);
             };
             mbar_wait(wbar, 0);
             for (int k = 0; k < mytiles; ++k) {
@@ -1483,20 +1491,30 @@ __global__ void __launch_bounds__((NPW + 9) * 32, 1) level_kernel(const __grid_c
                 mbar_wait(&in_full[s], (k / NIN) & 1);
                 mbar_wait(&a3_empty[a3], ((k >> 1) & 1) ^ 1);
                 tc_fence_after();
-                const uint32_t in = sbase + s * G::INB;
+                tr(k, 2);
+                // Descriptors: one base per operand, every tap / block / K-step a
+                // compile-time offset in 16-B units added to the start-address
+                // field (building each descriptor in the loop costs ~70 issue
+                // cycles per UMMA: the single MMA thread, not the tensor core,
+                // was the limit; tools/umma_layout_probe.cu)
+                const uint64_t da0 = umma_desc(sbase + s * G::INB, G::PIN, G::IC * 16);
+                const uint64_t db0 = umma_desc(sbase + G::OFF_W3, C3 * 16, 128);
+                if (!(a.dbg & 4)) {
 #pragma unroll 1
-                for (int tap = 0; tap < ((a.dbg & 4) ? 0 : 9); ++tap) {
-                    const int dy = tap / 3, dx = tap % 3;
+                    for (int tap = 0; tap < 9; ++tap) {
+                        const int dy = tap / 3, dx = tap - 3 * dy;
+                        const uint64_t dat = da0 + (uint64_t)(dy * G::IC + dx);            // 16-B units
+                        const uint64_t dbt = db0 + (uint64_t)(tap * G::KK * C3 * 2);
 #pragma unroll
-                    for (int b = 0; b < NB; ++b)
+                        for (int b = 0; b < NB; ++b)
 #pragma unroll
-                        for (int kk = 0; kk < G::KK; ++kk) {
-                            // M-block b: 16 output rows x 8 px; core matrix i = output row i
-                            const uint64_t da = umma_desc(in + (2 * kk) * G::PIN + (dy * G::IC + b * 8 + dx) * 16,
-                                                          G::PIN, G::IC * 16);
-                            const uint64_t db = umma_desc(sbase + G::OFF_W3 + (tap * G::KK + kk) * C3 * 32, C3 * 16, 128);
-                            umma_f16(tmem + G::ACC3 + (a3 * NB + b) * C3, da, db, idesc3, (tap | kk) ? 1u : 0u);
-                        }
+                            for (int kk = 0; kk < G::KK; ++kk) {
+                                // M-block b: 16 output rows x 8 px; core matrix i = output row i
+                                const uint64_t da = dat + (uint64_t)(((2 * kk) * G::PIN + b * 8 * 16) >> 4);
+                                const uint64_t db = dbt + (uint64_t)((kk * C3 * 32) >> 4);
+                                umma_f16(tmem + G::ACC3 + (a3 * NB + b) * C3, da, db, idesc3, (tap | kk) ? 1u : 0u);
+                            }
+                    }
                 }
                 umma_commit(&in_empty[s]);
                 umma_commit(&a3_full[a3]);
@@ -1516,6 +1534,7 @@ __global__ void __launch_bounds__((NPW + 9) * 32, 1) level_kernel(const __grid_c
             mbar_wait(&a3_full[a3], (k >> 1) & 1);
             mbar_wait(&mid_empty[mm], ((k / NMID) & 1) ^ 1);
             tc_fence_after();
+            if (warp == EW0 && lane == 0) tr(k, 4);
             uint8_t* mid = smem + G::OFF_MID + mm * G::MIDB;
 #pragma unroll 1
             for (int it = grp; it < ((a.dbg & 2) ? 0 : NB * (C3 / 16)); it += 2) {
@@ -1543,6 +1562,7 @@ __global__ void __launch_bounds__((NPW + 9) * 32, 1) level_kernel(const __grid_c
             tc_fence_before();
             mbar_arrive(&a3_empty[a3]);
             mbar_arrive(&mid_full[mm]);
+            if (warp == EW0 && lane == 0) tr(k, 5);
         };
         auto epi2 = [&](int j) {
             const int a1 = j & 1;
@@ -1550,6 +1570,7 @@ __global__ void __launch_bounds__((NPW + 9) * 32, 1) level_kernel(const __grid_c
             tile_of(j, f, y0, x0);
             mbar_wait(&a1_full[a1], (j >> 1) & 1);
             tc_fence_after();
+            if (warp == EW0 && lane == 0) tr(j, 6);
             const int oy = y0 + pi;
 #pragma unroll 1
             for (int it = grp; it < ((a.dbg & 2) ? 0 : NB * (C1 / 16)); it += 2) {
@@ -1605,6 +1626,7 @@ __global__ void __launch_bounds__((NPW + 9) * 32, 1) level_kernel(const __grid_c
             }
             tc_fence_before();
             mbar_arrive(&a1_empty[a1]);
+            if (warp == EW0 && lane == 0) tr(j, 7);
         };
         for (int k = 0; k < mytiles; ++k) {
             epi1(k);
@@ -1700,8 +1722,30 @@ nsm_status launch_level(const LevelArgs& a, int nf, cudaStream_t st, const char*
     const int grid = std::min(total, num_sms());      // TMEM: 512 columns -> one CTA per SM
     static const int dbg = getenv("NSM_LEVEL_DBG") ? atoi(getenv("NSM_LEVEL_DBG")) : 0;
     const_cast<LevelArgs&>(a).dbg = dbg;
+    static const char* trace_name = getenv("NSM_LEVEL_TRACE");
+    static long long* trace_buf = nullptr;
+    const bool trace = trace_name && !strcmp(trace_name, name);
+    if (trace) {
+        if (!trace_buf) cudaMalloc(&trace_buf, 32 * 8 * sizeof(long long));
+        cudaMemsetAsync(trace_buf, 0, 32 * 8 * sizeof(long long), st);
+    }
+    const_cast<LevelArgs&>(a).trace = trace ? trace_buf : nullptr;
     NSM_PROF(name, st);
     launch_pdl(k, dim3(grid), dim3((NPW + 9) * 32), G::SMEM, st, a, tin, tlo, total);
+    if (trace) {   // experiments only: print CTA 0's timeline (us at 1.965 GHz) and stall the stream
+        long long h[32 * 8];
+        cudaMemcpyAsync(h, trace_buf, sizeof h, cudaMemcpyDeviceToHost, st);
+        cudaStreamSynchronize(st);
+        long long t0 = 0;
+        for (long long v : h) if (v && (!t0 || v < t0)) t0 = v;
+        fprintf(stderr, "%s CTA0 (us): tile prod_start prod_done mma3_issue mma1_issued epi1_start epi1_end epi2_start epi2_end\n", name);
+        for (int k = 0; k < 32; ++k) {
+            if (!h[k * 8 + 2]) break;
+            fprintf(stderr, "%2d", k);
+            for (int e = 0; e < 8; ++e) fprintf(stderr, " %7.2f", h[k * 8 + e] ? (h[k * 8 + e] - t0) / 1965.0 : -1.0);
+            fprintf(stderr, "\n");
+        }
+    }
     return NSM_OK;
 }
 
