@@ -1220,7 +1220,12 @@ struct LvGeom {
     static constexpr int LR = TH / 2 + 2, LC = TW / 2 + 2;
     static constexpr int SKB = STG ? IR * IC * CIN * 2 : 0, LOB = STG ? LR * LC * CIN * 2 : 0;
     static constexpr int OFF_SK = round128(OFF_W1 + W1B);
-    static constexpr int OFF_LO = round128(OFF_SK + SKB);
+    // the skip tile is double-buffered (staged two tiles ahead, with the
+    // low-res tile) when shared memory allows, else streamed in row halves
+    static constexpr int TAIL = round128(2 * LOB) + (C3 + C1) * 4 + 16 + 256;
+    static constexpr int NSK = (STG && OFF_SK + 2 * round128(SKB) + TAIL <= 232448) ? 2 : 1;
+    static constexpr int SKBR = round128(SKB);
+    static constexpr int OFF_LO = round128(OFF_SK + NSK * SKBR);
     static constexpr int OFF_B = round128(OFF_LO + 2 * LOB);   // low-res staging double-buffered
     static constexpr int OFF_BAR = (OFF_B + (C3 + C1) * 4 + 15) / 16 * 16;
     static constexpr int SMEM = OFF_BAR + 256;
@@ -1358,10 +1363,10 @@ __global__ void __launch_bounds__((NPW + 9) * 32, 1) level_kernel(const __grid_c
             // producers finish rows 0-8 of tile k, the low tile of k+2 when
             // tile k is done.
             const int hl = a.H / 2, wl = a.W / 2;
-            const uint8_t* sk = smem + G::OFF_SK;
             // (NIN = 1: the input buffer is single, the producers wait for the
             // MMA anyway, so the skip tile is one piece issued per tile)
-            constexpr int NH = NIN == 2 ? 2 : 1;                // skip pieces per tile
+            constexpr bool kSk2 = G::NSK == 2;                  // skip double-buffered with the low tile
+            constexpr int NH = kSk2 ? 1 : (NIN == 2 ? 2 : 1);   // skip pieces per tile
             constexpr int HR = G::IR / NH;                      // rows per skip piece
             constexpr int SKH = HR * G::IC * CIN * 2;           // bytes per skip piece
             static_assert(G::IR % NH == 0, "skip halves");
@@ -1374,13 +1379,16 @@ __global__ void __launch_bounds__((NPW + 9) * 32, 1) level_kernel(const __grid_c
             auto stage_lo = [&](int k) {                        // thread 0 only
                 int f, y0, x0;
                 tile_of(k, f, y0, x0);
-                mbar_expect_tx(&lof[k & 1], G::LOB);
+                const bool sk2 = kSk2 && a.skip;
+                mbar_expect_tx(&lof[k & 1], G::LOB + (sk2 ? G::SKB : 0));
                 tma_load_4d(sbase + G::OFF_LO + (k & 1) * G::LOB, &tlo, 0, x0 / 2 - 1, y0 / 2 - 1, f, &lof[k & 1]);
+                if (sk2) tma_load_4d(sbase + G::OFF_SK + (k & 1) * G::SKBR, &tin, 0, x0 - 1, y0 - 1, f, &lof[k & 1]);
             };
             if (tid == 0) {
                 if (mytiles > 0) {
-                    for (int h = 0; h < NH; ++h)
-                        if (a.skip) stage_skip(0, h);
+                    if (!kSk2)
+                        for (int h = 0; h < NH; ++h)
+                            if (a.skip) stage_skip(0, h);
                     stage_lo(0);
                 }
                 if (mytiles > 1) stage_lo(1);
@@ -1391,13 +1399,14 @@ __global__ void __launch_bounds__((NPW + 9) * 32, 1) level_kernel(const __grid_c
                 tile_of(k, f, y0, x0);
                 const int ly0 = y0 / 2 - 1, lx0 = x0 / 2 - 1;
                 const uint8_t* lo = smem + G::OFF_LO + (k & 1) * G::LOB;
+                const uint8_t* sk = smem + G::OFF_SK + (kSk2 ? (k & 1) * G::SKBR : 0);
                 mbar_wait(&in_empty[s], ((k / NIN) & 1) ^ 1);
                 mbar_wait(&lof[k & 1], (k >> 1) & 1);
                 if (tid == 0) tr(k, 0);
                 uint8_t* in = smem + s * G::INB;
 #pragma unroll 1
                 for (int h = 0; h < NH; ++h) {
-                    if (a.skip) mbar_wait(&skf[h], k & 1);
+                    if (a.skip && !kSk2) mbar_wait(&skf[h], k & 1);
                     // one item = one 2x2 block of outputs (the children of low-res
                     // pixel (bi, bj)) x one 8-channel chunk: the block reads its 3x3
                     // low-res neighbourhood once with the fixed (1/4, 3/4) weights
@@ -1450,7 +1459,7 @@ __global__ void __launch_bounds__((NPW + 9) * 32, 1) level_kernel(const __grid_c
                     }
                     nbar_sync(1, NPT);             // all producers done with skip piece h (and, last, the low tile)
                     if (tid == 0) {
-                        if (a.skip && k + 1 < mytiles) stage_skip(k + 1, h);
+                        if (a.skip && !kSk2 && k + 1 < mytiles) stage_skip(k + 1, h);
                         if (h == NH - 1 && k + 2 < mytiles) stage_lo(k + 2);
                     }
                 }
@@ -1715,7 +1724,9 @@ nsm_status launch_level(const LevelArgs& a, int nf, cudaStream_t st, const char*
         ok = encode_nhwc_map(a.x, bf, CIN, a.H, a.W, nf, G::IC, G::IR, &tin);
     } else {
         ok = encode_nhwc_map4(a.x, bf, CIN, a.H / 2, a.W / 2, nf, G::LC, G::LR, &tlo);
-        if (a.skip) ok = ok && encode_nhwc_map4(a.skip, bf, CIN, a.H, a.W, nf, G::IC, NIN == 2 ? G::IR / 2 : G::IR, &tin);
+        if (a.skip)
+            ok = ok && encode_nhwc_map4(a.skip, bf, CIN, a.H, a.W, nf, G::IC,
+                                        (G::NSK == 1 && NIN == 2) ? G::IR / 2 : G::IR, &tin);
     }
     if (!ok) return fail(NSM_ERR_CUDA, "%s: TMA tensor map encoding failed", name);
     const int total = ((a.W + G::TW - 1) / G::TW) * ((a.H + G::TH - 1) / G::TH) * nf;
