@@ -1545,12 +1545,31 @@ __global__ void __launch_bounds__((NPW + 9) * 32, 1) level_kernel(const __grid_c
             tc_fence_after();
             if (warp == EW0 && lane == 0) tr(k, 4);
             uint8_t* mid = smem + G::OFF_MID + mm * G::MIDB;
-#pragma unroll 1
-            for (int it = grp; it < ((a.dbg & 2) ? 0 : NB * (C3 / 16)); it += 2) {
-                const int b = it / (C3 / 16), c0 = (it % (C3 / 16)) * 16;
+            // this warp's NB * C3 / 32 accumulator slices: all TMEM loads in
+            // flight before one wait (a wait per load serialised the epilogue)
+            constexpr int NIT1 = NB * (C3 / 16) / 2;
+            constexpr bool kPre = SRC == SRC_TENSOR;     // register room (no producer warps)
+            uint32_t r1[kPre ? NIT1 : 1][16];
+            if (kPre && !(a.dbg & 2)) {
+#pragma unroll
+                for (int i = 0; i < NIT1; ++i) {
+                    const int it = grp + 2 * i, b = it / (C3 / 16), c0 = (it % (C3 / 16)) * 16;
+                    tmem_ld16_nw(tmem + tl + G::ACC3 + (a3 * NB + b) * C3 + c0, r1[i]);
+                }
+                tmem_ld_wait();
+            }
+#pragma unroll
+            for (int i = 0; i < NIT1; ++i) {
+                if (a.dbg & 2) break;
+                const int it = grp + 2 * i, b = it / (C3 / 16), c0 = (it % (C3 / 16)) * 16;
                 {
                     float v[16];
-                    tmem_ld16(tmem + tl + G::ACC3 + (a3 * NB + b) * C3 + c0, v);
+                    if constexpr (!kPre) {
+                        tmem_ld16_nw(tmem + tl + G::ACC3 + (a3 * NB + b) * C3 + c0, r1[0]);
+                        tmem_ld_wait();
+                    }
+#pragma unroll
+                    for (int e = 0; e < 16; ++e) v[e] = __uint_as_float(r1[kPre ? i : 0][e]);
                     uint4 qv[2];
                     uint32_t* qp = &qv[0].x;
 #pragma unroll
@@ -1581,14 +1600,31 @@ __global__ void __launch_bounds__((NPW + 9) * 32, 1) level_kernel(const __grid_c
             tc_fence_after();
             if (warp == EW0 && lane == 0) tr(j, 6);
             const int oy = y0 + pi;
-#pragma unroll 1
-            for (int it = grp; it < ((a.dbg & 2) ? 0 : NB * (C1 / 16)); it += 2) {
-                const int b = it / (C1 / 16), c0 = (it % (C1 / 16)) * 16;
+            constexpr int NIT2 = NB * (C1 / 16) / 2;
+            constexpr bool kPre = SRC == SRC_TENSOR;
+            uint32_t r2[kPre ? NIT2 : 1][16];
+            if (kPre && !(a.dbg & 2)) {
+#pragma unroll
+                for (int i = 0; i < NIT2; ++i) {
+                    const int it = grp + 2 * i, b = it / (C1 / 16), c0 = (it % (C1 / 16)) * 16;
+                    tmem_ld16_nw(tmem + tl + G::ACC1 + (a1 * NB + b) * C1 + c0, r2[i]);
+                }
+                tmem_ld_wait();
+            }
+#pragma unroll
+            for (int i = 0; i < NIT2; ++i) {
+                if (a.dbg & 2) break;
+                const int it = grp + 2 * i, b = it / (C1 / 16), c0 = (it % (C1 / 16)) * 16;
                 const int ox = x0 + b * 8 + pj;
                 const bool inside = oy < a.H && ox < a.W;
                 {
                     float v[16];
-                    tmem_ld16(tmem + tl + G::ACC1 + (a1 * NB + b) * C1 + c0, v);
+                    if constexpr (!kPre) {
+                        tmem_ld16_nw(tmem + tl + G::ACC1 + (a1 * NB + b) * C1 + c0, r2[0]);
+                        tmem_ld_wait();
+                    }
+#pragma unroll
+                    for (int e = 0; e < 16; ++e) v[e] = __uint_as_float(r2[kPre ? i : 0][e]);
 #pragma unroll
                     for (int e = 0; e < 16; ++e) v[e] = fmaxf(v[e] + sb1[c0 + e], 0.f);
                     if (DST & DST_STORE) {
