@@ -114,13 +114,14 @@ uint16_t to_bits(float v) {
 }
 
 template <typename T>
-void pack_frag(const float* w, int cout, int cin, int k, bool s2d_perm, std::vector<uint32_t>& out) {
+void pack_frag(const float* w, int cout, int cin, int k, bool s2d_perm, std::vector<uint32_t>& out,
+               float scale = 1.f) {
     const int taps = k * k, KK = (cin + 15) / 16, NT = (cout + 7) / 8;
     out.assign(frag_words(taps, cin, cout), 0u);
     auto B = [&](int tap, int kk, int n) -> float {
         if (n >= cout || kk >= cin) return 0.f;
         const int ci = s2d_perm ? perm_s2d(kk, cin) : kk;
-        return w[((size_t)n * cin + ci) * taps + tap];
+        return scale * w[((size_t)n * cin + ci) * taps + tap];
     };
     for (int tap = 0; tap < taps; ++tap)
         for (int kk = 0; kk < KK; ++kk)
@@ -741,7 +742,7 @@ __global__ void __launch_bounds__(kSrc == 2 ? kE0Threads : kL0Threads, 1) enc0_k
 #pragma unroll
             for (int e = 0; e < 2; ++e) {
                 bias3[n][e] = __ldg(a.b3 + n * 8 + 2 * t + e);
-                bias1[n][e] = __ldg(a.b1 + n * 8 + 2 * t + e);
+                bias1[n][e] = 0.25f * __ldg(a.b1 + n * 8 + 2 * t + e);   // pool scale folded (see pack_f16)
             }
     }
     T* out = reinterpret_cast<T*>(a.out);
@@ -780,7 +781,7 @@ __global__ void __launch_bounds__(kSrc == 2 ? kE0Threads : kL0Threads, 1) enc0_k
                         T* o = obase + (oo >> 1) * W1 * 16;
 #pragma unroll
                         for (int n = 0; n < 2; ++n)
-                            *reinterpret_cast<uint32_t*>(o + n * 8) = Elem<T>::pack(pp[n][0] * 0.25f, pp[n][1] * 0.25f);
+                            *reinterpret_cast<uint32_t*>(o + n * 8) = Elem<T>::pack(pp[n][0], pp[n][1]);
                     }
                 }
             }, hook);
@@ -1960,10 +1961,10 @@ nsm_status pack_f16(Plan& p, std::vector<char>& blob, size_t& offset_out) {
         std::vector<char> bytes;
     };
     std::vector<Item> items;
-    auto frag = [&](ConvW& c, bool perm) {
+    auto frag = [&](ConvW& c, bool perm, float scale = 1.f) {
         std::vector<uint32_t> v;
-        if (bf) pack_frag<__nv_bfloat16>(c.w32, c.cout, c.cin, c.k, perm, v);
-        else pack_frag<__half>(c.w32, c.cout, c.cin, c.k, perm, v);
+        if (bf) pack_frag<__nv_bfloat16>(c.w32, c.cout, c.cin, c.k, perm, v, scale);
+        else pack_frag<__half>(c.w32, c.cout, c.cin, c.k, perm, v, scale);
         Item it{&c, std::vector<char>((char*)v.data(), (char*)v.data() + v.size() * 4)};
         items.push_back(std::move(it));
     };
@@ -1975,7 +1976,10 @@ nsm_status pack_f16(Plan& p, std::vector<char>& blob, size_t& offset_out) {
         items.push_back(std::move(it));
     };
     frag(p.lev[0].enc3, true);
-    frag(p.lev[0].enc1, false);
+    // l0.enc1 feeds only enc0's 2x2 average pool: relu(0.25 x) = 0.25 relu(x),
+    // so the 1/4 is folded into the weights (exact: a power of two) and the
+    // bias (enc0 loads it scaled) and the pool is a plain sum
+    frag(p.lev[0].enc1, false, 0.25f);
     frag(p.lev[0].dec3, false);
     frag(p.lev[0].dec1, false);
     frag(p.head, false);
