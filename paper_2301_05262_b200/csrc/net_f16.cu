@@ -1202,8 +1202,22 @@ struct LevelArgs {
 template <int CIN, int C3, int C1, int NB, int NIN, int NMID, int STG>
 struct LvGeom {
     static constexpr int TH = 16, TW = 8 * NB;
-    static constexpr int IR = TH + 2, IC = TW + 2, NPI = IR * IC;
+    static constexpr int IR = TH + 2, IC = TW + 2;
     static constexpr int NCI = CIN / 8, NC3 = C3 / 8, KK = CIN / 16;
+    // SRC_UP (STG): the low-res tile is always staged (double-buffered).  The
+    // skip tile is staged pixel-major and double-buffered when shared memory
+    // allows (STAGED), else TMA'd straight into the input buffer, whose box is
+    // then padded by a row and a column so that the chunk-plane stride is an
+    // odd multiple of 16 B (the producers' per-chunk accesses hit all banks)
+    static constexpr int LR = TH / 2 + 2, LC = TW / 2 + 2;
+    static constexpr int LOB = STG ? LR * LC * CIN * 2 : 0, SKB = STG ? IR * IC * CIN * 2 : 0;
+    static constexpr int MIDC_ = NB * C3 / 2, ACCM_ = 2 * NB * (C3 + C1);
+    static constexpr bool MIDT_ = ACCM_ + NMID * MIDC_ <= 512;
+    static constexpr int FIXED = NIN * round128(NCI * IR * IC * 16) + (MIDT_ ? 0 : NMID * round128(NC3 * plane_bytes(TH * TW, NC3))) +
+                                 9 * CIN * C3 * 2 + C3 * C1 * 2 + 128 + round128(2 * LOB) + (C3 + C1) * 4 + 16 + 256;
+    static constexpr bool STAGED = STG && FIXED + 2 * round128(SKB) <= 232448;
+    static constexpr int PADIN = (STG && !STAGED) ? 1 : 0;
+    static constexpr int ICB = IC + PADIN, IRB = IR + PADIN, NPI = IRB * ICB;
     static constexpr int PIN = NPI * 16;                       // dense: the TMA box layout
     static constexpr int INB = round128(NCI * PIN);
     static constexpr int PMID = plane_bytes(TH * TW, NC3);
@@ -1217,16 +1231,9 @@ struct LvGeom {
     static constexpr int OFF_MID = NIN * INB;
     static constexpr int OFF_W3 = OFF_MID + NMID * MIDB;
     static constexpr int OFF_W1 = OFF_W3 + W3B;
-    // SRC_UP staging (STG): skip tile (halo'd, pixel-major) and low-res tile
-    static constexpr int LR = TH / 2 + 2, LC = TW / 2 + 2;
-    static constexpr int SKB = STG ? IR * IC * CIN * 2 : 0, LOB = STG ? LR * LC * CIN * 2 : 0;
-    static constexpr int OFF_SK = round128(OFF_W1 + W1B);
-    // the skip tile is double-buffered (staged two tiles ahead, with the
-    // low-res tile) when shared memory allows, else streamed in row halves
-    static constexpr int TAIL = round128(2 * LOB) + (C3 + C1) * 4 + 16 + 256;
-    static constexpr int NSK = (STG && OFF_SK + 2 * round128(SKB) + TAIL <= 232448) ? 2 : 1;
     static constexpr int SKBR = round128(SKB);
-    static constexpr int OFF_LO = round128(OFF_SK + NSK * SKBR);
+    static constexpr int OFF_SK = round128(OFF_W1 + W1B);
+    static constexpr int OFF_LO = round128(OFF_SK + (STAGED ? 2 * SKBR : 0));
     static constexpr int OFF_B = round128(OFF_LO + 2 * LOB);   // low-res staging double-buffered
     static constexpr int OFF_BAR = (OFF_B + (C3 + C1) * 4 + 15) / 16 * 16;
     static constexpr int SMEM = OFF_BAR + 256;
@@ -1269,7 +1276,7 @@ __device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t
 // All hand-offs are mbarriers (tcgen05.commit on the tensor-core side), so
 // conv3 of tile k+1 overlaps the epilogues of tile k.
 template <typename T, int CIN, int C3, int C1, int SRC, int DST, int NB, int NIN, int NMID, int NPW>
-__global__ void __launch_bounds__((NPW + 9) * 32, 1) level_kernel(const __grid_constant__ LevelArgs a,
+__global__ void __launch_bounds__((NPW + 9 + (SRC == SRC_UP)) * 32, 1) level_kernel(const __grid_constant__ LevelArgs a,
                                                                    const __grid_constant__ CUtensorMap tin,
                                                                    const __grid_constant__ CUtensorMap tlo,
                                                                    int total) {
@@ -1286,9 +1293,10 @@ __global__ void __launch_bounds__((NPW + 9) * 32, 1) level_kernel(const __grid_c
     uint64_t* a1_full = bar + 16;
     uint64_t* a1_empty = bar + 18;
     uint64_t* wbar = bar + 20;        // weights landed
-    uint64_t* skf = bar + 21;         // SRC_UP: skip rows 0-8 / 9-17 of the tile landed [2]
+    uint64_t* skf = bar + 21;         // SRC_UP: skip tile landed in in[s] [NIN <= 2]
     uint64_t* lof = bar + 23;         // SRC_UP: low-res tile landed, double-buffered [2]
-    uint32_t* tptr = reinterpret_cast<uint32_t*>(smem + G::OFF_BAR + 208);
+    uint64_t* lo_empty = bar + 25;    // SRC_UP: producers done with low-res buffer [2]
+    uint32_t* tptr = reinterpret_cast<uint32_t*>(smem + G::OFF_BAR + 224);
     float* sb3 = reinterpret_cast<float*>(smem + G::OFF_B);
     float* sb1 = sb3 + C3;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -1326,6 +1334,7 @@ __global__ void __launch_bounds__((NPW + 9) * 32, 1) level_kernel(const __grid_c
         for (int i = 0; i < 2; ++i) {
             mbar_init(&skf[i], 1);
             mbar_init(&lof[i], 1);
+            mbar_init(&lo_empty[i], NPW);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         // resident weights: two async bulk copies, waited on by the MMA warp only
@@ -1355,7 +1364,7 @@ __global__ void __launch_bounds__((NPW + 9) * 32, 1) level_kernel(const __grid_c
                     tma_load_5d(sbase + s * G::INB, &tin, 0, x0 - 1, y0 - 1, 0, f, &in_full[s]);
                 }
             }
-        } else {
+        } else if constexpr (G::STAGED) {
             // up2(low) + skip from TMA-staged pixel-major tiles (skip: the halo'd
             // tile; low: (TH/2+2) x (TW/2+2) source pixels, edge-clamped indices).
             // The skip tile streams in two row halves and the low-res tile is
@@ -1366,7 +1375,7 @@ __global__ void __launch_bounds__((NPW + 9) * 32, 1) level_kernel(const __grid_c
             const int hl = a.H / 2, wl = a.W / 2;
             // (NIN = 1: the input buffer is single, the producers wait for the
             // MMA anyway, so the skip tile is one piece issued per tile)
-            constexpr bool kSk2 = G::NSK == 2;                  // skip double-buffered with the low tile
+            constexpr bool kSk2 = true;                         // skip double-buffered with the low tile
             constexpr int NH = kSk2 ? 1 : (NIN == 2 ? 2 : 1);   // skip pieces per tile
             constexpr int HR = G::IR / NH;                      // rows per skip piece
             constexpr int SKH = HR * G::IC * CIN * 2;           // bytes per skip piece
@@ -1465,6 +1474,87 @@ __global__ void __launch_bounds__((NPW + 9) * 32, 1) level_kernel(const __grid_c
                     }
                 }
             }
+        } else {
+            // up2(low) + skip.  The TMA warp lands the skip tile straight into
+            // the input buffer in[s] (chunk-planar, zero halo outside the
+            // frame) and the low-res tile ((TH/2+2) x (TW/2+2) source pixels,
+            // pixel-major) into one of two staging buffers, a tile ahead; the
+            // producers add up2(low) in place.  Per-warp arrivals (lo_empty)
+            // release the staging buffers, so no producer waits for a peer.
+            const int hl = a.H / 2, wl = a.W / 2;
+            for (int k = 0; k < mytiles; ++k) {
+                const int s = k % NIN;
+                int f, y0, x0;
+                tile_of(k, f, y0, x0);
+                const int ly0 = y0 / 2 - 1, lx0 = x0 / 2 - 1;
+                const uint8_t* lo = smem + G::OFF_LO + (k & 1) * G::LOB;
+                if (a.skip) mbar_wait(&skf[s], (k / NIN) & 1);             // skip landed in in[s] (in[s] free)
+                else mbar_wait(&in_empty[s], ((k / NIN) & 1) ^ 1);
+                mbar_wait(&lof[k & 1], (k >> 1) & 1);
+                if (tid == 0) tr(k, 0);
+                uint8_t* in = smem + s * G::INB;
+                {
+                    // one item = one 2x2 block of outputs (the children of low-res
+                    // pixel (bi, bj)) x one 8-channel chunk: the block reads its 3x3
+                    // low-res neighbourhood once with the fixed (1/4, 3/4) weights
+                    // (autodiff.py:258-287); clamping the source indices reproduces
+                    // the reference's edge clamp.
+                    constexpr int BR = G::IR / 2 + 1, BC = G::IC / 2 + 1;
+                    constexpr int NITEM = BR * BC * G::NCI;
+                    for (int it = tid; it < ((a.dbg & 1) ? 0 : NITEM); it += NPT) {
+                        const int c = it % G::NCI, blk = it / G::NCI;
+                        const int bil = blk / BC, bjl = blk - bil * BC;
+                        const int bi = ly0 + bil, bj = lx0 + bjl;      // low-res pixel of the block
+                        int rs[3], cs[3];
+#pragma unroll
+                        for (int u = 0; u < 3; ++u) {
+                            rs[u] = min(max(min(max(bi - 1 + u, 0), hl - 1) - ly0, 0), G::LR - 1);
+                            cs[u] = min(max(min(max(bj - 1 + u, 0), wl - 1) - lx0, 0), G::LC - 1);
+                        }
+                        uint4 qn[3][3], ob[4];
+#pragma unroll
+                        for (int u = 0; u < 3; ++u)
+#pragma unroll
+                            for (int v = 0; v < 3; ++v)
+                                qn[u][v] = *reinterpret_cast<const uint4*>(lo + ((rs[v] * G::LC + cs[u]) * CIN + c * 8) * 2);
+                        up2_block<T>(qn, ob);
+#pragma unroll
+                        for (int ab = 0; ab < 4; ++ab) {
+                            const int aa = ab >> 1, bb = ab & 1;
+                            const int yy = 2 * bi + aa, xx = 2 * bj + bb;       // output pixel
+                            const int ti = yy - (y0 - 1), tj = xx - (x0 - 1);
+                            if (ti < 0 || ti >= G::IR || tj < 0 || tj >= G::IC) continue;
+                            uint4* dst = reinterpret_cast<uint4*>(in + c * G::PIN + (ti * G::ICB + tj) * 16);
+                            uint4 q = make_uint4(0u, 0u, 0u, 0u);
+                            if (yy >= 0 && xx >= 0 && yy < a.H && xx < a.W)
+                                q = a.skip ? add_packed<T>(ob[ab], *dst) : ob[ab];   // up2(low) + skip (network.py:189-194)
+                            *dst = q;
+                        }
+                    }
+                }
+                fence_proxy_async();
+                mbar_arrive(&in_full[s]);
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&lo_empty[k & 1]);              // this warp is done with low tile k
+                if (tid == 0) tr(k, 1);
+            }
+        }
+    } else if (SRC == SRC_UP && warp == MW + 1) {
+        // ------------------------------------------------------------ TMA warp (SRC_UP, in-place skip)
+        if (!G::STAGED && lane == 0) {
+            for (int k = 0; k < mytiles; ++k) {
+                const int s = k % NIN;
+                int f, y0, x0;
+                tile_of(k, f, y0, x0);
+                if (a.skip) {
+                    mbar_wait(&in_empty[s], ((k / NIN) & 1) ^ 1);           // conv3 of tile k - NIN done with in[s]
+                    mbar_expect_tx(&skf[s], G::TX_BYTES);
+                    tma_load_5d(sbase + s * G::INB, &tin, 0, x0 - 1, y0 - 1, 0, f, &skf[s]);
+                }
+                if (k >= 2) mbar_wait(&lo_empty[k & 1], ((k - 2) >> 1) & 1);
+                mbar_expect_tx(&lof[k & 1], G::LOB);
+                tma_load_4d(sbase + G::OFF_LO + (k & 1) * G::LOB, &tlo, 0, x0 / 2 - 1, y0 / 2 - 1, f, &lof[k & 1]);
+            }
         }
     } else if (warp == MW) {
         // ------------------------------------------------------------ MMA issuer
@@ -1507,13 +1597,13 @@ __global__ void __launch_bounds__((NPW + 9) * 32, 1) level_kernel(const __grid_c
                 // field (building each descriptor in the loop costs ~70 issue
                 // cycles per UMMA: the single MMA thread, not the tensor core,
                 // was the limit; tools/umma_layout_probe.cu)
-                const uint64_t da0 = umma_desc(sbase + s * G::INB, G::PIN, G::IC * 16);
+                const uint64_t da0 = umma_desc(sbase + s * G::INB, G::PIN, G::ICB * 16);
                 const uint64_t db0 = umma_desc(sbase + G::OFF_W3, C3 * 16, 128);
                 if (!(a.dbg & 4)) {
 #pragma unroll 1
                     for (int tap = 0; tap < 9; ++tap) {
                         const int dy = tap / 3, dx = tap - 3 * dy;
-                        const uint64_t dat = da0 + (uint64_t)(dy * G::IC + dx);            // 16-B units
+                        const uint64_t dat = da0 + (uint64_t)(dy * G::ICB + dx);           // 16-B units
                         const uint64_t dbt = db0 + (uint64_t)(tap * G::KK * C3 * 2);
 #pragma unroll
                         for (int b = 0; b < NB; ++b)
@@ -1762,8 +1852,8 @@ nsm_status launch_level(const LevelArgs& a, int nf, cudaStream_t st, const char*
     } else {
         ok = encode_nhwc_map4(a.x, bf, CIN, a.H / 2, a.W / 2, nf, G::LC, G::LR, &tlo);
         if (a.skip)
-            ok = ok && encode_nhwc_map4(a.skip, bf, CIN, a.H, a.W, nf, G::IC,
-                                        (G::NSK == 1 && NIN == 2) ? G::IR / 2 : G::IR, &tin);
+            ok = ok && (G::STAGED ? encode_nhwc_map4(a.skip, bf, CIN, a.H, a.W, nf, G::IC, G::IR, &tin)
+                                  : encode_nhwc_map(a.skip, bf, CIN, a.H, a.W, nf, G::ICB, G::IRB, &tin));
     }
     if (!ok) return fail(NSM_ERR_CUDA, "%s: TMA tensor map encoding failed", name);
     const int total = ((a.W + G::TW - 1) / G::TW) * ((a.H + G::TH - 1) / G::TH) * nf;
@@ -1779,7 +1869,7 @@ nsm_status launch_level(const LevelArgs& a, int nf, cudaStream_t st, const char*
     }
     const_cast<LevelArgs&>(a).trace = trace ? trace_buf : nullptr;
     NSM_PROF(name, st);
-    launch_pdl(k, dim3(grid), dim3((NPW + 9) * 32), G::SMEM, st, a, tin, tlo, total);
+    launch_pdl(k, dim3(grid), dim3((NPW + 9 + (SRC == SRC_UP)) * 32), G::SMEM, st, a, tin, tlo, total);
     if (trace) {   // experiments only: print CTA 0's timeline (us at 1.965 GHz) and stall the stream
         long long h[32 * 8];
         cudaMemcpyAsync(h, trace_buf, sizeof h, cudaMemcpyDeviceToHost, st);
