@@ -5,6 +5,7 @@
 #include <cstdio>
 #include <cstdint>
 #include <cuda_runtime.h>
+#include <cuda_fp16.h>
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 __device__ __forceinline__ uint64_t make_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
@@ -35,6 +36,17 @@ __global__ void __launch_bounds__(256, 1) k(long long* cyc, int iters, int sbo, 
     asm volatile("tcgen05.fence::before_thread_sync;");
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;");
+    if (noise == 3) {   // fill the operands with pseudo-random fp16 values (not zeros)
+        for (int i = threadIdx.x; i < 200 * 1024 / 4; i += blockDim.x) {
+            uint32_t h = i * 2654435761u;
+            h ^= h >> 13;
+            const float f0 = ((h & 0xffff) / 65536.f - 0.5f), f1 = (((h >> 16) & 0xffff) / 65536.f - 0.5f);
+            __half2 v = __floats2half2_rn(f0, f1);
+            reinterpret_cast<uint32_t*>(sm)[i] = *reinterpret_cast<uint32_t*>(&v);
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncthreads();
+    }
     const uint32_t base = smem_u32(sm);
     const uint32_t bb = base + 160 * 1024;
     const uint32_t idesc = make_idesc(128, N);
@@ -93,7 +105,7 @@ __global__ void __launch_bounds__(256, 1) k(long long* cyc, int iters, int sbo, 
         cyc[blockIdx.x] = clock64() - t0;
         atomicExch(&g_sink, 1);
     }
-    if (threadIdx.x >= 128 && noise) {   // contention: TMEM loads (1) or SMEM loads (2) until the MMA loop ends
+    if (threadIdx.x >= 128 && (noise == 1 || noise == 2)) {   // contention: TMEM loads (1) or SMEM loads (2) until the MMA loop ends
         const int w = (threadIdx.x >> 5) & 3;
         uint32_t acc = 0;
         for (int it = 0; it < 200000 && !*(volatile int*)&g_sink; ++it) {
@@ -138,10 +150,9 @@ int main() {
         auto R = [&](int sbo, int shift, int lbo, int taps, int noise) {
             if (n == 32) run<32>(sbo, shift, lbo, taps, noise); else run<64>(sbo, shift, lbo, taps, noise);
         };
-        R(544, 0, 9792, -1, 0);    // one accumulator
-        R(544, 0, 9792, -2, 0);    // four accumulators, per-tap loop (level-kernel pattern)
-        R(544, 0, 9792, -3, 0);    // four accumulators, fully unrolled
-        R(544, 0, 9792, -4, 0);    // block-outer
+        R(544, 0, 9792, -2, 0);    // four accumulators, per-tap loop, zero operands
+        R(544, 0, 9792, -2, 3);    // ... random operands
+        R(544, 0, 9792, -3, 3);    // fully unrolled, random operands
     }
     return 0;
 }
