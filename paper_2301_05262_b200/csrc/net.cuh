@@ -32,6 +32,10 @@ struct Plan {
     int out_ch = 0;
     Level lev[kMaxLevels];
     ConvW head;
+    // level-0 decoder in polyphase form on the level-1 grid (dec0p_kernel):
+    // conv3(up2(x)) = 4 phase convolutions of x, stacked along N (4 x 16);
+    // dec1 and the head as phase-block-diagonal 1x1 convs (K = 64)
+    ConvW d0p3, d0p1, d0ph;
     int64_t n_params = 0;
     void* dev = nullptr;          // one allocation holding every tensor
     size_t dev_bytes = 0;

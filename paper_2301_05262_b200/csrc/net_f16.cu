@@ -1183,7 +1183,10 @@ __global__ void __launch_bounds__(128) recon_kernel(const float* __restrict__ y,
 
 // ------------------------------------------------------------- levels 1-3 (tcgen05)
 enum { SRC_TENSOR = 0, SRC_UP = 1 };
-enum { DST_STORE = 1, DST_POOL = 2 };
+// DST_PADREP: the stored tensor is (N, H + 2, W + 2, C1) with a one-pixel
+// border that replicates the edge (the polyphase level-0 decoder reads the
+// edge-clamped upsampling source from it without bounds logic)
+enum { DST_STORE = 1, DST_POOL = 2, DST_PADREP = 4 };
 
 struct LevelArgs {
     const void* x;       // SRC_TENSOR: (N, H, W, CIN); SRC_UP: (N, H/2, W/2, CIN)
@@ -1727,10 +1730,26 @@ __global__ void __launch_bounds__((NPW + 9 + (SRC == SRC_UP)) * 32, 1) level_ker
                             uint32_t* qp = &qv[0].x;
 #pragma unroll
                             for (int e = 0; e < 8; ++e) qp[e] = Elem<T>::pack(v[2 * e], v[2 * e + 1]);
-                            uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<T*>(a.out) +
-                                                                  (((int64_t)f * a.H + oy) * a.W + ox) * C1 + c0);
-                            dst[0] = qv[0];
-                            dst[1] = qv[1];
+                            if constexpr (DST & DST_PADREP) {
+                                const int wp = a.W + 2;
+                                T* fb = reinterpret_cast<T*>(a.out) + (int64_t)f * (a.H + 2) * wp * C1 + c0;
+                                const int ys[2] = {oy + 1, oy == 0 ? 0 : (oy == a.H - 1 ? a.H + 1 : -1)};
+                                const int xs[2] = {ox + 1, ox == 0 ? 0 : (ox == a.W - 1 ? a.W + 1 : -1)};
+#pragma unroll
+                                for (int iy = 0; iy < 2; ++iy)
+#pragma unroll
+                                    for (int ix = 0; ix < 2; ++ix)
+                                        if (ys[iy] >= 0 && xs[ix] >= 0) {
+                                            uint4* dst = reinterpret_cast<uint4*>(fb + ((int64_t)ys[iy] * wp + xs[ix]) * C1);
+                                            dst[0] = qv[0];
+                                            dst[1] = qv[1];
+                                        }
+                            } else {
+                                uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<T*>(a.out) +
+                                                                      (((int64_t)f * a.H + oy) * a.W + ox) * C1 + c0);
+                                dst[0] = qv[0];
+                                dst[1] = qv[1];
+                            }
                         }
                     }
                     if (DST & DST_POOL) {
@@ -1821,11 +1840,15 @@ bool encode_nhwc_map(const void* base, bool bf16, int C, int H, int W, int nf, i
 
 // 4-D pixel-major view (C elems, x, y, frame) of an NHWC 16-bit tensor.
 bool encode_nhwc_map4(const void* base, bool bf16, int C, int H, int W, int nf, int box_w, int box_h,
-                      CUtensorMap* m) {
+                      CUtensorMap* m, int pad = 0) {
+    // pad: the tensor lives inside a (H + 2 pad, W + 2 pad) allocation (the map
+    // covers the interior, so out-of-range boxes still read zeros)
     auto enc = tensor_map_encoder();
+    const int Wa = W + 2 * pad, Ha = H + 2 * pad;
+    base = (const char*)base + ((size_t)pad * Wa + pad) * C * 2;
     if (!enc || ((uintptr_t)base % 16)) return false;
     const cuuint64_t dims[4] = {(cuuint64_t)C, (cuuint64_t)W, (cuuint64_t)H, (cuuint64_t)nf};
-    const cuuint64_t strides[3] = {(cuuint64_t)C * 2, (cuuint64_t)W * C * 2, (cuuint64_t)H * W * C * 2};
+    const cuuint64_t strides[3] = {(cuuint64_t)C * 2, (cuuint64_t)Wa * C * 2, (cuuint64_t)Ha * Wa * C * 2};
     const cuuint32_t box[4] = {(cuuint32_t)C, (cuuint32_t)box_w, (cuuint32_t)box_h, 1};
     const cuuint32_t es[4] = {1, 1, 1, 1};
     return enc(m, bf16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 4,
@@ -1912,7 +1935,7 @@ Bufs carve(void* ws, int nf, int H0, int W0, int es) {
     b.p3 = take((size_t)nf * H3 * W3 * 64 * es);
     b.b3 = take((size_t)nf * H3 * W3 * 64 * es);
     b.d2 = take((size_t)nf * H2 * W2 * 32 * es);
-    b.d1 = take((size_t)nf * H1 * W1 * 16 * es);
+    b.d1 = take((size_t)nf * (H1 + 2) * (W1 + 2) * 16 * es);   // replicate-padded (DST_PADREP)
     b.y = (float*)take((size_t)nf * H0 * W0 * 16);
     b.bytes = (size_t)(p - (char*)ws);
     return b;
@@ -1943,7 +1966,7 @@ nsm_status run_levels(const Plan& p, const Bufs& b, int nf, int H0, int W0, cuda
     if (s != NSM_OK) return s;
     // l1 decoder: up(D2) + S1 -> 32 -> D1 (16)
     a = LevelArgs{b.d2, b.s1, H1, W1, L1.dec3.wpk, L1.dec3.b32, L1.dec1.wpk, L1.dec1.b32, b.d1, nullptr};
-    s = launch_level<T, 32, 32, 16, SRC_UP, DST_STORE, 4, 2, 2>(a, nf, st, "lv1_dec");
+    s = launch_level<T, 32, 32, 16, SRC_UP, DST_STORE | DST_PADREP, 4, 2, 2>(a, nf, st, "lv1_dec");
     (void)W3;
     return s;
 }
@@ -2012,7 +2035,7 @@ nsm_status run_l0(const Plan& p, const Bufs& b, const Enc0Args& e0, const GbufMa
     {
         CUtensorMap dm;
         memset(&dm, 0, sizeof dm);
-        if (!encode_nhwc_map4(b.d1, std::is_same<T, __nv_bfloat16>::value, 16, H0 / 2, W0 / 2, nf, D0_LC, D0_LR, &dm))
+        if (!encode_nhwc_map4(b.d1, std::is_same<T, __nv_bfloat16>::value, 16, H0 / 2, W0 / 2, nf, D0_LC, D0_LR, &dm, 1))
             return fail(NSM_ERR_CUDA, "dec0: TMA tensor map encoding failed");
         NSM_PROF("dec0_fused", st);
         launch_pdl(dec0_kernel<T>, dim3(pgrid), dim3(kL0Threads), DEC0_SMEM, st, d, dm, total);
@@ -2084,12 +2107,73 @@ nsm_status pack_f16(Plan& p, std::vector<char>& blob, size_t& offset_out) {
             umma(p.lev[j].dec1);
         }
     }
+    // Polyphase level-0 decoder (dec0p_kernel).  up2 with an edge clamp is
+    // up2 of the replicate-padded low-res tensor, so every output phase
+    // (a, b) of conv3(up2(x)) is a 3x3 convolution of x whose taps combine
+    // the reference's taps with the (1/4, 3/4) bilinear weights; only the
+    // outermost level-0 ring (where the conv's zero padding differs from
+    // the replicate padding) is recomputed by dec0_ring_kernel.
+    std::vector<float> w3p, w1d, whd;
+    const ConvW& d3 = p.lev[0].dec3;
+    const ConvW& d1 = p.lev[0].dec1;
+    if (d3.present() && d3.k == 3 && d3.cin == 16 && d3.cout == 16 && d1.cin == 16 && d1.cout == 16 &&
+        p.head.cin == 16 && p.head.cout == 4) {
+        auto coef = [](int a, int d, float (&c)[3]) {     // x(i + l - 1) weights in U(2i + a + d - 1)
+            c[0] = c[1] = c[2] = 0.f;
+            const int r = a + d - 1, m = (r >= 0 ? r / 2 : -1), ph = r - 2 * m;
+            if (ph == 0) {
+                c[m] += 0.25f;
+                c[m + 1] += 0.75f;
+            } else {
+                c[m + 1] += 0.75f;
+                c[m + 2] += 0.25f;
+            }
+        };
+        w3p.assign(64 * 16 * 9, 0.f);
+        for (int a = 0; a < 2; ++a)
+            for (int b = 0; b < 2; ++b)
+                for (int dy = 0; dy < 3; ++dy)
+                    for (int dx = 0; dx < 3; ++dx) {
+                        float cy[3], cx[3];
+                        coef(a, dy, cy);
+                        coef(b, dx, cx);
+                        for (int co = 0; co < 16; ++co)
+                            for (int ci = 0; ci < 16; ++ci) {
+                                const float w = d3.w32[((size_t)co * 16 + ci) * 9 + dy * 3 + dx];
+                                for (int ly = 0; ly < 3; ++ly)
+                                    for (int lx = 0; lx < 3; ++lx)
+                                        w3p[((size_t)((a * 2 + b) * 16 + co) * 16 + ci) * 9 + ly * 3 + lx] +=
+                                            w * cy[ly] * cx[lx];
+                            }
+                    }
+        w1d.assign(64 * 64, 0.f);
+        whd.assign(16 * 64, 0.f);
+        for (int ph = 0; ph < 4; ++ph) {
+            for (int co = 0; co < 16; ++co)
+                for (int ci = 0; ci < 16; ++ci) w1d[(size_t)(ph * 16 + co) * 64 + ph * 16 + ci] = d1.w32[co * 16 + ci];
+            for (int hc = 0; hc < 4; ++hc)
+                for (int ci = 0; ci < 16; ++ci) whd[(size_t)(ph * 4 + hc) * 64 + ph * 16 + ci] = p.head.w32[hc * 16 + ci];
+        }
+        auto setc = [](ConvW& c, const std::vector<float>& w, int cout, int cin, int k) {
+            c.cin = cin;
+            c.cout = cout;
+            c.k = k;
+            c.w32 = w.data();
+        };
+        setc(p.d0p3, w3p, 64, 16, 3);
+        setc(p.d0p1, w1d, 64, 64, 1);
+        setc(p.d0ph, whd, 16, 64, 1);
+        umma(p.d0p3);
+        umma(p.d0p1);
+        umma(p.d0ph);
+    }
     for (auto& it : items) {
         const size_t off = (blob.size() + 255) / 256 * 256;
         blob.resize(off + it.bytes.size());
         memcpy(blob.data() + off, it.bytes.data(), it.bytes.size());
         it.c->wpk = (const void*)(uintptr_t)off;   // rebased to the device block later
     }
+    p.d0p3.w32 = p.d0p1.w32 = p.d0ph.w32 = nullptr;   // host-only sources (packed above)
     offset_out = blob.size();
     return NSM_OK;
 }
