@@ -1797,6 +1797,400 @@ __global__ void __launch_bounds__((NPW + 9 + (SRC == SRC_UP)) * 32, 1) level_ker
     if (warp == EW0) tmem_dealloc<G::TCOLS>(tmem);
 }
 
+// The outer ring of level-0 pixels (rows 0 and H0-1, columns 0 and W0-1):
+// dec3 (zero padding of the up2 image), dec1 and the head in fp32, straight
+// from D1 (autodiff.py:258-287; network.py:199-205): dec0_ring_kernel runs
+// after dec0p_kernel and overwrites these pixels.  A warp takes a run of 30
+// consecutive pixels of one side (lanes 1-30; lanes 0 and 31 are the halo):
+// every lane computes the up2
+// values of its position on the two image lines the side's taps touch (16
+// independent D1 loads), the neighbouring taps come from the adjacent lanes
+// by shuffles, and all lanes use the same tap's weights at the same time, so
+// the weight loads are shared-memory broadcasts.
+struct RingW {              // packed once per plan (pack_f16)
+    float w3[9][16][16];   // [tap][ci][co]
+    float w1[16][16];      // [ci][co]
+    float wh[16][4];       // [ci][c]
+    float b[36];           // b3, b1, bh
+};
+// gwarp / nwarps: this warp's index among the ring warps of the grid
+template <typename T>
+__device__ __forceinline__ void ring_run(const RingW& rw, const T* __restrict__ d1p, int H1, int W1, int H0, int W0,
+                                         float* __restrict__ y, int nf, int gwarp, int nwarps) {
+    const int lane = threadIdx.x & 31;
+    const int Wp = W1 + 2;
+    const int64_t plane = (int64_t)H0 * W0;
+    const int runs_h = (W0 + 29) / 30, runs_v = (H0 - 2 + 29) / 30, per_frame = 2 * (runs_h + runs_v);
+    for (int item = gwarp; item < per_frame * nf; item += nwarps) {
+        const int f = item / per_frame;
+        int r = item - f * per_frame, side, run;
+        if (r < 2 * runs_h) side = r / runs_h, run = r % runs_h;              // 0 top, 1 bottom
+        else r -= 2 * runs_h, side = 2 + r / runs_v, run = r % runs_v;         // 2 left, 3 right
+        const bool horiz = side < 2;
+        // this lane's position along the side (a column, or a row in 1..H0-2)
+        const int sp = horiz ? run * 30 + lane - 1 : run * 30 + lane;
+        const int extent = horiz ? W0 : H0;
+        const bool owned = lane >= 1 && lane <= 30 && (horiz ? sp < W0 : sp <= H0 - 2);
+        const uint4* x = reinterpret_cast<const uint4*>(d1p + (int64_t)f * (H1 + 2) * Wp * 16);
+        // up2 of D1 at the two lines next to the side (0 outside the image)
+        float u[2][16];
+#pragma unroll
+        for (int k = 0; k < 2; ++k) {
+            const int line = side == 0 ? k : side == 1 ? H0 - 2 + k : side == 2 ? k : W0 - 2 + k;
+            const int rr = horiz ? line : sp, cc = horiz ? sp : line;
+            const float m = (sp >= 0 && sp < extent) ? 1.f : 0.f;
+            const float sy = fminf(fmaxf((rr + 0.5f) * 0.5f - 0.5f, 0.f), (float)(H1 - 1));
+            const float sx = fminf(fmaxf((cc + 0.5f) * 0.5f - 0.5f, 0.f), (float)(W1 - 1));
+            const int y0 = (int)sy, x0 = (int)sx;
+            const float wy = sy - y0, wx = sx - x0;
+            const int y1 = min(y0 + 1, H1 - 1), x1 = min(x0 + 1, W1 - 1);
+            uint4 q[8];
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+                const int64_t o = ((int64_t)((c >> 1 ? y1 : y0) + 1) * Wp + ((c & 1 ? x1 : x0) + 1)) * 2;
+                q[2 * c] = __ldg(x + o);
+                q[2 * c + 1] = __ldg(x + o + 1);
+            }
+            const float cw[4] = {m * (1.f - wy) * (1.f - wx), m * (1.f - wy) * wx, m * wy * (1.f - wx), m * wy * wx};
+#pragma unroll
+            for (int e = 0; e < 16; ++e) u[k][e] = 0.f;
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+                const uint32_t wv[8] = {q[2 * c].x, q[2 * c].y, q[2 * c].z, q[2 * c].w,
+                                        q[2 * c + 1].x, q[2 * c + 1].y, q[2 * c + 1].z, q[2 * c + 1].w};
+#pragma unroll
+                for (int e = 0; e < 8; ++e) {
+                    const float2 v = Elem<T>::unpack(wv[e]);
+                    u[k][2 * e] += cw[c] * v.x;
+                    u[k][2 * e + 1] += cw[c] * v.y;
+                }
+            }
+        }
+        // dec3 over the 6 in-image taps: line k, neighbour d along the side
+        float acc[16];
+#pragma unroll
+        for (int co = 0; co < 16; ++co) acc[co] = rw.b[co];
+#pragma unroll
+        for (int k = 0; k < 2; ++k) {
+            const int across = (side == 0 || side == 2) ? k + 1 : k;      // dy (horiz) / dx (vert) of line k
+#pragma unroll
+            for (int d = -1; d <= 1; ++d) {
+                const int tap = horiz ? across * 3 + d + 1 : (d + 1) * 3 + across;
+#pragma unroll
+                for (int ci = 0; ci < 16; ++ci) {
+                    const float v = d == 0 ? u[k][ci] : d < 0 ? __shfl_up_sync(0xffffffffu, u[k][ci], 1)
+                                                              : __shfl_down_sync(0xffffffffu, u[k][ci], 1);
+                    const float4* wr = reinterpret_cast<const float4*>(&rw.w3[tap][ci][0]);
+#pragma unroll
+                    for (int c4 = 0; c4 < 4; ++c4) {
+                        const float4 w = wr[c4];
+                        acc[4 * c4] += w.x * v;
+                        acc[4 * c4 + 1] += w.y * v;
+                        acc[4 * c4 + 2] += w.z * v;
+                        acc[4 * c4 + 3] += w.w * v;
+                    }
+                }
+            }
+        }
+        float hid[16];
+#pragma unroll
+        for (int co = 0; co < 16; ++co) hid[co] = rw.b[16 + co];
+#pragma unroll
+        for (int ci = 0; ci < 16; ++ci) {
+            const float a0 = fmaxf(acc[ci], 0.f);
+            const float4* wr = reinterpret_cast<const float4*>(&rw.w1[ci][0]);
+#pragma unroll
+            for (int c4 = 0; c4 < 4; ++c4) {
+                const float4 w = wr[c4];
+                hid[4 * c4] += w.x * a0;
+                hid[4 * c4 + 1] += w.y * a0;
+                hid[4 * c4 + 2] += w.z * a0;
+                hid[4 * c4 + 3] += w.w * a0;
+            }
+        }
+        float o[4] = {rw.b[32], rw.b[33], rw.b[34], rw.b[35]};
+#pragma unroll
+        for (int ci = 0; ci < 16; ++ci) {
+            const float hv = fmaxf(hid[ci], 0.f);
+            const float4 w = *reinterpret_cast<const float4*>(&rw.wh[ci][0]);
+            o[0] += w.x * hv;
+            o[1] += w.y * hv;
+            o[2] += w.z * hv;
+            o[3] += w.w * hv;
+        }
+        if (owned) {
+            const int R = horiz ? (side == 0 ? 0 : H0 - 1) : sp, C = horiz ? sp : (side == 2 ? 0 : W0 - 1);
+#pragma unroll
+            for (int c = 0; c < 4; ++c) y[((int64_t)f * 4 + c) * plane + (int64_t)R * W0 + C] = o[c];
+        }
+    }
+}
+
+// ------------------------------------------------------------- level 0 decoder, polyphase (tcgen05)
+// dec0 = head(relu(dec1(relu(conv3(up2(D1)))))) evaluated on the level-1
+// grid: up2 with an edge clamp is up2 of the replicate-padded D1 (written by
+// lv1_dec, DST_PADREP), so conv3(up2(D1)) is, for each of the 4 output
+// phases (a, b), a 3x3 convolution of D1 with combined taps (pack_f16).  One
+// M-block = 16 x 8 level-1 pixels (128 lanes); N = 4 phases x 16 channels:
+//   conv3  9 UMMAs  N = 64, K = 16   (A: shifted views of the D1 tile)
+//   dec1   4 UMMAs  N = 64, K = 64   (A in TMEM, phase-block-diagonal B)
+//   head   4 UMMAs  N = 16, K = 64   (A in TMEM)
+// Epilogues: bias + ReLU + pack into TMEM (the next A), and the head's 16
+// values (4 phases x 4 channels) into the fp32 Y planes.  The zero padding
+// of the level-0 conv differs from the replicate padding only on the outer
+// ring of level-0 pixels, which dec0_ring_kernel recomputes exactly.
+// Warps: 0 TMA, 1-4 conv3 epilogue, 5-8 dec1 epilogue, 9-12 head epilogue
+// (one warp per TMEM lane quadrant in each group), 13-15 one MMA issuer per
+// GEMM.  Every TMEM stage is double buffered and every stage has its own
+// warps, so the MMA/epilogue round trips of consecutive tiles overlap.
+struct Dec0pArgs {
+    const void* w3;      // umma [9][1][2][64][8]
+    const void* w1;      // umma [1][4][2][64][8]
+    const void* wh;      // umma [1][4][2][16][8]
+    const float* b3;     // (16,)  l0.dec3 bias (replicated per phase)
+    const float* b1;     // (16,)  l0.dec1 bias
+    const float* bh;     // (4,)   head bias
+    float* y;            // (N, 4, H0, W0)
+    int H1, W1, H0, W0;
+};
+constexpr int D0P_IR = 18, D0P_IC = 10, D0P_NIN = 4;
+constexpr int D0P_PIN = D0P_IR * D0P_IC * 16, D0P_INB = round128(2 * D0P_PIN);
+constexpr int D0P_W3B = 9 * 2 * 64 * 16, D0P_W1B = 4 * 2 * 64 * 16, D0P_WHB = 4 * 2 * 16 * 16;
+constexpr int D0P_OFF_W3 = D0P_NIN * D0P_INB, D0P_OFF_W1 = D0P_OFF_W3 + D0P_W3B, D0P_OFF_WH = D0P_OFF_W1 + D0P_W1B;
+constexpr int D0P_OFF_B = D0P_OFF_WH + D0P_WHB, D0P_OFF_BAR = D0P_OFF_B + 48 * 4;
+constexpr int D0P_SMEM = D0P_OFF_BAR + 256;
+constexpr int D0P_THREADS = 512;
+constexpr int D0P_ACC3 = 0, D0P_ACC1 = 128, D0P_ACCH = 256, D0P_MID = 288, D0P_MID2 = 352;   // MID/MID2: 2 x 32
+
+template <typename T>
+__global__ void __launch_bounds__(D0P_THREADS, 1) dec0p_kernel(const __grid_constant__ Dec0pArgs a,
+                                                       const __grid_constant__ CUtensorMap tin, int total) {
+    extern __shared__ __align__(128) uint8_t smem[];
+    uint64_t* bar = reinterpret_cast<uint64_t*>(smem + D0P_OFF_BAR);
+    uint64_t* in_full = bar + 0;     // [4]
+    uint64_t* in_empty = bar + 4;    // [4]
+    uint64_t* a3_full = bar + 8;     // [2]
+    uint64_t* a3_empty = bar + 10;
+    uint64_t* a1_full = bar + 12;
+    uint64_t* a1_empty = bar + 14;
+    uint64_t* ah_full = bar + 16;
+    uint64_t* ah_empty = bar + 18;
+    uint64_t* mid_full = bar + 20;   // [2]
+    uint64_t* mid_empty = bar + 22;
+    uint64_t* mid2_full = bar + 24;
+    uint64_t* mid2_empty = bar + 26;
+    uint64_t* wbar = bar + 28;
+    uint32_t* tptr = reinterpret_cast<uint32_t*>(smem + D0P_OFF_BAR + 240);
+    float* sbias = reinterpret_cast<float*>(smem + D0P_OFF_B);     // b3[16] b1[16] bh[4]
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const uint32_t sbase = smem_u32(smem);
+    const int ntx = (a.W1 + 7) / 8, nty = (a.H1 + 15) / 16;
+    const int mytiles = (int)blockIdx.x < total ? (total - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x : 0;
+    auto tile_of = [&](int k, int& f, int& y0, int& x0) {   // level-1 tile origin
+        const int t = blockIdx.x + k * gridDim.x;
+        x0 = (t % ntx) * 8;
+        y0 = ((t / ntx) % nty) * 16;
+        f = t / (ntx * nty);
+    };
+    if (tid == 0) pdl_trigger();
+    if (warp == 13) tmem_alloc<512>(tptr);
+    if (tid == 0) {
+        for (int i = 0; i < D0P_NIN; ++i) {
+            mbar_init(&in_full[i], 1);
+            mbar_init(&in_empty[i], 1);
+        }
+        for (int i = 0; i < 2; ++i) {                 // epilogue arrivals: every thread of a 4-warp group
+            mbar_init(&a3_full[i], 1);
+            mbar_init(&a3_empty[i], 128);
+            mbar_init(&a1_full[i], 1);
+            mbar_init(&a1_empty[i], 128);
+            mbar_init(&ah_full[i], 1);
+            mbar_init(&ah_empty[i], 128);
+            mbar_init(&mid_full[i], 128);
+            mbar_init(&mid_empty[i], 1);
+            mbar_init(&mid2_full[i], 128);
+            mbar_init(&mid2_empty[i], 1);
+        }
+        mbar_init(wbar, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        mbar_expect_tx(wbar, D0P_W3B + D0P_W1B + D0P_WHB);
+        bulk_g2s(sbase + D0P_OFF_W3, a.w3, D0P_W3B, wbar);
+        bulk_g2s(sbase + D0P_OFF_W1, a.w1, D0P_W1B, wbar);
+        bulk_g2s(sbase + D0P_OFF_WH, a.wh, D0P_WHB, wbar);
+    }
+    if (tid < 16) sbias[tid] = a.b3[tid];
+    else if (tid < 32) sbias[tid] = a.b1[tid - 16];
+    else if (tid < 36) sbias[tid] = a.bh[tid - 32];
+    fence_proxy_async();
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tptr;
+    pdl_wait();
+
+    if (warp == 0) {
+        // ------------------------------------------------------------ TMA
+        if (lane == 0) {
+            for (int k = 0; k < mytiles; ++k) {
+                const int s = k % D0P_NIN;
+                mbar_wait(&in_empty[s], ((k / D0P_NIN) & 1) ^ 1);
+                int f, y0, x0;
+                tile_of(k, f, y0, x0);
+                mbar_expect_tx(&in_full[s], 2 * D0P_PIN);
+                // padded coordinates: real (y0 - 1, x0 - 1) is padded (y0, x0)
+                tma_load_5d(sbase + s * D0P_INB, &tin, 0, x0, y0, 0, f, &in_full[s]);
+            }
+        }
+    } else if (warp >= 13) {
+        // ------------------------------------------------------------ MMA issuers, one per GEMM
+        if (lane == 0) {
+            constexpr uint32_t id64 = umma_idesc(128, 64, Elem<T>::kUmmaFmt);
+            constexpr uint32_t id16 = umma_idesc(128, 16, Elem<T>::kUmmaFmt);
+            mbar_wait(wbar, 0);
+            if (warp == 13) {
+                const uint64_t dw3 = umma_desc(sbase + D0P_OFF_W3, 64 * 16, 128);
+                for (int k = 0; k < mytiles; ++k) {                  // conv3(k)
+                    const int s = k % D0P_NIN, a3 = k & 1;
+                    mbar_wait(&in_full[s], (k / D0P_NIN) & 1);
+                    mbar_wait(&a3_empty[a3], ((k >> 1) & 1) ^ 1);
+                    tc_fence_after();
+                    const uint64_t da0 = umma_desc(sbase + s * D0P_INB, D0P_PIN, D0P_IC * 16);
+#pragma unroll
+                    for (int tap = 0; tap < 9; ++tap)
+                        umma_f16(tmem + D0P_ACC3 + a3 * 64, da0 + (uint64_t)((tap / 3) * D0P_IC + tap % 3),
+                                 dw3 + (uint64_t)(tap * 128), id64, tap ? 1u : 0u);
+                    umma_commit(&in_empty[s]);
+                    umma_commit(&a3_full[a3]);
+                }
+            } else if (warp == 14) {
+                const uint64_t dw1 = umma_desc(sbase + D0P_OFF_W1, 64 * 16, 128);
+                for (int j = 0; j < mytiles; ++j) {                  // dec1(j)
+                    const int a1 = j & 1;
+                    mbar_wait(&mid_full[a1], (j >> 1) & 1);
+                    mbar_wait(&a1_empty[a1], ((j >> 1) & 1) ^ 1);
+                    tc_fence_after();
+#pragma unroll
+                    for (int kk = 0; kk < 4; ++kk)
+                        umma_f16_ts(tmem + D0P_ACC1 + a1 * 64, tmem + D0P_MID + a1 * 32 + kk * 8, dw1 + (uint64_t)(kk * 128),
+                                    id64, kk ? 1u : 0u);
+                    umma_commit(&mid_empty[a1]);
+                    umma_commit(&a1_full[a1]);
+                }
+            } else {
+                const uint64_t dwh = umma_desc(sbase + D0P_OFF_WH, 16 * 16, 128);
+                for (int j = 0; j < mytiles; ++j) {                  // head(j)
+                    const int ah = j & 1;
+                    mbar_wait(&mid2_full[ah], (j >> 1) & 1);
+                    mbar_wait(&ah_empty[ah], ((j >> 1) & 1) ^ 1);
+                    tc_fence_after();
+#pragma unroll
+                    for (int kk = 0; kk < 4; ++kk)
+                        umma_f16_ts(tmem + D0P_ACCH + ah * 16, tmem + D0P_MID2 + ah * 32 + kk * 8, dwh + (uint64_t)(kk * 32),
+                                    id16, kk ? 1u : 0u);
+                    umma_commit(&mid2_empty[ah]);
+                    umma_commit(&ah_full[ah]);
+                }
+            }
+        }
+    } else {
+        // ------------------------------------------------------------ epilogue
+        const int q = warp & 3;                               // TMEM lane quadrant
+        const int m = q * 32 + lane, pi = m >> 3, pj = m & 7;
+        const uint32_t tl = (uint32_t)(q * 32) << 16;
+        const int64_t plane = (int64_t)a.H0 * a.W0;
+        // bias + ReLU of 64 accumulator columns -> 32 packed columns of the next A
+        auto relu_to_tmem = [&](uint32_t src, uint32_t dst, const float* bias) {
+            uint32_t r[4][16];
+#pragma unroll
+            for (int h = 0; h < 4; ++h) tmem_ld16_nw(src + h * 16, r[h]);
+            tmem_ld_wait();
+#pragma unroll
+            for (int h = 0; h < 4; ++h) {
+                uint32_t pk[8];
+#pragma unroll
+                for (int e = 0; e < 8; ++e)
+                    pk[e] = Elem<T>::pack(fmaxf(__uint_as_float(r[h][2 * e]) + bias[(2 * e) & 15], 0.f),
+                                          fmaxf(__uint_as_float(r[h][2 * e + 1]) + bias[(2 * e + 1) & 15], 0.f));
+                tmem_st8(dst + h * 8, pk);
+            }
+            tmem_st_wait();
+        };
+        if (warp <= 4) {
+            for (int k = 0; k < mytiles; ++k) {                      // conv3(k) -> MID[k & 1]
+                const int a3 = k & 1;
+                mbar_wait(&a3_full[a3], (k >> 1) & 1);
+                mbar_wait(&mid_empty[a3], ((k >> 1) & 1) ^ 1);
+                tc_fence_after();
+                relu_to_tmem(tmem + tl + D0P_ACC3 + a3 * 64, tmem + tl + D0P_MID + a3 * 32, sbias);
+                tc_fence_before();
+                mbar_arrive(&a3_empty[a3]);
+                mbar_arrive(&mid_full[a3]);
+            }
+        } else if (warp <= 8) {
+            for (int k = 0; k < mytiles; ++k) {                      // dec1(k) -> MID2[k & 1]
+                const int a1 = k & 1;
+                mbar_wait(&a1_full[a1], (k >> 1) & 1);
+                mbar_wait(&mid2_empty[a1], ((k >> 1) & 1) ^ 1);
+                tc_fence_after();
+                relu_to_tmem(tmem + tl + D0P_ACC1 + a1 * 64, tmem + tl + D0P_MID2 + a1 * 32, sbias + 16);
+                tc_fence_before();
+                mbar_arrive(&a1_empty[a1]);
+                mbar_arrive(&mid2_full[a1]);
+            }
+        } else {
+            for (int j = 0; j < mytiles; ++j) {                      // head(j) -> Y
+                const int ah = j & 1;
+                int f, y0, x0;
+                tile_of(j, f, y0, x0);
+                mbar_wait(&ah_full[ah], (j >> 1) & 1);
+                tc_fence_after();
+                uint32_t r[16];                                      // phases (a, b) x 4 channels
+                tmem_ld16_nw(tmem + tl + D0P_ACCH + ah * 16, r);
+                tmem_ld_wait();
+                tc_fence_before();
+                mbar_arrive(&ah_empty[ah]);
+                // level-0 pixels (oy, ox) and (oy, ox + 1); dec0_ring_kernel
+                // overwrites the outer ring afterwards
+                const int ox = 2 * (x0 + pj);
+#pragma unroll
+                for (int ph = 0; ph < 2; ++ph) {
+                    const int oy = 2 * (y0 + pi) + ph;
+                    if (oy < a.H0 && ox < a.W0) {
+                        float* yp = a.y + (int64_t)f * 4 * plane + (int64_t)oy * a.W0 + ox;
+#pragma unroll
+                        for (int c = 0; c < 4; ++c) {
+                            const float v0 = __uint_as_float(r[ph * 8 + c]) + sbias[32 + c];
+                            const float v1 = __uint_as_float(r[ph * 8 + 4 + c]) + sbias[32 + c];
+                            if (ox + 1 < a.W0) *reinterpret_cast<float2*>(yp + c * plane) = make_float2(v0, v1);
+                            else yp[c * plane] = v0;
+                        }
+                    }
+                }
+            }
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 13) tmem_dealloc<512>(tmem);
+}
+
+template <typename T>
+__global__ void __launch_bounds__(128) dec0_ring_kernel(const T* __restrict__ d1p, int H1, int W1, int H0, int W0,
+                                                        const RingW* __restrict__ wg, float* __restrict__ y, int nf) {
+    __shared__ __align__(16) RingW rw;
+    if (threadIdx.x == 0) pdl_trigger();
+    constexpr int NV = (int)sizeof(RingW) / 16;
+    static_assert(sizeof(RingW) % 16 == 0, "RingW is copied in 16-byte vectors");
+#pragma unroll
+    for (int k = 0; k < (NV + 127) / 128; ++k) {
+        const int i = threadIdx.x + k * 128;
+        if (i < NV) reinterpret_cast<uint4*>(&rw)[i] = __ldg(reinterpret_cast<const uint4*>(wg) + i);
+    }
+    __syncthreads();
+    pdl_wait();
+    ring_run<T>(rw, d1p, H1, W1, H0, W0, y, nf, blockIdx.x * 4 + (threadIdx.x >> 5), gridDim.x * 4);
+}
+
 // ------------------------------------------------------------------ host side
 int num_sms() {
     static int n = 0;
@@ -2032,7 +2426,33 @@ nsm_status run_l0(const Plan& p, const Bufs& b, const Enc0Args& e0, const GbufMa
     Dec0Args d{b.d1, H0, W0, (const uint2*)L0.dec3.wpk, (const uint2*)L0.dec1.wpk,
                (const uint2*)p.head.wpk, L0.dec3.b32, L0.dec1.b32, p.head.b32, b.y, d0dbg,
                tile_div(H0, W0)};
-    {
+    static const bool poly = !getenv("NSM_DEC0_POLY") || atoi(getenv("NSM_DEC0_POLY")) != 0;
+    if (poly && p.d0p3.present() && d0dbg == 0) {
+        // polyphase level-0 decoder on the level-1 grid + the exact outer ring
+        const int H1 = H0 / 2, W1 = W0 / 2;
+        static bool pattr = false;
+        if (!pattr) {
+            cudaFuncSetAttribute(dec0p_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, D0P_SMEM);
+            pattr = true;
+        }
+        CUtensorMap dm;
+        memset(&dm, 0, sizeof dm);
+        if (!encode_nhwc_map(b.d1, std::is_same<T, __nv_bfloat16>::value, 16, H1 + 2, W1 + 2, nf, D0P_IC, D0P_IR, &dm))
+            return fail(NSM_ERR_CUDA, "dec0p: TMA tensor map encoding failed");
+        const Dec0pArgs dp{p.d0p3.wpk, p.d0p1.wpk, p.d0ph.wpk, L0.dec3.b32, L0.dec1.b32, p.head.b32, b.y, H1, W1, H0, W0};
+        const int ptotal = ((W1 + 7) / 8) * ((H1 + 15) / 16) * nf;
+        {
+            NSM_PROF("dec0_fused", st);
+            launch_pdl(dec0p_kernel<T>, dim3(std::min(ptotal, num_sms())), dim3(D0P_THREADS), D0P_SMEM, st, dp, dm, ptotal);
+        }
+        static const bool ring = !getenv("NSM_DEC0_RING") || atoi(getenv("NSM_DEC0_RING")) != 0;   // 0: timing only
+        if (ring) {
+            const int items = 2 * ((W0 + 29) / 30 + (H0 - 2 + 29) / 30) * nf;
+            NSM_PROF("dec0_ring", st);
+            launch_pdl(dec0_ring_kernel<T>, dim3((items + 3) / 4), dim3(128), 0, st, (const T*)b.d1, H1, W1, H0, W0,
+                       (const RingW*)p.d0ring.wpk, b.y, nf);
+        }
+    } else {
         CUtensorMap dm;
         memset(&dm, 0, sizeof dm);
         if (!encode_nhwc_map4(b.d1, std::is_same<T, __nv_bfloat16>::value, 16, H0 / 2, W0 / 2, nf, D0_LC, D0_LR, &dm, 1))
@@ -2160,6 +2580,17 @@ nsm_status pack_f16(Plan& p, std::vector<char>& blob, size_t& offset_out) {
             c.k = k;
             c.w32 = w.data();
         };
+        RingW rwh{};
+        for (int co = 0; co < 16; ++co)
+            for (int ci = 0; ci < 16; ++ci)
+                for (int tap = 0; tap < 9; ++tap) rwh.w3[tap][ci][co] = d3.w32[(co * 16 + ci) * 9 + tap];
+        for (int i = 0; i < 256; ++i) rwh.w1[i & 15][i >> 4] = d1.w32[i];
+        for (int i = 0; i < 64; ++i) rwh.wh[i & 15][i >> 4] = p.head.w32[i];
+        for (int i = 0; i < 16; ++i) rwh.b[i] = d3.b32[i], rwh.b[16 + i] = d1.b32[i];
+        for (int i = 0; i < 4; ++i) rwh.b[32 + i] = p.head.b32[i];
+        p.d0ring.cin = p.d0ring.cout = 16;
+        p.d0ring.k = 1;
+        items.push_back(Item{&p.d0ring, std::vector<char>((const char*)&rwh, (const char*)&rwh + sizeof rwh)});
         setc(p.d0p3, w3p, 64, 16, 3);
         setc(p.d0p1, w1d, 64, 64, 1);
         setc(p.d0ph, whd, 16, 64, 1);
