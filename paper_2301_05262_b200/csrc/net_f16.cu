@@ -1278,8 +1278,17 @@ __device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t
 //                     NHWC store and/or 2x2 average pool
 // All hand-offs are mbarriers (tcgen05.commit on the tensor-core side), so
 // conv3 of tile k+1 overlaps the epilogues of tile k.
+// MMA issuer warps: SRC_UP kernels (up to 72 conv3 UMMAs per tile) issue each
+// M-block's conv3 from its own warp and conv1 from another, since one thread
+// issues a UMMA only every ~50-70 cycles; SRC_TENSOR kernels keep one issuer
+// (their epilogues need the registers).
+template <int SRC, int NB>
+__host__ __device__ constexpr int lv_mma_warps() { return SRC == SRC_UP ? NB + 1 : 1; }
+template <int SRC, int NB, int NPW>
+__host__ __device__ constexpr int lv_threads() { return (NPW + 8 + lv_mma_warps<SRC, NB>() + (SRC == SRC_UP)) * 32; }
+
 template <typename T, int CIN, int C3, int C1, int SRC, int DST, int NB, int NIN, int NMID, int NPW>
-__global__ void __launch_bounds__((NPW + 9 + (SRC == SRC_UP)) * 32, 1) level_kernel(const __grid_constant__ LevelArgs a,
+__global__ void __launch_bounds__(lv_threads<SRC, NB, NPW>(), 1) level_kernel(const __grid_constant__ LevelArgs a,
                                                                    const __grid_constant__ CUtensorMap tin,
                                                                    const __grid_constant__ CUtensorMap tlo,
                                                                    int total) {
@@ -1303,7 +1312,10 @@ __global__ void __launch_bounds__((NPW + 9 + (SRC == SRC_UP)) * 32, 1) level_ker
     float* sb3 = reinterpret_cast<float*>(smem + G::OFF_B);
     float* sb1 = sb3 + C3;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    constexpr int EW0 = NPW, MW = NPW + 8;          // first of 8 epilogue warps, MMA warp
+    constexpr int EW0 = NPW, MW = NPW + 8;          // first of 8 epilogue warps, first MMA warp
+    constexpr int NMW = lv_mma_warps<SRC, NB>();
+    constexpr bool kSplit = NMW > 1;                // MW + b: conv3 of M-block b; MW + NB: conv1
+    constexpr int TW_ = MW + NMW;                   // SRC_UP: TMA warp
     constexpr int NPT = NPW * 32;
     const uint32_t sbase = smem_u32(smem);
     const int ntx = (a.W + G::TW - 1) / G::TW, nty = (a.H + G::TH - 1) / G::TH;
@@ -1323,10 +1335,10 @@ __global__ void __launch_bounds__((NPW + 9 + (SRC == SRC_UP)) * 32, 1) level_ker
     if (tid == 0) {
         for (int i = 0; i < NIN; ++i) {
             mbar_init(&in_full[i], SRC == SRC_TENSOR ? 1 : NPT);
-            mbar_init(&in_empty[i], 1);
+            mbar_init(&in_empty[i], kSplit ? NB : 1);          // one commit per conv3 issuer
         }
         for (int i = 0; i < 2; ++i) {
-            mbar_init(&a3_full[i], 1);
+            mbar_init(&a3_full[i], kSplit ? NB : 1);
             mbar_init(&a3_empty[i], 256);
             mbar_init(&mid_full[i], 256);
             mbar_init(&mid_empty[i], 1);
@@ -1542,7 +1554,7 @@ __global__ void __launch_bounds__((NPW + 9 + (SRC == SRC_UP)) * 32, 1) level_ker
                 if (tid == 0) tr(k, 1);
             }
         }
-    } else if (SRC == SRC_UP && warp == MW + 1) {
+    } else if (SRC == SRC_UP && warp == TW_) {
         // ------------------------------------------------------------ TMA warp (SRC_UP, in-place skip)
         if (!G::STAGED && lane == 0) {
             for (int k = 0; k < mytiles; ++k) {
@@ -1559,8 +1571,9 @@ __global__ void __launch_bounds__((NPW + 9 + (SRC == SRC_UP)) * 32, 1) level_ker
                 tma_load_4d(sbase + G::OFF_LO + (k & 1) * G::LOB, &tlo, 0, x0 / 2 - 1, y0 / 2 - 1, f, &lof[k & 1]);
             }
         }
-    } else if (warp == MW) {
-        // ------------------------------------------------------------ MMA issuer
+    } else if (warp >= MW && warp < MW + NMW) {
+        // ------------------------------------------------------------ MMA issuer(s)
+        const int mi = warp - MW;                   // kSplit: M-block of this conv3 issuer, NB = conv1
         if (lane == 0) {
             constexpr uint32_t idesc3 = umma_idesc(128, C3, Elem<T>::kUmmaFmt);
             constexpr uint32_t idesc1 = umma_idesc(128, C1, Elem<T>::kUmmaFmt);
@@ -1589,7 +1602,9 @@ __global__ void __launch_bounds__((NPW + 9 + (SRC == SRC_UP)) * 32, 1) level_ker
                 tr(j, 3);
             };
             mbar_wait(wbar, 0);
-            for (int k = 0; k < mytiles; ++k) {
+            if (kSplit && mi == NB) {
+                for (int j = 0; j < mytiles; ++j) conv1(j);
+            } else for (int k = 0; k < mytiles; ++k) {
                 const int s = k % NIN, a3 = k & 1;
                 mbar_wait(&in_full[s], (k / NIN) & 1);
                 mbar_wait(&a3_empty[a3], ((k >> 1) & 1) ^ 1);
@@ -1614,6 +1629,7 @@ __global__ void __launch_bounds__((NPW + 9 + (SRC == SRC_UP)) * 32, 1) level_ker
                         for (int b = 0; b < NB; ++b)
 #pragma unroll
                             for (int kk = 0; kk < G::KK; ++kk) {
+                                if (kSplit && b != mi) continue;
                                 // M-block b: 16 output rows x 8 px; core matrix i = output row i
                                 const uint64_t da = dat + (uint64_t)(((2 * kk) * G::PIN + b * 8 * 16) >> 4);
                                 const uint64_t db = dbt + (uint64_t)((kk * C3 * 32) >> 4);
@@ -1624,9 +1640,9 @@ __global__ void __launch_bounds__((NPW + 9 + (SRC == SRC_UP)) * 32, 1) level_ker
                 if (SRC == SRC_TENSOR) tr(k, 1);            // conv3 UMMAs issued (SRC_TENSOR: slot 1 is free)
                 umma_commit(&in_empty[s]);
                 umma_commit(&a3_full[a3]);
-                if (k >= 1) conv1(k - 1);
+                if (!kSplit && k >= 1) conv1(k - 1);
             }
-            if (mytiles > 0) conv1(mytiles - 1);
+            if (!kSplit && mytiles > 0) conv1(mytiles - 1);
         }
     } else {
         // ------------------------------------------------------------ epilogue
@@ -1800,28 +1816,33 @@ __global__ void __launch_bounds__((NPW + 9 + (SRC == SRC_UP)) * 32, 1) level_ker
 // The outer ring of level-0 pixels (rows 0 and H0-1, columns 0 and W0-1):
 // dec3 (zero padding of the up2 image), dec1 and the head in fp32, straight
 // from D1 (autodiff.py:258-287; network.py:199-205): dec0_ring_kernel runs
-// after dec0p_kernel and overwrites these pixels.  A warp takes a run of 30
-// consecutive pixels of one side (lanes 1-30; lanes 0 and 31 are the halo):
-// every lane computes the up2
-// values of its position on the two image lines the side's taps touch (16
-// independent D1 loads), the neighbouring taps come from the adjacent lanes
-// by shuffles, and all lanes use the same tap's weights at the same time, so
-// the weight loads are shared-memory broadcasts.
+// after dec0p_kernel and overwrites these pixels.  A run is 30 consecutive
+// pixels of one side (lanes 1-30; lanes 0 and 31 are the halo): every lane
+// computes the up2 values of its position on the two image lines the side's
+// taps touch (16 independent D1 loads), the neighbouring taps come from the
+// adjacent lanes by shuffles, and all lanes use the same tap's weights at the
+// same time, so the weight loads are shared-memory broadcasts.
 struct RingW {              // packed once per plan (pack_f16)
     float w3[9][16][16];   // [tap][ci][co]
     float w1[16][16];      // [ci][co]
     float wh[16][4];       // [ci][c]
     float b[36];           // b3, b1, bh
 };
-// gwarp / nwarps: this warp's index among the ring warps of the grid
+// One run per 4-warp block: every warp builds the run's up2 lines (the D1
+// loads of warps 1-3 hit L1), warp w accumulates dec3 channels 4w..4w+3, and
+// dec1 / the head go through shared memory.
+struct RingScratch {
+    float h3[16][32];      // relu(dec3) [channel][lane]
+    float h1[16][32];      // relu(dec1)
+};
 template <typename T>
-__device__ __forceinline__ void ring_run(const RingW& rw, const T* __restrict__ d1p, int H1, int W1, int H0, int W0,
-                                         float* __restrict__ y, int nf, int gwarp, int nwarps) {
-    const int lane = threadIdx.x & 31;
+__device__ __forceinline__ void ring_run(const RingW& rw, RingScratch& sc, const T* __restrict__ d1p, int H1, int W1,
+                                         int H0, int W0, float* __restrict__ y, int nf) {
+    const int lane = threadIdx.x & 31, wq = threadIdx.x >> 5;     // warp = channel quarter
     const int Wp = W1 + 2;
     const int64_t plane = (int64_t)H0 * W0;
     const int runs_h = (W0 + 29) / 30, runs_v = (H0 - 2 + 29) / 30, per_frame = 2 * (runs_h + runs_v);
-    for (int item = gwarp; item < per_frame * nf; item += nwarps) {
+    for (int item = blockIdx.x; item < per_frame * nf; item += gridDim.x) {
         const int f = item / per_frame;
         int r = item - f * per_frame, side, run;
         if (r < 2 * runs_h) side = r / runs_h, run = r % runs_h;              // 0 top, 1 bottom
@@ -1866,10 +1887,10 @@ __device__ __forceinline__ void ring_run(const RingW& rw, const T* __restrict__ 
                 }
             }
         }
-        // dec3 over the 6 in-image taps: line k, neighbour d along the side
-        float acc[16];
+        // dec3 channels 4wq..4wq+3 over the 6 in-image taps: line k, neighbour d
+        float acc[4];
 #pragma unroll
-        for (int co = 0; co < 16; ++co) acc[co] = rw.b[co];
+        for (int c = 0; c < 4; ++c) acc[c] = rw.b[4 * wq + c];
 #pragma unroll
         for (int k = 0; k < 2; ++k) {
             const int across = (side == 0 || side == 2) ? k + 1 : k;      // dy (horiz) / dx (vert) of line k
@@ -1880,49 +1901,40 @@ __device__ __forceinline__ void ring_run(const RingW& rw, const T* __restrict__ 
                 for (int ci = 0; ci < 16; ++ci) {
                     const float v = d == 0 ? u[k][ci] : d < 0 ? __shfl_up_sync(0xffffffffu, u[k][ci], 1)
                                                               : __shfl_down_sync(0xffffffffu, u[k][ci], 1);
-                    const float4* wr = reinterpret_cast<const float4*>(&rw.w3[tap][ci][0]);
-#pragma unroll
-                    for (int c4 = 0; c4 < 4; ++c4) {
-                        const float4 w = wr[c4];
-                        acc[4 * c4] += w.x * v;
-                        acc[4 * c4 + 1] += w.y * v;
-                        acc[4 * c4 + 2] += w.z * v;
-                        acc[4 * c4 + 3] += w.w * v;
-                    }
+                    const float4 w = *reinterpret_cast<const float4*>(&rw.w3[tap][ci][4 * wq]);
+                    acc[0] += w.x * v;
+                    acc[1] += w.y * v;
+                    acc[2] += w.z * v;
+                    acc[3] += w.w * v;
                 }
             }
         }
-        float hid[16];
 #pragma unroll
-        for (int co = 0; co < 16; ++co) hid[co] = rw.b[16 + co];
+        for (int c = 0; c < 4; ++c) sc.h3[4 * wq + c][lane] = fmaxf(acc[c], 0.f);
+        __syncthreads();
+        float hid[4];
 #pragma unroll
-        for (int ci = 0; ci < 16; ++ci) {
-            const float a0 = fmaxf(acc[ci], 0.f);
-            const float4* wr = reinterpret_cast<const float4*>(&rw.w1[ci][0]);
-#pragma unroll
-            for (int c4 = 0; c4 < 4; ++c4) {
-                const float4 w = wr[c4];
-                hid[4 * c4] += w.x * a0;
-                hid[4 * c4 + 1] += w.y * a0;
-                hid[4 * c4 + 2] += w.z * a0;
-                hid[4 * c4 + 3] += w.w * a0;
-            }
-        }
-        float o[4] = {rw.b[32], rw.b[33], rw.b[34], rw.b[35]};
+        for (int c = 0; c < 4; ++c) hid[c] = rw.b[16 + 4 * wq + c];
 #pragma unroll
         for (int ci = 0; ci < 16; ++ci) {
-            const float hv = fmaxf(hid[ci], 0.f);
-            const float4 w = *reinterpret_cast<const float4*>(&rw.wh[ci][0]);
-            o[0] += w.x * hv;
-            o[1] += w.y * hv;
-            o[2] += w.z * hv;
-            o[3] += w.w * hv;
+            const float a0 = sc.h3[ci][lane];
+            const float4 w = *reinterpret_cast<const float4*>(&rw.w1[ci][4 * wq]);
+            hid[0] += w.x * a0;
+            hid[1] += w.y * a0;
+            hid[2] += w.z * a0;
+            hid[3] += w.w * a0;
         }
+#pragma unroll
+        for (int c = 0; c < 4; ++c) sc.h1[4 * wq + c][lane] = fmaxf(hid[c], 0.f);
+        __syncthreads();
+        float o = rw.b[32 + wq];                                        // head channel wq
+#pragma unroll
+        for (int ci = 0; ci < 16; ++ci) o += rw.wh[ci][wq] * sc.h1[ci][lane];
         if (owned) {
             const int R = horiz ? (side == 0 ? 0 : H0 - 1) : sp, C = horiz ? sp : (side == 2 ? 0 : W0 - 1);
-#pragma unroll
-            for (int c = 0; c < 4; ++c) y[((int64_t)f * 4 + c) * plane + (int64_t)R * W0 + C] = o[c];
+            y[((int64_t)f * 4 + wq) * plane + (int64_t)R * W0 + C] = o;
         }
+        __syncthreads();                                                // sc reused by the next run
     }
 }
 
@@ -2178,6 +2190,7 @@ template <typename T>
 __global__ void __launch_bounds__(128) dec0_ring_kernel(const T* __restrict__ d1p, int H1, int W1, int H0, int W0,
                                                         const RingW* __restrict__ wg, float* __restrict__ y, int nf) {
     __shared__ __align__(16) RingW rw;
+    __shared__ RingScratch sc;
     if (threadIdx.x == 0) pdl_trigger();
     constexpr int NV = (int)sizeof(RingW) / 16;
     static_assert(sizeof(RingW) % 16 == 0, "RingW is copied in 16-byte vectors");
@@ -2188,7 +2201,7 @@ __global__ void __launch_bounds__(128) dec0_ring_kernel(const T* __restrict__ d1
     }
     __syncthreads();
     pdl_wait();
-    ring_run<T>(rw, d1p, H1, W1, H0, W0, y, nf, blockIdx.x * 4 + (threadIdx.x >> 5), gridDim.x * 4);
+    ring_run<T>(rw, sc, d1p, H1, W1, H0, W0, y, nf);
 }
 
 // ------------------------------------------------------------------ host side
@@ -2289,7 +2302,7 @@ nsm_status launch_level(const LevelArgs& a, int nf, cudaStream_t st, const char*
     }
     const_cast<LevelArgs&>(a).trace = trace ? trace_buf : nullptr;
     NSM_PROF(name, st);
-    launch_pdl(k, dim3(grid), dim3((NPW + 9 + (SRC == SRC_UP)) * 32), G::SMEM, st, a, tin, tlo, total);
+    launch_pdl(k, dim3(grid), dim3(lv_threads<SRC, NB, NPW>()), G::SMEM, st, a, tin, tlo, total);
     if (trace) {   // experiments only: print CTA 0's timeline (us at 1.965 GHz) and stall the stream
         long long h[32 * 8];
         cudaMemcpyAsync(h, trace_buf, sizeof h, cudaMemcpyDeviceToHost, st);
@@ -2449,7 +2462,7 @@ nsm_status run_l0(const Plan& p, const Bufs& b, const Enc0Args& e0, const GbufMa
         if (ring) {
             const int items = 2 * ((W0 + 29) / 30 + (H0 - 2 + 29) / 30) * nf;
             NSM_PROF("dec0_ring", st);
-            launch_pdl(dec0_ring_kernel<T>, dim3((items + 3) / 4), dim3(128), 0, st, (const T*)b.d1, H1, W1, H0, W0,
+            launch_pdl(dec0_ring_kernel<T>, dim3(std::min(items, 4 * num_sms())), dim3(128), 0, st, (const T*)b.d1, H1, W1, H0, W0,
                        (const RingW*)p.d0ring.wpk, b.y, nf);
         }
     } else {
