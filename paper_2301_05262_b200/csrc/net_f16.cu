@@ -5,7 +5,8 @@
 //
 //   enc0   features + space_to_depth + l0.enc3 + l0.enc1 + avg_pool2  (mma.sync)
 //   lv<>   l1 enc / l2 enc / l3 bottleneck / l2 dec / l1 dec          (tcgen05)
-//   dec0   up2 + l0.dec3 + l0.dec1 + head                              (mma.sync)
+//   dec0p  up2 + l0.dec3 + l0.dec1 + head, polyphase on the L1 grid    (tcgen05)
+//   ring   the same for the outer level-0 ring (zero padding), fp32    (CUDA cores)
 //   recon  bilinear(ch0) + depth_to_space(detail) + sigmoid, crop      (CUDA cores)
 //
 // Activations live in NHWC 16-bit tensors between kernels (L2-resident for

@@ -95,7 +95,8 @@ def full(path):
     return "\n".join(out), recs
 
 
-KMAP = {"enc0_kernel": "enc0_fused", "dec0_kernel": "dec0_fused", "recon_kernel": "recon"}
+KMAP = {"enc0_kernel": "enc0_fused", "dec0p_kernel": "dec0_fused", "dec0_ring_kernel": "dec0_ring",
+        "recon_kernel": "recon"}
 
 
 def traffic(path, frames_per_launch, out, source, workload="cfg4-1080p-soft-window8"):
