@@ -820,7 +820,7 @@ struct Dec0Args {
     const float* b3;
     const float* b1;
     const float* bh;
-    float* y;             // head output, 4 fp32 planes per frame: (N, 4, H0, W0)
+    __half* y;            // head output, 4 fp16 planes per frame: (N, 4, H0, W0)
     int dbg;              // experiments only: 1 skip upsample math, 2 skip convolutions
     TileDiv td;
 };
@@ -1063,7 +1063,7 @@ __global__ void __launch_bounds__(kL0Threads, 1) dec0_kernel(const __grid_consta
             if (a.dbg & 2) return;
             const int hw0 = a.H0 * a.W0;
             const bool full_w = tl.tx0 + sx + 16 <= a.W0;
-            float* ybase = a.y + ((int64_t)tl.f * 4 + 2 * t) * hw0 + (int64_t)(tl.ty0 + r0) * a.W0 + tl.tx0 + sx + g;
+            __half* ybase = a.y + ((int64_t)tl.f * 4 + 2 * t) * hw0 + (int64_t)(tl.ty0 + r0) * a.W0 + tl.tx0 + sx + g;
             conv3_strip16<T, 8>(smem_u32(buf), E0_PLANE, E0_IC, r0, sx, B3, bias3, [&](int oo, float (&acc)[2][4]) {
                 uint32_t a1[4], a2[4];
                 relu_pack_a<T>(acc, a1);
@@ -1078,18 +1078,18 @@ __global__ void __launch_bounds__(kL0Threads, 1) dec0_kernel(const __grid_consta
                 // head channels 2t, 2t+1 (t < 2) of pixels g, g+8: one 64-bit base
                 // per tile, 32-bit row offsets (planes and the +8 are immediates)
                 if (t < 2 && tl.ty0 + r0 + oo < a.H0) {
-                    float* yp = ybase + oo * a.W0;
+                    __half* yp = ybase + oo * a.W0;
                     if (full_w) {
-                        yp[0] = yh[0];
-                        yp[8] = yh[2];
-                        yp[hw0] = yh[1];
-                        yp[hw0 + 8] = yh[3];
+                        yp[0] = __float2half_rn(yh[0]);
+                        yp[8] = __float2half_rn(yh[2]);
+                        yp[hw0] = __float2half_rn(yh[1]);
+                        yp[hw0 + 8] = __float2half_rn(yh[3]);
                     } else {
 #pragma unroll
                         for (int hlf = 0; hlf < 2; ++hlf)
                             if (tl.tx0 + sx + g + 8 * hlf < a.W0) {
-                                yp[8 * hlf] = yh[2 * hlf];
-                                yp[hw0 + 8 * hlf] = yh[2 * hlf + 1];
+                                yp[8 * hlf] = __float2half_rn(yh[2 * hlf]);
+                                yp[hw0 + 8 * hlf] = __float2half_rn(yh[2 * hlf + 1]);
                             }
                     }
                 }
@@ -1103,17 +1103,19 @@ __global__ void __launch_bounds__(kL0Threads, 1) dec0_kernel(const __grid_consta
 // rows/cols Y-1..Y+1 with weights (1/4, 3/4); clamping the neighbour indices
 // reproduces the reference's edge clamp (_upsample_taps, autodiff.py:258-264).
 __device__ __forceinline__ float sigmoid_fast(float v) {
-    // stable logistic (autodiff.py:200-209): e = exp(-|v|) in (0, 1]
-    const float e = __expf(-fabsf(v));
-    const float r = __fdividef(1.f, 1.f + e);
-    return v >= 0.f ? r : e * r;
+    // logistic (autodiff.py:200-209) as 1/2 + tanh(v/2)/2: one MUFU.TANH
+    // (max relative error ~2^-11, saturating, so no overflow for large |v|)
+    float t;
+    asm("tanh.approx.f32 %0, %1;" : "=f"(t) : "f"(0.5f * v));
+    return fmaf(0.5f, t, 0.5f);
 }
 
 // Each thread reconstructs 4 consecutive level-0 pixels (8 x 2 outputs):
-// ch0 of rows Y-1..Y+1 at columns X0-1..X0+4 (float4 + 2 edge loads per
-// row), the 3 detail channels as float4, two 16-B rows of fp16 out.
+// ch0 of rows Y-1..Y+1 at columns X0-1..X0+4 (8-B + 2 edge loads per row),
+// the 3 detail channels as 8-B loads of the fp16 Y planes, two 16-B rows of
+// fp16 out.
 constexpr int kReconPx = 4;
-__global__ void __launch_bounds__(128) recon_kernel(const float* __restrict__ y, int H0, int W0, int h,
+__global__ void __launch_bounds__(128) recon_kernel(const __half* __restrict__ y, int H0, int W0, int h,
                                                      int w, int n, void* __restrict__ out, int f16) {
     if (threadIdx.x == 0) pdl_trigger();
     pdl_wait();
@@ -1122,24 +1124,28 @@ __global__ void __launch_bounds__(128) recon_kernel(const float* __restrict__ y,
     const int f = blockIdx.z;
     if (X0 >= W0) return;
     const int hw0 = H0 * W0;
-    const float* y0 = y + (int64_t)f * 4 * hw0;
+    const __half* y0 = y + (int64_t)f * 4 * hw0;
+    auto ld4 = [](const __half* p, float (&v)[4]) {    // 4 consecutive fp16 (8-B aligned)
+        const uint2 q = __ldg(reinterpret_cast<const uint2*>(p));
+        const float2 a = __half22float2(*reinterpret_cast<const __half2*>(&q.x));
+        const float2 b = __half22float2(*reinterpret_cast<const __half2*>(&q.y));
+        v[0] = a.x, v[1] = a.y, v[2] = b.x, v[3] = b.y;
+    };
     const int rows[3] = {max(Y - 1, 0), Y, min(Y + 1, H0 - 1)};
     const int xm = max(X0 - 1, 0), xp = min(X0 + kReconPx, W0 - 1);
     float r[3][kReconPx + 2];
 #pragma unroll
     for (int i = 0; i < 3; ++i) {
-        const float* row = y0 + rows[i] * W0;
-        const float4 c = __ldg(reinterpret_cast<const float4*>(row + X0));
-        r[i][0] = __ldg(row + xm);
-        r[i][1] = c.x, r[i][2] = c.y, r[i][3] = c.z, r[i][4] = c.w;
-        r[i][5] = __ldg(row + xp);
+        const __half* row = y0 + rows[i] * W0;
+        float c[4];
+        ld4(row + X0, c);
+        r[i][0] = __half2float(row[xm]);
+        r[i][1] = c[0], r[i][2] = c[1], r[i][3] = c[2], r[i][4] = c[3];
+        r[i][5] = __half2float(row[xp]);
     }
     float det[3][kReconPx];
 #pragma unroll
-    for (int c = 0; c < 3; ++c) {
-        const float4 v = __ldg(reinterpret_cast<const float4*>(y0 + (c + 1) * hw0 + Y * W0 + X0));
-        det[c][0] = v.x, det[c][1] = v.y, det[c][2] = v.z, det[c][3] = v.w;
-    }
+    for (int c = 0; c < 3; ++c) ld4(y0 + (c + 1) * hw0 + Y * W0 + X0, det[c]);
 #pragma unroll
     for (int sy = 0; sy < 2; ++sy) {
         const int oy = 2 * Y + sy;
@@ -1838,7 +1844,7 @@ struct RingScratch {
 };
 template <typename T>
 __device__ __forceinline__ void ring_run(const RingW& rw, RingScratch& sc, const T* __restrict__ d1p, int H1, int W1,
-                                         int H0, int W0, float* __restrict__ y, int nf) {
+                                         int H0, int W0, __half* __restrict__ y, int nf) {
     const int lane = threadIdx.x & 31, wq = threadIdx.x >> 5;     // warp = channel quarter
     const int Wp = W1 + 2;
     const int64_t plane = (int64_t)H0 * W0;
@@ -1933,7 +1939,7 @@ __device__ __forceinline__ void ring_run(const RingW& rw, RingScratch& sc, const
         for (int ci = 0; ci < 16; ++ci) o += rw.wh[ci][wq] * sc.h1[ci][lane];
         if (owned) {
             const int R = horiz ? (side == 0 ? 0 : H0 - 1) : sp, C = horiz ? sp : (side == 2 ? 0 : W0 - 1);
-            y[((int64_t)f * 4 + wq) * plane + (int64_t)R * W0 + C] = o;
+            y[((int64_t)f * 4 + wq) * plane + (int64_t)R * W0 + C] = __float2half_rn(o);
         }
         __syncthreads();                                                // sc reused by the next run
     }
@@ -1949,7 +1955,7 @@ __device__ __forceinline__ void ring_run(const RingW& rw, RingScratch& sc, const
 //   dec1   4 UMMAs  N = 64, K = 64   (A in TMEM, phase-block-diagonal B)
 //   head   4 UMMAs  N = 16, K = 64   (A in TMEM)
 // Epilogues: bias + ReLU + pack into TMEM (the next A), and the head's 16
-// values (4 phases x 4 channels) into the fp32 Y planes.  The zero padding
+// values (4 phases x 4 channels) into the fp16 Y planes.  The zero padding
 // of the level-0 conv differs from the replicate padding only on the outer
 // ring of level-0 pixels, which dec0_ring_kernel recomputes exactly.
 // Warps: 0 TMA, 1-4 conv3 epilogue, 5-8 dec1 epilogue, 9-12 head epilogue
@@ -1963,7 +1969,7 @@ struct Dec0pArgs {
     const float* b3;     // (16,)  l0.dec3 bias (replicated per phase)
     const float* b1;     // (16,)  l0.dec1 bias
     const float* bh;     // (4,)   head bias
-    float* y;            // (N, 4, H0, W0)
+    __half* y;           // (N, 4, H0, W0)
     int H1, W1, H0, W0;
 };
 constexpr int D0P_IR = 18, D0P_IC = 10, D0P_NIN = 4;
@@ -2169,13 +2175,13 @@ __global__ void __launch_bounds__(D0P_THREADS, 1) dec0p_kernel(const __grid_cons
                 for (int ph = 0; ph < 2; ++ph) {
                     const int oy = 2 * (y0 + pi) + ph;
                     if (oy < a.H0 && ox < a.W0) {
-                        float* yp = a.y + (int64_t)f * 4 * plane + (int64_t)oy * a.W0 + ox;
+                        __half* yp = a.y + (int64_t)f * 4 * plane + (int64_t)oy * a.W0 + ox;
 #pragma unroll
                         for (int c = 0; c < 4; ++c) {
                             const float v0 = __uint_as_float(r[ph * 8 + c]) + sbias[32 + c];
                             const float v1 = __uint_as_float(r[ph * 8 + 4 + c]) + sbias[32 + c];
-                            if (ox + 1 < a.W0) *reinterpret_cast<float2*>(yp + c * plane) = make_float2(v0, v1);
-                            else yp[c * plane] = v0;
+                            if (ox + 1 < a.W0) *reinterpret_cast<__half2*>(yp + c * plane) = __floats2half2_rn(v0, v1);
+                            else yp[c * plane] = __float2half_rn(v0);
                         }
                     }
                 }
@@ -2189,7 +2195,7 @@ __global__ void __launch_bounds__(D0P_THREADS, 1) dec0p_kernel(const __grid_cons
 
 template <typename T>
 __global__ void __launch_bounds__(128) dec0_ring_kernel(const T* __restrict__ d1p, int H1, int W1, int H0, int W0,
-                                                        const RingW* __restrict__ wg, float* __restrict__ y, int nf) {
+                                                        const RingW* __restrict__ wg, __half* __restrict__ y, int nf) {
     __shared__ __align__(16) RingW rw;
     __shared__ RingScratch sc;
     if (threadIdx.x == 0) pdl_trigger();
@@ -2323,7 +2329,7 @@ nsm_status launch_level(const LevelArgs& a, int nf, cudaStream_t st, const char*
 
 struct Bufs {
     void *p1, *s1, *p2, *s2, *p3, *b3, *d2, *d1;
-    float* y;
+    __half* y;
     size_t bytes;
 };
 
@@ -2344,7 +2350,7 @@ Bufs carve(void* ws, int nf, int H0, int W0, int es) {
     b.b3 = take((size_t)nf * H3 * W3 * 64 * es);
     b.d2 = take((size_t)nf * H2 * W2 * 32 * es);
     b.d1 = take((size_t)nf * (H1 + 2) * (W1 + 2) * 16 * es);   // replicate-padded (DST_PADREP)
-    b.y = (float*)take((size_t)nf * H0 * W0 * 16);
+    b.y = (__half*)take((size_t)nf * H0 * W0 * 8);
     b.bytes = (size_t)(p - (char*)ws);
     return b;
 }
@@ -2478,7 +2484,7 @@ nsm_status run_l0(const Plan& p, const Bufs& b, const Enc0Args& e0, const GbufMa
         static_assert(8 % kReconPx == 0, "W0 = round16(w) / 2 is a multiple of 8: float4 rows");
         dim3 g2((W0 / kReconPx + 127) / 128, H0, nf);
         NSM_PROF("recon", st);
-        launch_pdl(recon_kernel, g2, dim3(128), 0, st, (const float*)b.y, H0, W0, h, w, nf, y, y_f16);
+        launch_pdl(recon_kernel, g2, dim3(128), 0, st, (const __half*)b.y, H0, W0, h, w, nf, y, y_f16);
     }
     return NSM_OK;
 }
