@@ -1291,8 +1291,14 @@ __device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t
 // (their epilogues need the registers).
 template <int SRC, int NB>
 __host__ __device__ constexpr int lv_mma_warps() { return SRC == SRC_UP ? NB + 1 : 1; }
+// epilogue warps: 4 per TMEM lane quadrant where the warp budget allows
+// (the epilogue is latency-bound), else 2; they split the accumulator columns
+template <int SRC>
+__host__ __device__ constexpr int lv_epi_warps() { return SRC == SRC_TENSOR ? 16 : 8; }
 template <int SRC, int NB, int NPW>
-__host__ __device__ constexpr int lv_threads() { return (NPW + 8 + lv_mma_warps<SRC, NB>() + (SRC == SRC_UP)) * 32; }
+__host__ __device__ constexpr int lv_threads() {
+    return (NPW + lv_epi_warps<SRC>() + lv_mma_warps<SRC, NB>() + (SRC == SRC_UP)) * 32;
+}
 
 template <typename T, int CIN, int C3, int C1, int SRC, int DST, int NB, int NIN, int NMID, int NPW>
 __global__ void __launch_bounds__(lv_threads<SRC, NB, NPW>(), 1) level_kernel(const __grid_constant__ LevelArgs a,
@@ -1319,7 +1325,9 @@ __global__ void __launch_bounds__(lv_threads<SRC, NB, NPW>(), 1) level_kernel(co
     float* sb3 = reinterpret_cast<float*>(smem + G::OFF_B);
     float* sb1 = sb3 + C3;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    constexpr int EW0 = NPW, MW = NPW + 8;          // first of 8 epilogue warps, first MMA warp
+    constexpr int NE = lv_epi_warps<SRC>(), NG = NE / 4;   // epilogue warps, column groups
+    constexpr int EW0 = NPW, MW = NPW + NE;         // first epilogue warp, first MMA warp
+    static_assert((NB * C3 / 16) % NG == 0 && (NB * C1 / 16) % NG == 0, "column slices per epilogue warp");
     constexpr int NMW = lv_mma_warps<SRC, NB>();
     constexpr bool kSplit = NMW > 1;                // MW + b: conv3 of M-block b; MW + NB: conv1
     constexpr int TW_ = MW + NMW;                   // SRC_UP: TMA warp
@@ -1346,11 +1354,11 @@ __global__ void __launch_bounds__(lv_threads<SRC, NB, NPW>(), 1) level_kernel(co
         }
         for (int i = 0; i < 2; ++i) {
             mbar_init(&a3_full[i], kSplit ? NB : 1);
-            mbar_init(&a3_empty[i], 256);
-            mbar_init(&mid_full[i], 256);
+            mbar_init(&a3_empty[i], NE * 32);
+            mbar_init(&mid_full[i], NE * 32);
             mbar_init(&mid_empty[i], 1);
             mbar_init(&a1_full[i], 1);
-            mbar_init(&a1_empty[i], 256);
+            mbar_init(&a1_empty[i], NE * 32);
         }
         mbar_init(wbar, 1);
         for (int i = 0; i < 2; ++i) {
@@ -1654,7 +1662,7 @@ __global__ void __launch_bounds__(lv_threads<SRC, NB, NPW>(), 1) level_kernel(co
     } else {
         // ------------------------------------------------------------ epilogue
         const int q = warp & 3;                      // TMEM lane quadrant of this warp
-        const int grp = (warp - EW0) >> 2;           // two warps per quadrant split the columns
+        const int grp = (warp - EW0) >> 2;           // NG warps per quadrant split the columns
         const int m = q * 32 + lane;                 // M row == TMEM lane
         const int pi = m >> 3, pj = m & 7;           // pixel row / column inside an M-block
         const uint32_t tl = (uint32_t)(q * 32) << 16;
@@ -1667,13 +1675,13 @@ __global__ void __launch_bounds__(lv_threads<SRC, NB, NPW>(), 1) level_kernel(co
             uint8_t* mid = smem + G::OFF_MID + mm * G::MIDB;
             // this warp's NB * C3 / 32 accumulator slices: all TMEM loads in
             // flight before one wait (a wait per load serialised the epilogue)
-            constexpr int NIT1 = NB * (C3 / 16) / 2;
+            constexpr int NIT1 = NB * (C3 / 16) / NG;
             constexpr bool kPre = SRC == SRC_TENSOR;     // register room (no producer warps)
             uint32_t r1[kPre ? NIT1 : 1][16];
             if (kPre && !(a.dbg & 2)) {
 #pragma unroll
                 for (int i = 0; i < NIT1; ++i) {
-                    const int it = grp + 2 * i, b = it / (C3 / 16), c0 = (it % (C3 / 16)) * 16;
+                    const int it = grp + NG * i, b = it / (C3 / 16), c0 = (it % (C3 / 16)) * 16;
                     tmem_ld16_nw(tmem + tl + G::ACC3 + (a3 * NB + b) * C3 + c0, r1[i]);
                 }
                 tmem_ld_wait();
@@ -1681,7 +1689,7 @@ __global__ void __launch_bounds__(lv_threads<SRC, NB, NPW>(), 1) level_kernel(co
 #pragma unroll
             for (int i = 0; i < NIT1; ++i) {
                 if (a.dbg & 2) break;
-                const int it = grp + 2 * i, b = it / (C3 / 16), c0 = (it % (C3 / 16)) * 16;
+                const int it = grp + NG * i, b = it / (C3 / 16), c0 = (it % (C3 / 16)) * 16;
                 {
                     float v[16];
                     if constexpr (!kPre) {
@@ -1720,13 +1728,13 @@ __global__ void __launch_bounds__(lv_threads<SRC, NB, NPW>(), 1) level_kernel(co
             tc_fence_after();
             if (warp == EW0 && lane == 0) tr(j, 6);
             const int oy = y0 + pi;
-            constexpr int NIT2 = NB * (C1 / 16) / 2;
+            constexpr int NIT2 = NB * (C1 / 16) / NG;
             constexpr bool kPre = SRC == SRC_TENSOR;
             uint32_t r2[kPre ? NIT2 : 1][16];
             if (kPre && !(a.dbg & 2)) {
 #pragma unroll
                 for (int i = 0; i < NIT2; ++i) {
-                    const int it = grp + 2 * i, b = it / (C1 / 16), c0 = (it % (C1 / 16)) * 16;
+                    const int it = grp + NG * i, b = it / (C1 / 16), c0 = (it % (C1 / 16)) * 16;
                     tmem_ld16_nw(tmem + tl + G::ACC1 + (a1 * NB + b) * C1 + c0, r2[i]);
                 }
                 tmem_ld_wait();
@@ -1734,7 +1742,7 @@ __global__ void __launch_bounds__(lv_threads<SRC, NB, NPW>(), 1) level_kernel(co
 #pragma unroll
             for (int i = 0; i < NIT2; ++i) {
                 if (a.dbg & 2) break;
-                const int it = grp + 2 * i, b = it / (C1 / 16), c0 = (it % (C1 / 16)) * 16;
+                const int it = grp + NG * i, b = it / (C1 / 16), c0 = (it % (C1 / 16)) * 16;
                 const int ox = x0 + b * 8 + pj;
                 const bool inside = oy < a.H && ox < a.W;
                 {
