@@ -292,7 +292,6 @@ nsm_status nsm_plan_create(const nsm_net_config* cfg, int32_t n_tensors, const c
         rebase(p->d0p3);
         rebase(p->d0p1);
         rebase(p->d0ph);
-        rebase(p->d0ring);
     }
     *out_plan = reinterpret_cast<nsm_plan*>(p);
     return NSM_OK;

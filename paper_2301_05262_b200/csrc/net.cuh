@@ -36,7 +36,6 @@ struct Plan {
     // conv3(up2(x)) = 4 phase convolutions of x, stacked along N (4 x 16);
     // dec1 and the head as phase-block-diagonal 1x1 convs (K = 64)
     ConvW d0p3, d0p1, d0ph;
-    ConvW d0ring;                 // fp32 level-0 decoder block of dec0_ring_kernel (RingW, in wpk)
     int64_t n_params = 0;
     void* dev = nullptr;          // one allocation holding every tensor
     size_t dev_bytes = 0;

@@ -1828,131 +1828,6 @@ __global__ void __launch_bounds__(lv_threads<SRC, NB, NPW>(), 1) level_kernel(co
     if (warp == EW0) tmem_dealloc<G::TCOLS>(tmem);
 }
 
-// The outer ring of level-0 pixels (rows 0 and H0-1, columns 0 and W0-1):
-// dec3 (zero padding of the up2 image), dec1 and the head in fp32, straight
-// from D1 (autodiff.py:258-287; network.py:199-205): dec0_ring_kernel runs
-// after dec0p_kernel and overwrites these pixels.  A run is 30 consecutive
-// pixels of one side (lanes 1-30; lanes 0 and 31 are the halo): every lane
-// computes the up2 values of its position on the two image lines the side's
-// taps touch (16 independent D1 loads), the neighbouring taps come from the
-// adjacent lanes by shuffles, and all lanes use the same tap's weights at the
-// same time, so the weight loads are shared-memory broadcasts.
-struct RingW {              // packed once per plan (pack_f16)
-    float w3[9][16][16];   // [tap][ci][co]
-    float w1[16][16];      // [ci][co]
-    float wh[16][4];       // [ci][c]
-    float b[36];           // b3, b1, bh
-};
-// One run per 4-warp block: every warp builds the run's up2 lines (the D1
-// loads of warps 1-3 hit L1), warp w accumulates dec3 channels 4w..4w+3, and
-// dec1 / the head go through shared memory.
-struct RingScratch {
-    float h3[16][32];      // relu(dec3) [channel][lane]
-    float h1[16][32];      // relu(dec1)
-};
-template <typename T>
-__device__ __forceinline__ void ring_run(const RingW& rw, RingScratch& sc, const T* __restrict__ d1p, int H1, int W1,
-                                         int H0, int W0, __half* __restrict__ y, int nf) {
-    const int lane = threadIdx.x & 31, wq = threadIdx.x >> 5;     // warp = channel quarter
-    const int Wp = W1 + 2;
-    const int64_t plane = (int64_t)H0 * W0;
-    const int runs_h = (W0 + 29) / 30, runs_v = (H0 - 2 + 29) / 30, per_frame = 2 * (runs_h + runs_v);
-    for (int item = blockIdx.x; item < per_frame * nf; item += gridDim.x) {
-        const int f = item / per_frame;
-        int r = item - f * per_frame, side, run;
-        if (r < 2 * runs_h) side = r / runs_h, run = r % runs_h;              // 0 top, 1 bottom
-        else r -= 2 * runs_h, side = 2 + r / runs_v, run = r % runs_v;         // 2 left, 3 right
-        const bool horiz = side < 2;
-        // this lane's position along the side (a column, or a row in 1..H0-2)
-        const int sp = horiz ? run * 30 + lane - 1 : run * 30 + lane;
-        const int extent = horiz ? W0 : H0;
-        const bool owned = lane >= 1 && lane <= 30 && (horiz ? sp < W0 : sp <= H0 - 2);
-        const uint4* x = reinterpret_cast<const uint4*>(d1p + (int64_t)f * (H1 + 2) * Wp * 16);
-        // up2 of D1 at the two lines next to the side (0 outside the image)
-        float u[2][16];
-#pragma unroll
-        for (int k = 0; k < 2; ++k) {
-            const int line = side == 0 ? k : side == 1 ? H0 - 2 + k : side == 2 ? k : W0 - 2 + k;
-            const int rr = horiz ? line : sp, cc = horiz ? sp : line;
-            const float m = (sp >= 0 && sp < extent) ? 1.f : 0.f;
-            const float sy = fminf(fmaxf((rr + 0.5f) * 0.5f - 0.5f, 0.f), (float)(H1 - 1));
-            const float sx = fminf(fmaxf((cc + 0.5f) * 0.5f - 0.5f, 0.f), (float)(W1 - 1));
-            const int y0 = (int)sy, x0 = (int)sx;
-            const float wy = sy - y0, wx = sx - x0;
-            const int y1 = min(y0 + 1, H1 - 1), x1 = min(x0 + 1, W1 - 1);
-            uint4 q[8];
-#pragma unroll
-            for (int c = 0; c < 4; ++c) {
-                const int64_t o = ((int64_t)((c >> 1 ? y1 : y0) + 1) * Wp + ((c & 1 ? x1 : x0) + 1)) * 2;
-                q[2 * c] = __ldg(x + o);
-                q[2 * c + 1] = __ldg(x + o + 1);
-            }
-            const float cw[4] = {m * (1.f - wy) * (1.f - wx), m * (1.f - wy) * wx, m * wy * (1.f - wx), m * wy * wx};
-#pragma unroll
-            for (int e = 0; e < 16; ++e) u[k][e] = 0.f;
-#pragma unroll
-            for (int c = 0; c < 4; ++c) {
-                const uint32_t wv[8] = {q[2 * c].x, q[2 * c].y, q[2 * c].z, q[2 * c].w,
-                                        q[2 * c + 1].x, q[2 * c + 1].y, q[2 * c + 1].z, q[2 * c + 1].w};
-#pragma unroll
-                for (int e = 0; e < 8; ++e) {
-                    const float2 v = Elem<T>::unpack(wv[e]);
-                    u[k][2 * e] += cw[c] * v.x;
-                    u[k][2 * e + 1] += cw[c] * v.y;
-                }
-            }
-        }
-        // dec3 channels 4wq..4wq+3 over the 6 in-image taps: line k, neighbour d
-        float acc[4];
-#pragma unroll
-        for (int c = 0; c < 4; ++c) acc[c] = rw.b[4 * wq + c];
-#pragma unroll
-        for (int k = 0; k < 2; ++k) {
-            const int across = (side == 0 || side == 2) ? k + 1 : k;      // dy (horiz) / dx (vert) of line k
-#pragma unroll
-            for (int d = -1; d <= 1; ++d) {
-                const int tap = horiz ? across * 3 + d + 1 : (d + 1) * 3 + across;
-#pragma unroll
-                for (int ci = 0; ci < 16; ++ci) {
-                    const float v = d == 0 ? u[k][ci] : d < 0 ? __shfl_up_sync(0xffffffffu, u[k][ci], 1)
-                                                              : __shfl_down_sync(0xffffffffu, u[k][ci], 1);
-                    const float4 w = *reinterpret_cast<const float4*>(&rw.w3[tap][ci][4 * wq]);
-                    acc[0] += w.x * v;
-                    acc[1] += w.y * v;
-                    acc[2] += w.z * v;
-                    acc[3] += w.w * v;
-                }
-            }
-        }
-#pragma unroll
-        for (int c = 0; c < 4; ++c) sc.h3[4 * wq + c][lane] = fmaxf(acc[c], 0.f);
-        __syncthreads();
-        float hid[4];
-#pragma unroll
-        for (int c = 0; c < 4; ++c) hid[c] = rw.b[16 + 4 * wq + c];
-#pragma unroll
-        for (int ci = 0; ci < 16; ++ci) {
-            const float a0 = sc.h3[ci][lane];
-            const float4 w = *reinterpret_cast<const float4*>(&rw.w1[ci][4 * wq]);
-            hid[0] += w.x * a0;
-            hid[1] += w.y * a0;
-            hid[2] += w.z * a0;
-            hid[3] += w.w * a0;
-        }
-#pragma unroll
-        for (int c = 0; c < 4; ++c) sc.h1[4 * wq + c][lane] = fmaxf(hid[c], 0.f);
-        __syncthreads();
-        float o = rw.b[32 + wq];                                        // head channel wq
-#pragma unroll
-        for (int ci = 0; ci < 16; ++ci) o += rw.wh[ci][wq] * sc.h1[ci][lane];
-        if (owned) {
-            const int R = horiz ? (side == 0 ? 0 : H0 - 1) : sp, C = horiz ? sp : (side == 2 ? 0 : W0 - 1);
-            y[((int64_t)f * 4 + wq) * plane + (int64_t)R * W0 + C] = __float2half_rn(o);
-        }
-        __syncthreads();                                                // sc reused by the next run
-    }
-}
-
 // ------------------------------------------------------------- level 0 decoder, polyphase (tcgen05)
 // dec0 = head(relu(dec1(relu(conv3(up2(D1)))))) evaluated on the level-1
 // grid: up2 with an edge clamp is up2 of the replicate-padded D1 (written by
@@ -2201,22 +2076,156 @@ __global__ void __launch_bounds__(D0P_THREADS, 1) dec0p_kernel(const __grid_cons
     if (warp == 13) tmem_dealloc<512>(tmem);
 }
 
+// The outer ring of level-0 pixels (rows 0 and H0-1, columns 0 and W0-1),
+// where the level-0 conv's zero padding differs from dec0p's replicate
+// padding: l0.dec3 (zero padding of the up2 image), l0.dec1 and the head
+// straight from D1 (autodiff.py:258-287; network.py:199-205), overwriting
+// dec0p's values.  One warp per run of 30 pixels along one side: the up2
+// values of the two image lines the side's taps touch are staged in shared
+// memory for 34 positions (chunk-planar, 16-bit like every level-0 operand),
+// and the 6 in-image taps are m16n8k16 MMAs on ldmatrix views shifted by
+// -1, 0, +1 positions (the sliding window of conv3_strip16); dec1 and the
+// head reuse the accumulators as A fragments.  The taps outside the image
+// are simply not issued, which is the zero padding.
+constexpr int kRingPos = 34, kRingWarpBytes = 2 * 2 * kRingPos * 16;
 template <typename T>
 __global__ void __launch_bounds__(128) dec0_ring_kernel(const T* __restrict__ d1p, int H1, int W1, int H0, int W0,
-                                                        const RingW* __restrict__ wg, __half* __restrict__ y, int nf) {
-    __shared__ __align__(16) RingW rw;
-    __shared__ RingScratch sc;
+                                                        const uint2* __restrict__ wb3, const uint2* __restrict__ wb1,
+                                                        const uint2* __restrict__ wbh, const float* __restrict__ b3,
+                                                        const float* __restrict__ b1, const float* __restrict__ bh,
+                                                        __half* __restrict__ y, int nf) {
+    __shared__ __align__(128) uint8_t su[4 * kRingWarpBytes];
     if (threadIdx.x == 0) pdl_trigger();
-    constexpr int NV = (int)sizeof(RingW) / 16;
-    static_assert(sizeof(RingW) % 16 == 0, "RingW is copied in 16-byte vectors");
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    const int g = lane >> 2, t = lane & 3;
+    uint32_t B3[9][2][2], B1[2][2], BH[2];
+    float bias3[2][2], bias1[2][2], biash[2];
 #pragma unroll
-    for (int k = 0; k < (NV + 127) / 128; ++k) {
-        const int i = threadIdx.x + k * 128;
-        if (i < NV) reinterpret_cast<uint4*>(&rw)[i] = __ldg(reinterpret_cast<const uint4*>(wg) + i);
+    for (int tap = 0; tap < 9; ++tap)
+#pragma unroll
+        for (int n = 0; n < 2; ++n) {
+            const uint2 v = __ldg(wb3 + (tap * 2 + n) * 32 + lane);
+            B3[tap][n][0] = v.x;
+            B3[tap][n][1] = v.y;
+        }
+#pragma unroll
+    for (int n = 0; n < 2; ++n) {
+        const uint2 v = __ldg(wb1 + n * 32 + lane);
+        B1[n][0] = v.x;
+        B1[n][1] = v.y;
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+            bias3[n][e] = __ldg(b3 + n * 8 + 2 * t + e);
+            bias1[n][e] = __ldg(b1 + n * 8 + 2 * t + e);
+        }
     }
-    __syncthreads();
+    {
+        const uint2 v = __ldg(wbh + lane);
+        BH[0] = v.x;
+        BH[1] = v.y;
+        biash[0] = t < 2 ? __ldg(bh + 2 * t) : 0.f;
+        biash[1] = t < 2 ? __ldg(bh + 2 * t + 1) : 0.f;
+    }
     pdl_wait();
-    ring_run<T>(rw, sc, d1p, H1, W1, H0, W0, y, nf);
+    uint8_t* u = su + wib * kRingWarpBytes;               // [line][chunk][position] x 16 B
+    const uint32_t ub = smem_u32(u);
+    const int Wp = W1 + 2;
+    const int64_t plane = (int64_t)H0 * W0;
+    const int runs_h = (W0 + 29) / 30, runs_v = (H0 - 2 + 29) / 30, per_frame = 2 * (runs_h + runs_v);
+    const int nwarps = gridDim.x * 4;
+    for (int item = blockIdx.x * 4 + wib; item < per_frame * nf; item += nwarps) {
+        const int f = item / per_frame;
+        int r = item - f * per_frame, side, run;
+        if (r < 2 * runs_h) side = r / runs_h, run = r % runs_h;              // 0 top, 1 bottom
+        else r -= 2 * runs_h, side = 2 + r / runs_v, run = r % runs_v;         // 2 left, 3 right
+        const bool horiz = side < 2;
+        // output row m (0..31) is position p0 - 1 + m along the side (a column,
+        // or a row in 1..H0-2); staged position j is p0 - 2 + j
+        const int p0 = horiz ? run * 30 : run * 30 + 1;
+        const int extent = horiz ? W0 : H0;
+        const uint4* x = reinterpret_cast<const uint4*>(d1p + (int64_t)f * (H1 + 2) * Wp * 16);
+        __syncwarp();                                    // the previous run's ldmatrix reads are done
+        for (int it = lane; it < 2 * 2 * kRingPos; it += 32) {
+            const int j = it % kRingPos, kc = it / kRingPos, k = kc >> 1, c = kc & 1;
+            const int sp = p0 - 2 + j;
+            const int line = side == 0 ? k : side == 1 ? H0 - 2 + k : side == 2 ? k : W0 - 2 + k;
+            const int rr = horiz ? line : sp, cc = horiz ? sp : line;
+            uint4 q = make_uint4(0u, 0u, 0u, 0u);
+            if (sp >= 0 && sp < extent) {                // 0 outside the image: the conv's zero padding
+                const float sy = fminf(fmaxf((rr + 0.5f) * 0.5f - 0.5f, 0.f), (float)(H1 - 1));
+                const float sx = fminf(fmaxf((cc + 0.5f) * 0.5f - 0.5f, 0.f), (float)(W1 - 1));
+                const int y0 = (int)sy, x0 = (int)sx;
+                const float wy = sy - y0, wx = sx - x0;
+                const int y1 = min(y0 + 1, H1 - 1), x1 = min(x0 + 1, W1 - 1);
+                const float cw[4] = {(1.f - wy) * (1.f - wx), (1.f - wy) * wx, wy * (1.f - wx), wy * wx};
+                float v[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+                for (int cr = 0; cr < 4; ++cr) {
+                    const uint4 s4 = __ldg(x + ((int64_t)((cr >> 1 ? y1 : y0) + 1) * Wp + ((cr & 1 ? x1 : x0) + 1)) * 2 + c);
+                    const uint32_t w4[4] = {s4.x, s4.y, s4.z, s4.w};
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) {
+                        const float2 h2 = Elem<T>::unpack(w4[e]);
+                        v[2 * e] = fmaf(cw[cr], h2.x, v[2 * e]);
+                        v[2 * e + 1] = fmaf(cw[cr], h2.y, v[2 * e + 1]);
+                    }
+                }
+                q = make_uint4(Elem<T>::pack(v[0], v[1]), Elem<T>::pack(v[2], v[3]), Elem<T>::pack(v[4], v[5]),
+                               Elem<T>::pack(v[6], v[7]));
+            }
+            *reinterpret_cast<uint4*>(u + (kc * kRingPos + j) * 16) = q;
+        }
+        __syncwarp();
+        // A fragment rows: position m0 + row + d + 1 of line k (both chunks)
+        const int lm = lane >> 3, li = lane & 7;
+        const uint32_t a_off = ((lm >> 1) * kRingPos + li + 8 * (lm & 1)) * 16;
+#pragma unroll
+        for (int mt = 0; mt < 2; ++mt) {
+            float acc[2][4];
+            bool first = true;
+#pragma unroll
+            for (int k = 0; k < 2; ++k) {
+                const int across = (side == 0 || side == 2) ? k + 1 : k;      // dy (horiz) / dx (vert) of line k
+#pragma unroll
+                for (int d = -1; d <= 1; ++d) {
+                    const int tap = horiz ? across * 3 + d + 1 : (d + 1) * 3 + across;
+                    uint32_t A[4];
+                    ldsm_x4(ub + a_off + ((2 * k) * kRingPos + mt * 16 + d + 1) * 16, A);
+#pragma unroll
+                    for (int n = 0; n < 2; ++n) {
+                        if (first)
+                            mma16816_c<T>(acc[n], A, B3[tap][n][0], B3[tap][n][1], bias3[n][0], bias3[n][1],
+                                          bias3[n][0], bias3[n][1]);
+                        else
+                            mma16816<T>(acc[n], A, B3[tap][n][0], B3[tap][n][1]);
+                    }
+                    first = false;
+                }
+            }
+            uint32_t a1[4], a2[4];
+            relu_pack_a<T>(acc, a1);
+            float hv[2][4];
+#pragma unroll
+            for (int n = 0; n < 2; ++n)
+                mma16816_c<T>(hv[n], a1, B1[n][0], B1[n][1], bias1[n][0], bias1[n][1], bias1[n][0], bias1[n][1]);
+            relu_pack_a<T>(hv, a2);
+            float yh[4];
+            mma16816_c<T>(yh, a2, BH[0], BH[1], biash[0], biash[1], biash[0], biash[1]);
+            // head channels 2t, 2t+1 (t < 2) of rows g, g + 8
+            if (t < 2) {
+#pragma unroll
+                for (int hh = 0; hh < 2; ++hh) {
+                    const int m = mt * 16 + g + 8 * hh, sp = p0 - 1 + m;
+                    if (m >= 1 && m <= 30 && (horiz ? sp < W0 : sp <= H0 - 2)) {
+                        const int R = horiz ? (side == 0 ? 0 : H0 - 1) : sp, C = horiz ? sp : (side == 2 ? 0 : W0 - 1);
+                        __half* yp = y + ((int64_t)f * 4 + 2 * t) * plane + (int64_t)R * W0 + C;
+                        yp[0] = __float2half_rn(yh[2 * hh]);
+                        yp[plane] = __float2half_rn(yh[2 * hh + 1]);
+                    }
+                }
+            }
+        }
+    }
 }
 
 // ------------------------------------------------------------------ host side
@@ -2477,8 +2486,9 @@ nsm_status run_l0(const Plan& p, const Bufs& b, const Enc0Args& e0, const GbufMa
         if (ring) {
             const int items = 2 * ((W0 + 29) / 30 + (H0 - 2 + 29) / 30) * nf;
             NSM_PROF("dec0_ring", st);
-            launch_pdl(dec0_ring_kernel<T>, dim3(std::min(items, 4 * num_sms())), dim3(128), 0, st, (const T*)b.d1, H1, W1, H0, W0,
-                       (const RingW*)p.d0ring.wpk, b.y, nf);
+            launch_pdl(dec0_ring_kernel<T>, dim3(std::min((items + 3) / 4, 2 * num_sms())), dim3(128), 0, st, (const T*)b.d1,
+                       H1, W1, H0, W0, (const uint2*)L0.dec3.wpk, (const uint2*)L0.dec1.wpk, (const uint2*)p.head.wpk,
+                       L0.dec3.b32, L0.dec1.b32, p.head.b32, b.y, nf);
         }
     } else {
         CUtensorMap dm;
@@ -2608,17 +2618,6 @@ nsm_status pack_f16(Plan& p, std::vector<char>& blob, size_t& offset_out) {
             c.k = k;
             c.w32 = w.data();
         };
-        RingW rwh{};
-        for (int co = 0; co < 16; ++co)
-            for (int ci = 0; ci < 16; ++ci)
-                for (int tap = 0; tap < 9; ++tap) rwh.w3[tap][ci][co] = d3.w32[(co * 16 + ci) * 9 + tap];
-        for (int i = 0; i < 256; ++i) rwh.w1[i & 15][i >> 4] = d1.w32[i];
-        for (int i = 0; i < 64; ++i) rwh.wh[i & 15][i >> 4] = p.head.w32[i];
-        for (int i = 0; i < 16; ++i) rwh.b[i] = d3.b32[i], rwh.b[16 + i] = d1.b32[i];
-        for (int i = 0; i < 4; ++i) rwh.b[32 + i] = p.head.b32[i];
-        p.d0ring.cin = p.d0ring.cout = 16;
-        p.d0ring.k = 1;
-        items.push_back(Item{&p.d0ring, std::vector<char>((const char*)&rwh, (const char*)&rwh + sizeof rwh)});
         setc(p.d0p3, w3p, 64, 16, 3);
         setc(p.d0p1, w1d, 64, 64, 1);
         setc(p.d0ph, whd, 16, 64, 1);
