@@ -2228,6 +2228,15 @@ __global__ void __launch_bounds__(128) dec0_ring_kernel(const T* __restrict__ d1
     }
 }
 
+// first_bad[i] = INT64_MAX ("no frustum error"), PDL-chained so that enc0's
+// prologue overlaps it
+__global__ void fill_first_bad(int64_t* p, int n) {
+    pdl_trigger();
+    pdl_wait();
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) p[i] = INT64_MAX;
+}
+
 // ------------------------------------------------------------------ host side
 int num_sms() {
     static int n = 0;
@@ -2649,7 +2658,10 @@ nsm_status infer_f16(const Plan& p, const nsm_gbuffer* g, const float* sm, int64
                     (long long)sm_stride, nfmax);
     Bufs b = carve(ws, nfmax, H0, W0, 2);
     if (ws_bytes < b.bytes) return fail(NSM_ERR_ARG, "workspace too small (%zu < %zu)", ws_bytes, b.bytes);
-    launch_fill_i64(first_bad, n, INT64_MAX, st);
+    {
+        NSM_PROF("fill_i64", st);
+        launch_pdl(fill_first_bad, dim3((n + 127) / 128), dim3(128), 0, st, first_bad, n);
+    }
     for (int f0 = 0; f0 < n; f0 += chunk_frames()) {
         const int nf = std::min(chunk_frames(), n - f0);
         Enc0Args e{};
