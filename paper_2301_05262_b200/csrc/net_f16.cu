@@ -811,20 +811,6 @@ __global__ void __launch_bounds__(kSrc == 2 ? kE0Threads : kL0Threads, 1) enc0_k
     }
 }
 
-struct Dec0Args {
-    const void* x;        // D1: (N, H0/2, W0/2, 16)
-    int H0, W0;
-    const uint2* wb3;     // l0.dec3 [9][2][32]
-    const uint2* wb1;     // l0.dec1 [2][32]
-    const uint2* wbh;     // head [1][32] (n 4..7 zero)
-    const float* b3;
-    const float* b1;
-    const float* bh;
-    __half* y;            // head output, 4 fp16 planes per frame: (N, 4, H0, W0)
-    int dbg;              // experiments only: 1 skip upsample math, 2 skip convolutions
-    TileDiv td;
-};
-
 // Bilinear 2x of an NHWC 16-bit tensor at one output pixel, 8 channels
 // (bilinear_upsample2 + _upsample_taps, autodiff.py:258-274: rows then cols).
 template <typename T>
@@ -943,160 +929,6 @@ __device__ __forceinline__ uint4 add_packed(uint4 a, uint4 b) {
     return r;
 }
 
-// dec0 source staging: the D1 (level-1, 16 ch) pixels a level-0 tile's
-// up2 reads, (TH/2 + 2) x (TW/2 + 2), pixel-major, double-buffered by TMA.
-constexpr int D0_LR = E0_TH / 2 + 2, D0_LC = E0_TW / 2 + 2;
-constexpr int D0_STG = round128(D0_LR * D0_LC * 32);
-constexpr int DEC0_SMEM = 2 * E0_SMEM + 2 * D0_STG + 32;
-
-template <typename T>
-__global__ void __launch_bounds__(kL0Threads, 1) dec0_kernel(const __grid_constant__ Dec0Args a,
-                                                             const __grid_constant__ CUtensorMap tm, int total) {
-    const int H1 = a.H0 / 2, W1 = a.W0 / 2;
-    if (threadIdx.x == 0) pdl_trigger();
-    pdl_wait();
-    if (threadIdx.x < kL0Prod) {
-        extern __shared__ __align__(128) uint8_t smem[];
-        uint8_t* stg = smem + 2 * E0_SMEM;
-        uint64_t* full = reinterpret_cast<uint64_t*>(stg + 2 * D0_STG);
-        const int ptid = threadIdx.x;
-        const int mytiles = (int)blockIdx.x < total ? (total - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x : 0;
-        auto issue = [&](int k) {
-            const L0Tile tl = l0_tile(blockIdx.x + k * gridDim.x, a.td);
-            mbar_expect_tx(&full[k & 1], D0_LR * D0_LC * 32);
-            tma_load_4d(smem_u32(stg + (k & 1) * D0_STG), &tm, 0, tl.tx0 / 2 - 1, tl.ty0 / 2 - 1, tl.f, &full[k & 1]);
-        };
-        if (ptid == 0) {
-            mbar_init(&full[0], 1);
-            mbar_init(&full[1], 1);
-            asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-        }
-        nbar_sync(5, kL0Prod);
-        if (ptid == 0) {
-            if (mytiles > 0) issue(0);
-            if (mytiles > 1) issue(1);
-        }
-        for (int k = 0; k < mytiles; ++k) {
-            const L0Tile tl = l0_tile(blockIdx.x + k * gridDim.x, a.td);
-            const int sb = k & 1;
-            if (k >= 2) nbar_sync(3 + sb, kL0Threads);
-            uint8_t* buf = smem + sb * E0_SMEM;
-            mbar_wait(&full[sb], (k >> 1) & 1);
-            const uint8_t* lo = stg + sb * D0_STG;
-            const int ly0 = tl.ty0 / 2 - 1, lx0 = tl.tx0 / 2 - 1;
-            // up2(D1) over the halo'd tile (zero outside the frame: conv padding),
-            // one 2x2 output block per item: the block of D1 pixel (bi, bj) reads its
-            // 3x3 neighbourhood with fixed (1/4, 3/4) weights; clamping the source
-            // indices reproduces the reference's edge clamp (autodiff.py:258-264).
-            constexpr int BR = E0_IR / 2 + 1, BC = E0_IC / 2 + 1;     // 10 x 34 blocks
-            for (int it = ptid; it < ((a.dbg & 1) ? 0 : BR * BC * 2); it += kL0Prod) {
-                const int c = it & 1, blk = it >> 1;
-                const int bil = blk / BC, bjl = blk - bil * BC;
-                const int bi = ly0 + bil, bj = lx0 + bjl;          // D1 pixel of the block
-                int rs[3], cs[3];
-#pragma unroll
-                for (int u = 0; u < 3; ++u) {
-                    rs[u] = min(max(min(max(bi - 1 + u, 0), H1 - 1) - ly0, 0), D0_LR - 1);
-                    cs[u] = min(max(min(max(bj - 1 + u, 0), W1 - 1) - lx0, 0), D0_LC - 1);
-                }
-                uint4 qn[3][3], ob[4];
-#pragma unroll
-                for (int u = 0; u < 3; ++u)
-#pragma unroll
-                    for (int v = 0; v < 3; ++v)
-                        qn[u][v] = *reinterpret_cast<const uint4*>(lo + ((rs[v] * D0_LC + cs[u]) * 16 + c * 8) * 2);
-                up2_block<T>(qn, ob);
-#pragma unroll
-                for (int ab = 0; ab < 4; ++ab) {
-                    const int aa = ab >> 1, bb = ab & 1;
-                    const int oy = 2 * bi + aa, ox = 2 * bj + bb;        // level-0 pixel
-                    const int ti = oy - (tl.ty0 - 1), tj = ox - (tl.tx0 - 1);
-                    if (ti < 0 || ti >= E0_IR || tj < 0 || tj >= E0_IC) continue;
-                    const bool in = oy >= 0 && ox >= 0 && oy < a.H0 && ox < a.W0;
-                    const uint4 q = in ? ob[ab] : make_uint4(0u, 0u, 0u, 0u);
-                    *reinterpret_cast<uint4*>(buf + c * E0_PLANE + (ti * E0_IC + tj) * 16) = q;
-                }
-            }
-            nbar_sync(5, kL0Prod);                 // everyone is done with stage sb
-            if (ptid == 0 && k + 2 < mytiles) issue(k + 2);
-            nbar_arrive(1 + sb, kL0Threads);
-        }
-        return;
-    }
-    const int cw = (threadIdx.x - kL0Prod) >> 5;
-    const int lane = threadIdx.x & 31;
-    const int g = lane >> 2, t = lane & 3;
-    const int sx = (cw & 3) * 16, r0 = (cw >> 2) * 8;
-    uint32_t B3[9][2][2], B1[2][2], BH[2];
-    float bias3[2][2], bias1[2][2], biash[2];
-    {
-#pragma unroll
-        for (int tap = 0; tap < 9; ++tap)
-#pragma unroll
-            for (int n = 0; n < 2; ++n) {
-                const uint2 v = __ldg(a.wb3 + (tap * 2 + n) * 32 + lane);
-                B3[tap][n][0] = v.x;
-                B3[tap][n][1] = v.y;
-            }
-#pragma unroll
-        for (int n = 0; n < 2; ++n) {
-            const uint2 v = __ldg(a.wb1 + n * 32 + lane);
-            B1[n][0] = v.x;
-            B1[n][1] = v.y;
-        }
-        const uint2 v = __ldg(a.wbh + lane);
-        BH[0] = v.x;
-        BH[1] = v.y;
-#pragma unroll
-        for (int n = 0; n < 2; ++n)
-#pragma unroll
-            for (int e = 0; e < 2; ++e) {
-                bias3[n][e] = __ldg(a.b3 + n * 8 + 2 * t + e);
-                bias1[n][e] = __ldg(a.b1 + n * 8 + 2 * t + e);
-            }
-        biash[0] = t < 2 ? __ldg(a.bh + 2 * t) : 0.f;
-        biash[1] = t < 2 ? __ldg(a.bh + 2 * t + 1) : 0.f;
-    }
-    l0_consume_loop(total,
-        [&](uint8_t* buf, int tile) {
-            const L0Tile tl = l0_tile(tile, a.td);
-            if (a.dbg & 2) return;
-            const int hw0 = a.H0 * a.W0;
-            const bool full_w = tl.tx0 + sx + 16 <= a.W0;
-            __half* ybase = a.y + ((int64_t)tl.f * 4 + 2 * t) * hw0 + (int64_t)(tl.ty0 + r0) * a.W0 + tl.tx0 + sx + g;
-            conv3_strip16<T, 8>(smem_u32(buf), E0_PLANE, E0_IC, r0, sx, B3, bias3, [&](int oo, float (&acc)[2][4]) {
-                uint32_t a1[4], a2[4];
-                relu_pack_a<T>(acc, a1);
-                float u[2][4];
-#pragma unroll
-                for (int n = 0; n < 2; ++n) {
-                    mma16816_c<T>(u[n], a1, B1[n][0], B1[n][1], bias1[n][0], bias1[n][1], bias1[n][0], bias1[n][1]);
-                }
-                relu_pack_a<T>(u, a2);
-                float yh[4];
-                mma16816_c<T>(yh, a2, BH[0], BH[1], biash[0], biash[1], biash[0], biash[1]);
-                // head channels 2t, 2t+1 (t < 2) of pixels g, g+8: one 64-bit base
-                // per tile, 32-bit row offsets (planes and the +8 are immediates)
-                if (t < 2 && tl.ty0 + r0 + oo < a.H0) {
-                    __half* yp = ybase + oo * a.W0;
-                    if (full_w) {
-                        yp[0] = __float2half_rn(yh[0]);
-                        yp[8] = __float2half_rn(yh[2]);
-                        yp[hw0] = __float2half_rn(yh[1]);
-                        yp[hw0 + 8] = __float2half_rn(yh[3]);
-                    } else {
-#pragma unroll
-                        for (int hlf = 0; hlf < 2; ++hlf)
-                            if (tl.tx0 + sx + g + 8 * hlf < a.W0) {
-                                yp[8 * hlf] = __float2half_rn(yh[2 * hlf]);
-                                yp[hw0 + 8 * hlf] = __float2half_rn(yh[2 * hlf + 1]);
-                            }
-                    }
-                }
-            });
-    });
-}
-
 // Head reconstruction (network.py:199-209) + sigmoid, cropped to (h, w):
 // out(2Y+sy, 2X+sx) = sigmoid(up2(y0) + [sy,sx != 0,0] * y_{2sy+sx}(Y, X)).
 // The 2x half-pixel bilinear of y0 at the 4 outputs of L0 pixel (Y, X) uses
@@ -1190,8 +1022,8 @@ __global__ void __launch_bounds__(128) recon_kernel(const __half* __restrict__ y
 
 // ------------------------------------------------------------- levels 1-3 (tcgen05)
 enum { SRC_TENSOR = 0, SRC_UP = 1 };
-// DST_PADREP: the stored tensor is (N, H + 2, W + 2, C1) with a one-pixel
-// border that replicates the edge (the polyphase level-0 decoder reads the
+// DST_PADREP: the stored tensor is chunk-planar (N, 2, H + 2, W + 2, 8)
+// (C1 = 16) with a one-pixel border that replicates the edge (the polyphase level-0 decoder reads the
 // edge-clamped upsampling source from it without bounds logic)
 enum { DST_STORE = 1, DST_POOL = 2, DST_PADREP = 4 };
 
@@ -1762,8 +1594,12 @@ __global__ void __launch_bounds__(lv_threads<SRC, NB, NPW>(), 1) level_kernel(co
 #pragma unroll
                             for (int e = 0; e < 8; ++e) qp[e] = Elem<T>::pack(v[2 * e], v[2 * e + 1]);
                             if constexpr (DST & DST_PADREP) {
+                                // chunk-planar (N, 2, H + 2, W + 2, 8): the consumer's TMA
+                                // box rows are then 10 contiguous pixels of one chunk
+                                static_assert(C1 == 16, "DST_PADREP stores one 16-channel slice as 2 chunk planes");
                                 const int wp = a.W + 2;
-                                T* fb = reinterpret_cast<T*>(a.out) + (int64_t)f * (a.H + 2) * wp * C1 + c0;
+                                const int64_t cpl = (int64_t)(a.H + 2) * wp * 8;      // one chunk plane
+                                T* fb = reinterpret_cast<T*>(a.out) + (int64_t)f * 2 * cpl;
                                 const int ys[2] = {oy + 1, oy == 0 ? 0 : (oy == a.H - 1 ? a.H + 1 : -1)};
                                 const int xs[2] = {ox + 1, ox == 0 ? 0 : (ox == a.W - 1 ? a.W + 1 : -1)};
 #pragma unroll
@@ -1771,9 +1607,9 @@ __global__ void __launch_bounds__(lv_threads<SRC, NB, NPW>(), 1) level_kernel(co
 #pragma unroll
                                     for (int ix = 0; ix < 2; ++ix)
                                         if (ys[iy] >= 0 && xs[ix] >= 0) {
-                                            uint4* dst = reinterpret_cast<uint4*>(fb + ((int64_t)ys[iy] * wp + xs[ix]) * C1);
-                                            dst[0] = qv[0];
-                                            dst[1] = qv[1];
+                                            T* px = fb + ((int64_t)ys[iy] * wp + xs[ix]) * 8;
+                                            *reinterpret_cast<uint4*>(px) = qv[0];
+                                            *reinterpret_cast<uint4*>(px + cpl) = qv[1];
                                         }
                             } else {
                                 uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<T*>(a.out) +
@@ -1940,7 +1776,7 @@ __global__ void __launch_bounds__(D0P_THREADS, 1) dec0p_kernel(const __grid_cons
                 tile_of(k, f, y0, x0);
                 mbar_expect_tx(&in_full[s], 2 * D0P_PIN);
                 // padded coordinates: real (y0 - 1, x0 - 1) is padded (y0, x0)
-                tma_load_5d(sbase + s * D0P_INB, &tin, 0, x0, y0, 0, f, &in_full[s]);
+                tma_load_3d(sbase + s * D0P_INB, &tin, 8 * x0, y0, 2 * f, &in_full[s]);   // both chunk planes
             }
         }
     } else if (warp >= 13) {
@@ -2143,7 +1979,9 @@ __global__ void __launch_bounds__(128) dec0_ring_kernel(const T* __restrict__ d1
         // or a row in 1..H0-2); staged position j is p0 - 2 + j
         const int p0 = horiz ? run * 30 : run * 30 + 1;
         const int extent = horiz ? W0 : H0;
-        const uint4* x = reinterpret_cast<const uint4*>(d1p + (int64_t)f * (H1 + 2) * Wp * 16);
+        // D1 is chunk-planar (N, 2, H1 + 2, W1 + 2, 8): one uint4 per pixel and chunk
+        const int64_t cpl = (int64_t)(H1 + 2) * Wp;
+        const uint4* x = reinterpret_cast<const uint4*>(d1p) + (int64_t)f * 2 * cpl;
         __syncwarp();                                    // the previous run's ldmatrix reads are done
         for (int it = lane; it < 2 * 2 * kRingPos; it += 32) {
             const int j = it % kRingPos, kc = it / kRingPos, k = kc >> 1, c = kc & 1;
@@ -2161,7 +1999,7 @@ __global__ void __launch_bounds__(128) dec0_ring_kernel(const T* __restrict__ d1
                 float v[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
 #pragma unroll
                 for (int cr = 0; cr < 4; ++cr) {
-                    const uint4 s4 = __ldg(x + ((int64_t)((cr >> 1 ? y1 : y0) + 1) * Wp + ((cr & 1 ? x1 : x0) + 1)) * 2 + c);
+                    const uint4 s4 = __ldg(x + (int64_t)c * cpl + (int64_t)((cr >> 1 ? y1 : y0) + 1) * Wp + ((cr & 1 ? x1 : x0) + 1));
                     const uint32_t w4[4] = {s4.x, s4.y, s4.z, s4.w};
 #pragma unroll
                     for (int e = 0; e < 4; ++e) {
@@ -2278,6 +2116,22 @@ bool encode_nhwc_map(const void* base, bool bf16, int C, int H, int W, int nf, i
                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+// 3-D view (x * 8 + channel, y, frame * 2 + chunk) of a chunk-planar 16-bit
+// tensor (N, 2, H, W, 8): a box row is box_w contiguous pixels of one chunk
+// (box_w * 16 B), not one 16-B pixel chunk as in encode_nhwc_map.
+bool encode_cplanar_map(const void* base, bool bf16, int H, int W, int nf, int box_w, int box_h, CUtensorMap* m) {
+    auto enc = tensor_map_encoder();
+    if (!enc || ((uintptr_t)base % 16)) return false;
+    const cuuint64_t dims[3] = {(cuuint64_t)W * 8, (cuuint64_t)H, (cuuint64_t)nf * 2};
+    const cuuint64_t strides[2] = {(cuuint64_t)W * 16, (cuuint64_t)H * W * 16};
+    const cuuint32_t box[3] = {(cuuint32_t)box_w * 8, (cuuint32_t)box_h, 2};
+    const cuuint32_t es[3] = {1, 1, 1};
+    return enc(m, bf16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 3,
+               const_cast<void*>(base), dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+               CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 // 4-D pixel-major view (C elems, x, y, frame) of an NHWC 16-bit tensor.
 bool encode_nhwc_map4(const void* base, bool bf16, int C, int H, int W, int nf, int box_w, int box_h,
                       CUtensorMap* m, int pad = 0) {
@@ -2375,7 +2229,7 @@ Bufs carve(void* ws, int nf, int H0, int W0, int es) {
     b.p3 = take((size_t)nf * H3 * W3 * 64 * es);
     b.b3 = take((size_t)nf * H3 * W3 * 64 * es);
     b.d2 = take((size_t)nf * H2 * W2 * 32 * es);
-    b.d1 = take((size_t)nf * (H1 + 2) * (W1 + 2) * 16 * es);   // replicate-padded (DST_PADREP)
+    b.d1 = take((size_t)nf * (H1 + 2) * (W1 + 2) * 16 * es);   // replicate-padded, chunk-planar (DST_PADREP)
     b.y = (__half*)take((size_t)nf * H0 * W0 * 8);
     b.bytes = (size_t)(p - (char*)ws);
     return b;
@@ -2447,7 +2301,6 @@ nsm_status run_l0(const Plan& p, const Bufs& b, const Enc0Args& e0, const GbufMa
         cudaFuncSetAttribute(enc0_kernel<T, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * E0_SMEM);
         cudaFuncSetAttribute(enc0_kernel<T, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * E0_SMEM);
         cudaFuncSetAttribute(enc0_kernel<T, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, ENC0_SMEM_TMA);
-        cudaFuncSetAttribute(dec0_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, DEC0_SMEM);
         // setmaxnreg.inc blocks until .dec released enough of the CTA's
         // launch allocation: refuse to launch a budget that could hang
         cudaFuncAttributes fa{};
@@ -2468,12 +2321,8 @@ nsm_status run_l0(const Plan& p, const Bufs& b, const Enc0Args& e0, const GbufMa
     nsm_status s = run_levels<T>(p, b, nf, H0, W0, st);
     if (s != NSM_OK) return s;
     const Level& L0 = p.lev[0];
-    static const int d0dbg = getenv("NSM_DEC0_DBG") ? atoi(getenv("NSM_DEC0_DBG")) : 0;
-    Dec0Args d{b.d1, H0, W0, (const uint2*)L0.dec3.wpk, (const uint2*)L0.dec1.wpk,
-               (const uint2*)p.head.wpk, L0.dec3.b32, L0.dec1.b32, p.head.b32, b.y, d0dbg,
-               tile_div(H0, W0)};
-    static const bool poly = !getenv("NSM_DEC0_POLY") || atoi(getenv("NSM_DEC0_POLY")) != 0;
-    if (poly && p.d0p3.present() && d0dbg == 0) {
+    if (!p.d0p3.present()) return fail(NSM_ERR_UNSUPPORTED, "dec0: polyphase level-0 decoder weights missing");
+    {
         // polyphase level-0 decoder on the level-1 grid + the exact outer ring
         const int H1 = H0 / 2, W1 = W0 / 2;
         static bool pattr = false;
@@ -2483,7 +2332,7 @@ nsm_status run_l0(const Plan& p, const Bufs& b, const Enc0Args& e0, const GbufMa
         }
         CUtensorMap dm;
         memset(&dm, 0, sizeof dm);
-        if (!encode_nhwc_map(b.d1, std::is_same<T, __nv_bfloat16>::value, 16, H1 + 2, W1 + 2, nf, D0P_IC, D0P_IR, &dm))
+        if (!encode_cplanar_map(b.d1, std::is_same<T, __nv_bfloat16>::value, H1 + 2, W1 + 2, nf, D0P_IC, D0P_IR, &dm))
             return fail(NSM_ERR_CUDA, "dec0p: TMA tensor map encoding failed");
         const Dec0pArgs dp{p.d0p3.wpk, p.d0p1.wpk, p.d0ph.wpk, L0.dec3.b32, L0.dec1.b32, p.head.b32, b.y, H1, W1, H0, W0};
         const int ptotal = ((W1 + 7) / 8) * ((H1 + 15) / 16) * nf;
@@ -2499,13 +2348,6 @@ nsm_status run_l0(const Plan& p, const Bufs& b, const Enc0Args& e0, const GbufMa
                        H1, W1, H0, W0, (const uint2*)L0.dec3.wpk, (const uint2*)L0.dec1.wpk, (const uint2*)p.head.wpk,
                        L0.dec3.b32, L0.dec1.b32, p.head.b32, b.y, nf);
         }
-    } else {
-        CUtensorMap dm;
-        memset(&dm, 0, sizeof dm);
-        if (!encode_nhwc_map4(b.d1, std::is_same<T, __nv_bfloat16>::value, 16, H0 / 2, W0 / 2, nf, D0_LC, D0_LR, &dm, 1))
-            return fail(NSM_ERR_CUDA, "dec0: TMA tensor map encoding failed");
-        NSM_PROF("dec0_fused", st);
-        launch_pdl(dec0_kernel<T>, dim3(pgrid), dim3(kL0Threads), DEC0_SMEM, st, d, dm, total);
     }
     {
         static_assert(8 % kReconPx == 0, "W0 = round16(w) / 2 is a multiple of 8: float4 rows");
