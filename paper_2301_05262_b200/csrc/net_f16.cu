@@ -531,6 +531,7 @@ __device__ __forceinline__ void produce_features_tma(const Enc0Args& a, const Gb
     const int nh = 2 * mytiles;
     if (ptid >= kE0Feat) {                         // TMA warp
         if (lane == 0) {
+            const uint64_t pol = l2_evict_first_policy();      // the G-buffer is read once
             for (int q = 0; q < nh; ++q) {
                 const int sidx = q & 1;
                 if (q >= 2) mbar_wait(&empty[sidx], ((q - 2) >> 1) & 1);
@@ -538,9 +539,9 @@ __device__ __forceinline__ void produce_features_tma(const Enc0Args& a, const Gb
                 const uint32_t dst = smem_u32(stage + sidx * ST_BYTES);
                 const int x = 2 * tl.tx0 - 4, y = 2 * tl.ty0 - 2 + ST_ROWS * (q & 1);
                 mbar_expect_tx(&full[sidx], ST_TX);
-                tma_load_3d(dst, &tm.d, x, y, tl.f, &full[sidx]);
-                tma_load_4d(dst + ST_OFF_N, &tm.n, x, y, 0, tl.f, &full[sidx]);
-                tma_load_4d(dst + ST_OFF_P, &tm.p, x, y, 0, tl.f, &full[sidx]);
+                tma_load_3d_stream(dst, &tm.d, x, y, tl.f, &full[sidx], pol);
+                tma_load_4d_stream(dst + ST_OFF_N, &tm.n, x, y, 0, tl.f, &full[sidx], pol);
+                tma_load_4d_stream(dst + ST_OFF_P, &tm.p, x, y, 0, tl.f, &full[sidx], pol);
             }
         }
         return;
@@ -1098,6 +1099,16 @@ __device__ __forceinline__ void tma_load_5d(uint32_t dst, const CUtensorMap* map
         : "memory");
 }
 
+__device__ __forceinline__ void tma_load_5d_stream(uint32_t dst, const CUtensorMap* map, int c0, int c1, int c2,
+                                                   int c3, int c4, uint64_t* bar, uint64_t pol) {
+    asm volatile(
+        "cp.async.bulk.tensor.5d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint [%0], "
+        "[%1, {%2, %3, %4, %5, %6}], [%7], %8;" ::"r"(dst),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4), "r"(smem_u32(bar)),
+        "l"(pol)
+        : "memory");
+}
+
 // 1-D bulk copy global -> SMEM (TMA engine, no tensor map), 16-B granules.
 __device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint64_t* bar) {
     asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
@@ -1223,7 +1234,7 @@ __global__ void __launch_bounds__(lv_threads<SRC, NB, NPW>(), 1) level_kernel(co
                     int f, y0, x0;
                     tile_of(k, f, y0, x0);
                     mbar_expect_tx(&in_full[s], G::TX_BYTES);
-                    tma_load_5d(sbase + s * G::INB, &tin, 0, x0 - 1, y0 - 1, 0, f, &in_full[s]);
+                    tma_load_5d_stream(sbase + s * G::INB, &tin, 0, x0 - 1, y0 - 1, 0, f, &in_full[s], l2_evict_first_policy());
                 }
             }
         } else if constexpr (G::STAGED) {
@@ -1246,15 +1257,18 @@ __global__ void __launch_bounds__(lv_threads<SRC, NB, NPW>(), 1) level_kernel(co
                 int f, y0, x0;
                 tile_of(k, f, y0, x0);
                 mbar_expect_tx(&skf[h], SKH);
-                tma_load_4d(sbase + G::OFF_SK + h * SKH, &tin, 0, x0 - 1, y0 - 1 + h * HR, f, &skf[h]);
+                tma_load_4d_stream(sbase + G::OFF_SK + h * SKH, &tin, 0, x0 - 1, y0 - 1 + h * HR, f, &skf[h], l2_evict_first_policy());
             };
             auto stage_lo = [&](int k) {                        // thread 0 only
                 int f, y0, x0;
                 tile_of(k, f, y0, x0);
                 const bool sk2 = kSk2 && a.skip;
                 mbar_expect_tx(&lof[k & 1], G::LOB + (sk2 ? G::SKB : 0));
-                tma_load_4d(sbase + G::OFF_LO + (k & 1) * G::LOB, &tlo, 0, x0 / 2 - 1, y0 / 2 - 1, f, &lof[k & 1]);
-                if (sk2) tma_load_4d(sbase + G::OFF_SK + (k & 1) * G::SKBR, &tin, 0, x0 - 1, y0 - 1, f, &lof[k & 1]);
+                tma_load_4d_stream(sbase + G::OFF_LO + (k & 1) * G::LOB, &tlo, 0, x0 / 2 - 1, y0 / 2 - 1, f, &lof[k & 1],
+                                   l2_evict_first_policy());
+                if (sk2)
+                    tma_load_4d_stream(sbase + G::OFF_SK + (k & 1) * G::SKBR, &tin, 0, x0 - 1, y0 - 1, f, &lof[k & 1],
+                                       l2_evict_first_policy());
             };
             if (tid == 0) {
                 if (mytiles > 0) {
@@ -1411,11 +1425,12 @@ __global__ void __launch_bounds__(lv_threads<SRC, NB, NPW>(), 1) level_kernel(co
                 if (a.skip) {
                     mbar_wait(&in_empty[s], ((k / NIN) & 1) ^ 1);           // conv3 of tile k - NIN done with in[s]
                     mbar_expect_tx(&skf[s], G::TX_BYTES);
-                    tma_load_5d(sbase + s * G::INB, &tin, 0, x0 - 1, y0 - 1, 0, f, &skf[s]);
+                    tma_load_5d_stream(sbase + s * G::INB, &tin, 0, x0 - 1, y0 - 1, 0, f, &skf[s], l2_evict_first_policy());
                 }
                 if (k >= 2) mbar_wait(&lo_empty[k & 1], ((k - 2) >> 1) & 1);
                 mbar_expect_tx(&lof[k & 1], G::LOB);
-                tma_load_4d(sbase + G::OFF_LO + (k & 1) * G::LOB, &tlo, 0, x0 / 2 - 1, y0 / 2 - 1, f, &lof[k & 1]);
+                tma_load_4d_stream(sbase + G::OFF_LO + (k & 1) * G::LOB, &tlo, 0, x0 / 2 - 1, y0 / 2 - 1, f, &lof[k & 1],
+                                   l2_evict_first_policy());
             }
         }
     } else if (warp >= MW && warp < MW + NMW) {
@@ -1776,7 +1791,7 @@ __global__ void __launch_bounds__(D0P_THREADS, 1) dec0p_kernel(const __grid_cons
                 tile_of(k, f, y0, x0);
                 mbar_expect_tx(&in_full[s], 2 * D0P_PIN);
                 // padded coordinates: real (y0 - 1, x0 - 1) is padded (y0, x0)
-                tma_load_3d(sbase + s * D0P_INB, &tin, 8 * x0, y0, 2 * f, &in_full[s]);   // both chunk planes
+                tma_load_3d_stream(sbase + s * D0P_INB, &tin, 8 * x0, y0, 2 * f, &in_full[s], l2_evict_first_policy());   // both chunk planes
             }
         }
     } else if (warp >= 13) {
