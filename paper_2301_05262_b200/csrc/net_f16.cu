@@ -2296,14 +2296,14 @@ bool encode_gbuf_maps(const GBufK& g, int nf, int h, int w, GbufMaps* m) {
     const cuuint64_t str4[3] = {(cuuint64_t)w * 4, (cuuint64_t)h * w * 4, (cuuint64_t)fs * 12};
     CUresult r = enc(&m->d, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<void*>(g.d), dim3_, str3, box3, es,
                      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-                     CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                     CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) return false;
     r = enc(&m->n, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, const_cast<void*>(g.normal), dim4, str4, box4, es,
-            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) return false;
     r = enc(&m->p, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, const_cast<void*>(g.position), dim4, str4, box4, es,
-            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     return r == CUDA_SUCCESS;
 }
