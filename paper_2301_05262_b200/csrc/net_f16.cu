@@ -700,7 +700,10 @@ __global__ void __launch_bounds__(kSrc == 2 ? kE0Threads : kL0Threads, 1) enc0_k
         }
         __syncthreads();
     }
-    pdl_wait();
+    // The G-buffer is an input, not the previous kernel's output: the TMA
+    // warp starts streaming it before the grid dependency resolves; every
+    // other thread waits (first_bad, the pooled output).
+    if (kSrc != 2 || threadIdx.x / 32 != kE0FeatWarps) pdl_wait();
     if (kSrc == 2) {
         static_assert(kE0ProdRegs == 72 && kE0MmaRegs == 112, "keep the asm immediates in sync");
         if (threadIdx.x < kProd) asm volatile("setmaxnreg.dec.sync.aligned.u32 72;");
