@@ -1630,10 +1630,9 @@ __global__ void __launch_bounds__(lv_threads<SRC, NB, NPW>(), 1) level_kernel(co
                                             *reinterpret_cast<uint4*>(px + cpl) = qv[1];
                                         }
                             } else {
-                                uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<T*>(a.out) +
-                                                                      (((int64_t)f * a.H + oy) * a.W + ox) * C1 + c0);
-                                dst[0] = qv[0];
-                                dst[1] = qv[1];
+                                // one 256-bit store: a full 32-B sector per lane
+                                st_global_256(reinterpret_cast<T*>(a.out) + (((int64_t)f * a.H + oy) * a.W + ox) * C1 + c0,
+                                              qv[0], qv[1]);
                             }
                         }
                     }

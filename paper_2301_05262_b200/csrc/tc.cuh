@@ -13,6 +13,14 @@
 
 namespace nsm {
 
+// 256-bit global store (sm_100: STG.E.ENL2.256), p 32-B aligned: one full
+// sector per lane instead of two half-sector 128-bit stores.
+__device__ __forceinline__ void st_global_256(void* p, const uint4& a, const uint4& b) {
+    asm volatile("st.global.v8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(p), "r"(a.x), "r"(a.y),
+                 "r"(a.z), "r"(a.w), "r"(b.x), "r"(b.y), "r"(b.z), "r"(b.w)
+                 : "memory");
+}
+
 template <typename T>
 struct Elem;
 template <>
