@@ -3,24 +3,37 @@
 
 Contract (one JSON line on rank 0):
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                    [--config 4] [--dtype fp16]
+                    [--config 4] [--dtype fp16] [--features 4|5]
 
 Workload (default ``--config 4``, BASELINE.json configs[3]): a temporal
 window of 8 consecutive 1920x1080 soft-shadow frames (spherical light of
 radius U[0.05, 0.5], 32 objects, 2048^2 shadow map, light / one object /
 camera moving 0.02 units per frame), fp16 activations with fp32
-accumulation, seeded random-init weights of the reference architecture
-(NetworkConfig(), 164,500 parameters). A step = the full hot path (feature
-pass + U-Net -> visibility) over the 8-frame batch. Every rank processes its
-own window (seed = rank): weak scaling, no collective on the data path; NCCL
-only gathers the per-rank timings (max over ranks). Inputs (G-buffer and
-shadow maps, ~600 MB per window) are larger than L2, so no flush is needed
-between steps. Synthetic data: procedural scenes rendered on the GPU by the
-repo's own producer kernels (the reference ships no dataset).
+accumulation, seeded random-init weights of the reference architecture.
+A step = the full hot path (feature pass + U-Net -> visibility) over the
+job's frames.
 
-``--impl reference`` times the reference algorithm on the host CPU cores
-(the numpy oracle port of shadowkit's assemble_features + forward; the
-reference package itself is not present on the GPU box), one frame per step.
+Multi-GPU (north_star: "shards the frame batch and temporal window across
+the GPUs"): one process per GPU.  ``--gpus N`` re-executes itself under
+torchrun when WORLD_SIZE is unset.  The job's frames (config 4: the 8-frame
+window; config 5: the 64 scenes) are split with ``shard.shard_bounds``
+(8/4/2/1 frames per rank at N = 1/2/4/8) -- strong scaling, no collective on
+the data path; NCCL gathers the per-rank step times (the job time is the
+max over ranks) and, with ``--gather``, the visibility frames in frame
+order.  ``--scaling weak`` gives every rank its own window instead
+(labelled).  Configs 2/3 are one frame: N > 1 runs replicas.
+
+Inputs (G-buffer + shadow maps, ~75 MB per 1080p frame) are larger than L2
+across a step, so no flush is needed.  Synthetic data: procedural scenes
+rendered on the GPU by the repo's producer kernels (the reference ships no
+dataset).
+
+``--impl reference`` times the reference's own CPU implementation --
+``shadowkit``'s ``raster.assemble_features`` + ``network.forward`` under
+``autodiff.no_grad()`` (``oracle/_ref``, staged by ``build()``; the numpy
+oracle port when it is absent) -- on the host cores, with inputs rendered
+on the CPU (``oracle.producer``) so that the process never loads the CUDA
+library.
 """
 
 from __future__ import annotations
@@ -38,46 +51,129 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-METRIC = "1080p soft-shadow frames/sec"
 UNIT = "frames/s"
 
 
 def metric_name(config):
-    return {2: "1080p hard-shadow frames/sec", 3: METRIC, 4: METRIC,
+    return {2: "1080p hard-shadow frames/sec", 3: "1080p soft-shadow frames/sec",
+            4: "1080p soft-shadow frames/sec",
             5: "4K hard/soft-shadow frames/sec (64-scene sweep)"}[config]
 
 
-def parse():
+def parse(argv=None):
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--config", type=int, default=4, choices=[2, 3, 4, 5])
-    ap.add_argument("--dtype", choices=["fp16", "bf16", "fp32"], default="fp16")
-    ap.add_argument("--frames", type=int, default=None, help="frames per rank (default: config)")
+    ap.add_argument("--dtype", choices=["fp16", "bf16", "fp32"], default=None,
+                    help="default: fp16 (configs 2-4), bf16 (config 5)")
+    ap.add_argument("--features", type=int, choices=[4, 5], default=None,
+                    help="input planes: 4 (reference layout) or 5 (+ blocker-search penumbra); "
+                         "default: 5 for the soft configs 3/4, 4 otherwise")
+    ap.add_argument("--frames", type=int, default=None, help="frames of the job (default: config)")
+    ap.add_argument("--scaling", choices=["strong", "weak"], default="strong",
+                    help="strong: shard the job's frames over the ranks; weak: one job per rank")
+    ap.add_argument("--cover", choices=["scene", "full"], default="scene",
+                    help="full: the fully covered camera variant as the main workload")
+    ap.add_argument("--gather", action="store_true", help="NCCL-gather the visibility to every rank")
     ap.add_argument("--no-graph", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-soak", action="store_true", help="skip the 1 s clock-sampling soak")
-    return ap.parse_args()
+    ap.add_argument("--no-variants", action="store_true", help="skip the fully covered variant")
+    a = ap.parse_args(argv)
+    if a.dtype is None:
+        a.dtype = "bf16" if a.config == 5 else "fp16"
+    if a.features is None:
+        a.features = 5 if a.config in (3, 4) else 4
+    return a
 
 
-def workload_name(config):
-    return {2: "cfg2-1080p-hard", 3: "cfg3-1080p-soft", 4: "cfg4-1080p-soft-window8",
-            5: "cfg5-4k-sweep"}[config]
+def workload_name(args):
+    base = {2: "cfg2-1080p-hard", 3: "cfg3-1080p-soft", 4: "cfg4-1080p-soft-window8",
+            5: "cfg5-4k-sweep"}[args.config]
+    if args.features == 5:
+        base += "-blocker"
+    if args.cover == "full":
+        base += "-fullcover"
+    return base
 
 
-def dist_setup():
+# --------------------------------------------------------------------------
+# job / sharding (pure host logic; tests/test_bench_shard.py drives it)
+# --------------------------------------------------------------------------
+
+def job_frames(args, seed=0):
+    """All frames of one job (every rank of a strong-scaling run sees the
+    same list and takes its shard)."""
+    from paper_2301_05262_b200 import scenes
+    if args.config in (2, 3):
+        frames = scenes.config_frames(args.config, seed=seed) * (args.frames or 1)
+    else:
+        frames = scenes.config_frames(args.config, seed=seed, n_frames=args.frames)
+    if args.cover == "full":
+        frames = [full_cover_frame(f) for f in frames]
+    return frames
+
+
+def full_cover_frame(f):
+    from paper_2301_05262_b200 import scenes
+    return scenes.full_cover(f, offset=np.asarray(f.camera.position) - np.asarray(scenes.CAMERA_POS))
+
+
+def rank_frames(args, rank, world):
+    """(frames this rank runs, [lo, hi) of the job, job size, scaling label)."""
+    from paper_2301_05262_b200 import shard
+    if args.scaling == "weak":
+        frames = job_frames(args, seed=shard.window_seed(rank))
+        return frames, (0, len(frames)), len(frames) * world, "weak"
+    frames = job_frames(args, seed=0)
+    if len(frames) < world:            # one-frame configs: replicas
+        return frames, (0, len(frames)), len(frames) * world, "weak"
+    lo, hi = shard.shard_bounds(len(frames), rank, world)
+    return frames[lo:hi], (lo, hi), len(frames), "strong"
+
+
+def env_guard():
+    """Refuse to time anything while experiment switches could be active."""
+    bad = sorted(k for k in os.environ if k.startswith("NSM_"))
+    if bad:
+        sys.exit(f"bench.py: refusing to run with {bad} set (experiment switches; unset them)")
+
+
+def maybe_spawn(args):
+    """--gpus N without a torchrun environment: re-exec under torchrun."""
+    if args.gpus <= 1 or "WORLD_SIZE" in os.environ:
+        return
+    import socket
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    sys.exit(subprocess.call(cmd))
+
+
+# --------------------------------------------------------------------------
+# distributed plumbing
+# --------------------------------------------------------------------------
+
+def dist_setup(backend=None):
     import torch
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    torch.cuda.set_device(local)
+    if backend is None:
+        backend = "nccl"
+    if backend == "nccl":
+        torch.cuda.set_device(local)
     if world > 1:
         import torch.distributed as dist
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        kw = {"device_id": torch.device("cuda", local)} if backend == "nccl" else {}
+        dist.init_process_group(backend, **kw)
     return rank, world, local
 
 
@@ -87,14 +183,16 @@ def barrier(world):
         dist.barrier()
 
 
-def allreduce_max(v, world):
-    if world == 1:
-        return v
+def gather_floats(vals, world, device):
+    """All-gather a small float vector from every rank -> (world, len)."""
     import torch
+    t = torch.tensor([float(v) for v in vals], dtype=torch.float64, device=device)
+    if world == 1:
+        return t[None].cpu().numpy()
     import torch.distributed as dist
-    t = torch.tensor([v], dtype=torch.float64, device="cuda")
-    dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    return float(t.item())
+    out = [torch.empty_like(t) for _ in range(world)]
+    dist.all_gather(out, t)
+    return torch.stack(out).cpu().numpy()
 
 
 class ClockSampler:
@@ -157,15 +255,15 @@ def peaks():
 
 
 # --------------------------------------------------------------------------
-# algorithmic cost models
+# algorithmic cost models ("roofline accounting")
 # --------------------------------------------------------------------------
 
 def covered_pixels(inputs):
     return int((inputs["d"] > 0).sum().item())
 
 
-def kernel_models(frames, inputs, cfg, dtype):
-    """Per-launch algorithmic bytes / flops of the kernels we can model."""
+def kernel_models(frames, inputs, cfg, dtype, features):
+    """Per-step algorithmic bytes / flops of the kernels we model."""
     n = len(frames)
     h, w = frames[0].camera.resolution
     px = n * h * w
@@ -185,6 +283,13 @@ def kernel_models(frames, inputs, cfg, dtype):
         "enc0_fused": {"bytes": 28 * px + 4 * cov + n * (l0 // 4) * 16 * act,
                        "flops": 2 * n * l0 * (16 * 16 * 9 + 16 * 16)},
     }
+    if features == 5:
+        # blocker pass: G-buffer in, one 4-B texel per covered pixel from
+        # HBM (the 16x16 window is served by SMEM / L1), 24 16-bit s2d
+        # channels per level-0 pixel out; enc0 reads them back
+        models["feat5_blocker"] = {"bytes": 28 * px + 4 * cov + n * l0 * 24 * act, "flops": 0}
+        models["enc0_s2d"] = {"bytes": n * l0 * 24 * act + n * (l0 // 4) * 16 * act,
+                              "flops": 2 * n * l0 * (16 * 20 * 9 + 16 * 16)}
     step_bytes = 28 * px + 4 * cov + px * act
     step_flops = 2.0 * n * hp * wp * sum(s["flops_per_pixel"] for s in st)
     return models, step_bytes, step_flops
@@ -210,29 +315,57 @@ def ncu_traffic(kernel, algo_bytes, frames_per_launch, workload):
 # our arm
 # --------------------------------------------------------------------------
 
+def make_plan(args):
+    from paper_2301_05262_b200 import network
+    cfg = network.NetworkConfig(in_channels=args.features)
+    w = network.init_weights(cfg, np.random.default_rng(np.random.SeedSequence([0, 0x11])))
+    return cfg, w, network.Plan(w, cfg, args.dtype)
+
+
+def time_steps(step, steps, world, soak=True, local=0):
+    """Device time per step (CUDA events on the launching stream, barrier +
+    synchronize on both sides), with clocks sampled under load."""
+    import torch
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        t_end = time.time() + (1.0 if soak else 0.0)      # ~1 s under load for nvidia-smi
+        while time.time() < t_end:
+            for _ in range(20):
+                step()
+            torch.cuda.synchronize()
+        barrier(world)
+        torch.cuda.synchronize()
+        e0.record()
+        for _ in range(steps):
+            step()
+        e1.record()
+        torch.cuda.synchronize()
+        barrier(world)
+    return e0.elapsed_time(e1) / steps, clk.summary()
+
+
 def run_ours(args):
     import torch
-    from paper_2301_05262_b200 import _lib, network, producer, scenes
+    from paper_2301_05262_b200 import _lib, producer
     from paper_2301_05262_b200.infer import ShadowInference
 
+    if _lib.experiment_build():
+        sys.exit("bench.py: libnsm.so is an experiment build (NSM_EXPERIMENTS); rebuild the release library")
     rank, world, local = dist_setup()
-    frames = scenes.config_frames(args.config, seed=rank, n_frames=args.frames)
-    if args.config in (2, 3):
-        frames = frames * (args.frames or 1)
+    dev = torch.device("cuda", local)
+    frames, (lo, hi), job_n, scaling = rank_frames(args, rank, world)
+    n = len(frames)
     inputs = producer.render_inputs(frames)
-    cfg = network.NetworkConfig()
-    w = network.init_weights(cfg, np.random.default_rng(np.random.SeedSequence([0, 0x11])))
-    plan = network.Plan(w, cfg, args.dtype)
+    cfg, w, plan = make_plan(args)
     out_dtype = "fp32" if args.dtype == "fp32" else "fp16"
     run = ShadowInference(plan, frames, out_dtype=out_dtype)
     run(inputs)                                  # validates frustum, warms up
     torch.cuda.synchronize()
-    n = len(frames)
     h, wd = frames[0].camera.resolution
 
     c0 = _lib.lib.nsm_launch_count()
     if args.no_graph:
-        step = lambda: run.launch(inputs)        # noqa: E731
+        step = lambda: run.launch(inputs, check=False)        # noqa: E731
         run.launch(inputs)
         per_step = _lib.lib.nsm_launch_count() - c0
     else:
@@ -242,110 +375,99 @@ def run_ours(args):
     for _ in range(max(args.warmup, 3)):
         step()
     torch.cuda.synchronize()
+    ms, clocks = time_steps(step, args.steps, world, soak=not args.no_soak, local=local)
+    per_rank = gather_floats([ms, n], world, dev)
+    ms_max = float(per_rank[:, 0].max())
+    value = job_n / (ms_max / 1e3)
 
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with ClockSampler(local) as clk:
-        # keep the GPU loaded ~1 s so nvidia-smi samples clocks under load
-        t_end = time.time() + (0.0 if args.no_soak else 1.0)
-        while time.time() < t_end:
-            for _ in range(20):
-                step()
-            torch.cuda.synchronize()
-        barrier(world)
-        torch.cuda.synchronize()
-        e0.record()
-        for _ in range(args.steps):
-            step()
-        e1.record()
-        torch.cuda.synchronize()
-        barrier(world)
-    ms = e0.elapsed_time(e1) / args.steps
-    ms_max = allreduce_max(ms, world)
-    frames_total = n * world
-    value = frames_total / (ms_max / 1e3)
+    gathered = None
+    if args.gather and world > 1:
+        from paper_2301_05262_b200 import shard
+        import torch.distributed as dist
+        full = shard.gather_frames(run.y, job_n if scaling == "strong" else n * world)
+        # every rank re-derives the rank-0 shard's checksum: frame order proof
+        gathered = {"frames": int(full.shape[0]), "checksum": float(full.double().sum().item()),
+                    "rank0_shard_equal": bool(torch.equal(full[:hi - lo], run.y) if rank == 0 else True)}
+        dist.barrier()
 
     # ---- per-kernel timing (eager, traced launches on the same stream) ----
     _lib.lib.nsm_profile_enable(1)
     _lib.profile_report()
     for _ in range(args.steps):
-        run.launch(inputs)
+        run.launch(inputs, check=False)
     torch.cuda.synchronize()
     prof = _lib.profile_report()
     _lib.lib.nsm_profile_enable(0)
-    models, step_bytes, step_flops = kernel_models(frames, inputs, cfg, args.dtype)
+    models, step_bytes, step_flops = kernel_models(frames, inputs, cfg, args.dtype, args.features)
     hbm, tfl, src = peaks()
     dom = max(prof, key=lambda k: prof[k][1]) if prof else None
     step_prof_ms = sum(v[1] for v in prof.values()) / max(args.steps, 1)
+    # the roofline names the dominant kernel we have an algorithmic model for
+    modelled = [k for k in prof if k in models]
+    rk = max(modelled, key=lambda k: prof[k][1]) if modelled else None
     roof = None
-    if dom in models:
-        cnt, tot = prof[dom]
+    if rk is not None:
+        cnt, tot = prof[rk]
+        launches_per_step = max(1, cnt // args.steps)
         avg_ms = tot / cnt
-        mb = models[dom]["bytes"] / max(1, cnt // args.steps)   # model is per step
+        mb = models[rk]["bytes"] / launches_per_step
         ach = mb / (avg_ms / 1e3) / 1e9
-        roof = {"bound": "hbm", "kernel": dom, "achieved": round(ach, 1), "peak": hbm,
+        roof = {"bound": "hbm", "kernel": rk, "achieved": round(ach, 1), "peak": hbm,
                 "unit": "GB/s", "frac": round(ach / hbm, 4),
-                "traffic": ncu_traffic(dom, mb, n // max(1, cnt // args.steps), workload_name(args.config)),
+                "traffic": ncu_traffic(rk, mb, n // launches_per_step, workload_name(args)),
                 "avg_launch_ms": round(avg_ms, 5), "peak_source": src,
-                "share_of_step": round(tot / args.steps / step_prof_ms, 3)}
-    elif dom is not None:
-        cnt, tot = prof[dom]
-        roof = {"bound": "hbm", "kernel": "step", "achieved":
-                round(step_bytes / (ms / 1e3) / 1e9, 1), "peak": hbm, "unit": "GB/s",
-                "frac": round(step_bytes / (ms / 1e3) / 1e9 / hbm, 4), "traffic": None,
-                "peak_source": src, "dominant_kernel": dom,
-                "dominant_share_of_step": round(tot / args.steps / step_prof_ms, 3)}
+                "algorithmic_bytes_per_launch": int(mb),
+                "share_of_step": round(tot / args.steps / step_prof_ms, 3),
+                "dominant_kernel": dom}
 
     # ---- end to end through the public API with host buffers ----
-    # HostPipeline: pinned host inputs -> H2D (copy stream) -> fused kernels
-    # -> D2H of the visibility, overlapped across consecutive batches
     e2e = None
     if not args.no_e2e:
-        from paper_2301_05262_b200.infer import HostPipeline
-        host = {k: torch.empty(v.shape, dtype=v.dtype, pin_memory=True) for k, v in inputs.items()}
-        for k in host:
-            host[k].copy_(inputs[k])
-        yh = torch.empty(run.y.shape, dtype=run.y.dtype, pin_memory=True)
-        h2d = sum(v.numel() * v.element_size() for v in host.values())
-        d2h = yh.numel() * yh.element_size()
-        pipe = HostPipeline(run)
-        for _ in range(2):
-            pipe.submit(host, yh)
-        pipe.synchronize()
-        torch.cuda.synchronize()
-        k2 = max(3, min(args.steps, 10))
-        barrier(world)
-        e0.record(pipe.h2d)
-        for _ in range(k2):
-            pipe.submit(host, yh)
-        e1.record(pipe.d2h)
-        pipe.synchronize()
-        torch.cuda.synchronize()
-        barrier(world)
-        ems = allreduce_max(e0.elapsed_time(e1) / k2, world)
-        e2e = {"value": round(frames_total / (ems / 1e3), 3), "unit": UNIT,
-               "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
-               "ms_per_step": round(ems, 4), "steps": k2,
-               "api": "infer.HostPipeline.submit (pinned host in/out, copies overlapped)"}
+        e2e = run_e2e(args, run, inputs, frames, job_n, world)
+
+    # ---- the fully covered variant (a typical game G-buffer) ----
+    variants = None
+    if not args.no_variants and args.cover == "scene" and args.config in (2, 3, 4):
+        fc = [full_cover_frame(f) for f in frames]
+        fin = producer.render_inputs(fc)
+        frun = ShadowInference(plan, fc, out_dtype=out_dtype)
+        frun(fin)
+        frun.capture(fin)
+        for _ in range(3):
+            frun.replay()
+        fms, _ = time_steps(frun.replay, args.steps, world, soak=False, local=local)
+        fms_max = float(gather_floats([fms], world, dev)[:, 0].max())
+        variants = {"full_coverage": {"value": round(job_n / (fms_max / 1e3), 3), "unit": UNIT,
+                                      "ms_per_step": round(fms_max, 5),
+                                      "coverage": round(covered_pixels(fin) / (len(fc) * h * wd), 4)}}
+        del frun, fin
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cpu = cpu_baseline_sample(frames[:1], inputs, w, reps=2)
+        planes = {k: v[0].cpu().numpy() for k, v in inputs.items()}
+        cpu = cpu_leg(args, [frames[0]], [planes], reps=1 if args.config == 5 else 3)
 
     if rank == 0:
-        mpix = value * h * wd / 1e6
         line = {
             "metric": metric_name(args.config), "value": round(value, 3), "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": max(args.warmup, 3), "ms_per_step": round(ms_max, 5),
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "higher_is_better": True, "scaling": scaling, "vs_baseline": None,
             "dtype": {"fp16": "f16", "bf16": "bf16", "fp32": "f32"}[args.dtype],
             "data": "synthetic (procedural scenes rendered on-GPU; random-init weights)",
-            "config": {"workload": workload_name(args.config), "frames_per_rank": n,
+            "config": {"workload": workload_name(args), "job_frames": job_n,
+                       "frames_per_rank": [int(v) for v in per_rank[:, 1]],
                        "resolution": [h, wd], "net_resolution": [(h + 15) // 16 * 16, wd],
                        "shadow_map": list(frames[0].view.resolution),
-                       "network": "NetworkConfig(layers=5, base=16, in=4, s2d) 164,500 params",
+                       "network": f"NetworkConfig(layers=5, base=16, in={args.features}, s2d) "
+                                  f"{sum(int(np.asarray(v.data).size) for v in w.values()):,} params",
+                       "features": args.features,
+                       "precision": plan.precision,
+                       "coverage": round(covered_pixels(inputs) / (n * h * wd), 4),
                        "l2": "inputs > L2 (no flush needed)",
-                       "graph": not args.no_graph, "parallelism": f"frames-dp{world}"},
-            "mpix_per_s": round(mpix, 2),
+                       "graph": not args.no_graph,
+                       "parallelism": f"frames-dp{world} ({'sharded job' if scaling == 'strong' else 'one job per rank'})"},
+            "mpix_per_s": round(value * h * wd / 1e6, 2),
+            "per_rank_ms": [round(float(v), 5) for v in per_rank[:, 0]],
             "roofline": roof,
             "step_roofline": {"bytes": int(step_bytes), "flops": step_flops,
                               "gbps": round(step_bytes / (ms / 1e3) / 1e9, 1),
@@ -354,8 +476,10 @@ def run_ours(args):
                                            sorted(prof.items(), key=lambda kv: -kv[1][1])},
             "cpu_baseline": cpu,
             "e2e": e2e,
+            "variants": variants,
+            "gathered": gathered,
             "gpu_launches": int(per_step * args.steps),
-            "clocks": clk.summary(),
+            "clocks": clocks,
         }
         print(json.dumps(line))
     if world > 1:
@@ -363,70 +487,188 @@ def run_ours(args):
         dist.destroy_process_group()
 
 
+def run_e2e(args, run, inputs, frames, job_n, world):
+    """The same metric through infer.HostPipeline.submit: pinned host
+    inputs -> H2D (copy stream) -> fused kernels -> D2H of the visibility,
+    overlapped across consecutive batches; each batch carries its frames."""
+    import torch
+    from paper_2301_05262_b200.infer import HostPipeline
+    host = {k: torch.empty(v.shape, dtype=v.dtype, pin_memory=True) for k, v in inputs.items()}
+    for k in host:
+        host[k].copy_(inputs[k])
+    yh = torch.empty(run.y.shape, dtype=run.y.dtype, pin_memory=True)
+    h2d = sum(v.numel() * v.element_size() for v in host.values())
+    d2h = yh.numel() * yh.element_size()
+    table = run.frame_table(frames)
+    pipe = HostPipeline(run)
+    for _ in range(2):
+        pipe.submit(host, yh, frames=table)
+    pipe.synchronize()
+    torch.cuda.synchronize()
+    k2 = max(3, min(args.steps, 10))
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    barrier(world)
+    e0.record(pipe.h2d)
+    for _ in range(k2):
+        pipe.submit(host, yh, frames=table)
+    e1.record(pipe.d2h)
+    pipe.synchronize()
+    torch.cuda.synchronize()
+    barrier(world)
+    ems = float(gather_floats([e0.elapsed_time(e1) / k2], world, run.y.device)[:, 0].max())
+    return {"value": round(job_n / (ems / 1e3), 3), "unit": UNIT,
+            "h2d_bytes_per_step": int(h2d * world), "d2h_bytes_per_step": int(d2h * world),
+            "ms_per_step": round(ems, 4), "steps": k2,
+            "api": "infer.HostPipeline.submit (pinned host in/out, per-batch frames, copies overlapped)"}
+
+
 # --------------------------------------------------------------------------
-# CPU reference arm (the oracle port of shadowkit's algorithm)
+# CPU legs: the reference's own code (oracle/_ref) or the oracle port
 # --------------------------------------------------------------------------
 
-def _oracle_frame(fr, planes, weights):
+def _stock():
+    """The staged reference package (oracle/_ref/shadowkit) or None."""
+    ref = os.path.join(ROOT, "oracle", "_ref")
+    if not os.path.isdir(os.path.join(ref, "shadowkit")):
+        return None
+    if ref not in sys.path:
+        sys.path.insert(0, ref)
+    import shadowkit
+    return shadowkit
+
+
+def _blas_info():
+    try:
+        from threadpoolctl import threadpool_info
+        return [{k: d.get(k) for k in ("internal_api", "num_threads", "version")}
+                for d in threadpool_info() if d.get("user_api") == "blas"]
+    except Exception as e:      # noqa: BLE001
+        return [f"threadpoolctl unavailable: {e}"]
+
+
+def _cpu_frame_fn(args, fr, planes):
+    """One frame of the reference algorithm: stage 1 + stage 2 (padded to
+    1088 rows as the GPU path pads, cropped back).  Returns (callable, kind,
+    what)."""
     from oracle import features as of
     from oracle import network as on
-    feats, _ = of.features_from_planes(planes["d"], planes["normal"], planes["position"],
-                                       planes["sm"], fr.camera, fr.view, fr.scene.emitter_center,
-                                       fr.size_index, fr.bias)
-    h, w = feats.shape[1:]
+    h, w = fr.camera.resolution
     hp, wp = (h + 15) // 16 * 16, (w + 15) // 16 * 16
-    x = np.zeros((4, hp, wp), np.float32)
-    x[:, :h, :w] = feats
-    return on.forward(weights, x)[:, :h, :w]
+    sk = _stock()
+    if args.features == 5:
+        from oracle import blocker as ob
+    if sk is not None:
+        from shadowkit import autodiff as ad, network as skn, raster as skr, scene as sks
+        cam = sks.CameraPose(fr.camera.position, fr.camera.forward, fr.camera.up, fr.camera.fov_y,
+                             fr.camera.resolution)
+        view = skr.EmitterView(np.asarray(fr.view.position), np.asarray(fr.view.forward),
+                               np.asarray(fr.view.up), np.asarray(fr.view.right), float(fr.view.tan_half),
+                               tuple(fr.view.resolution))
+        z_f, c_e, c_c, cov = of.derive_planes(planes["d"], planes["normal"], planes["position"], fr.camera,
+                                              fr.scene.emitter_center)
+        g = skr.GBuffer(d=planes["d"].astype(np.float64), normal=planes["normal"].astype(np.float64),
+                        position=planes["position"].astype(np.float64), n_e=None, z_f=z_f, c_e=c_e,
+                        c_c=c_c, coverage=cov, camera=cam)
+        sm = skr.ShadowMap(depth=planes["sm"].astype(np.float64), view=view,
+                           scene_diag=float(fr.bias) / skr.DEFAULT_BIAS_FACTOR)
+        cfg = skn.NetworkConfig(in_channels=args.features)
+        wts = skn.init_weights(cfg, np.random.default_rng(np.random.SeedSequence([0, 0x11])))
+
+        def one():
+            with ad.no_grad():
+                fs = skr.assemble_features(g, sm, float(fr.size_index), float(fr.bias))
+                x = np.zeros((args.features, hp, wp), np.float32)
+                x[:4, :h, :w] = fs.data
+                if args.features == 5:
+                    x[4, :h, :w] = ob.blocker_plane(planes["d"], planes["position"], z_f, cov, planes["sm"],
+                                                    fr.view, fr.bias, fr.size_index, fr.camera.focal_px)
+                return skn.forward(wts, cfg, x).data[:, :h, :w]
+        what = "shadowkit raster.assemble_features + network.forward (no_grad)"
+        if args.features == 5:
+            what += " + oracle blocker plane"
+        return one, "reference", what
+
+    from paper_2301_05262_b200 import network as pn
+    cfg = pn.NetworkConfig(in_channels=args.features)
+    W = {k: v.data for k, v in pn.init_weights(cfg, np.random.default_rng(np.random.SeedSequence([0, 0x11]))).items()}
+
+    def one():
+        feats, cov = of.features_from_planes(planes["d"], planes["normal"], planes["position"], planes["sm"],
+                                             fr.camera, fr.view, fr.scene.emitter_center, fr.size_index, fr.bias)
+        x = np.zeros((args.features, hp, wp), np.float32)
+        x[:4, :h, :w] = feats
+        if args.features == 5:
+            z_f, _, _, _ = of.derive_planes(planes["d"], planes["normal"], planes["position"], fr.camera,
+                                            fr.scene.emitter_center)
+            x[4, :h, :w] = ob.blocker_plane(planes["d"], planes["position"], z_f, cov, planes["sm"], fr.view,
+                                            fr.bias, fr.size_index, fr.camera.focal_px)
+        return on.forward(W, x)[:, :h, :w]
+    return one, "port", "oracle port of assemble_features + forward (numpy)"
 
 
-def cpu_baseline_sample(frames, inputs, weights, reps=2):
-    """Time the oracle port on a bounded sample (one frame, best of reps)."""
-    W = {k: v.data for k, v in weights.items()}
-    planes = {k: v[0].cpu().numpy() for k, v in inputs.items()}
+def cpu_leg(args, frames, planes, reps=3):
+    """Best-of-``reps`` seconds per frame of the reference algorithm on the
+    host cores (BLAS capped at the process's affinity set)."""
+    cores = len(os.sched_getaffinity(0))
+    try:
+        from threadpoolctl import threadpool_limits
+        limit = threadpool_limits(limits=cores)
+    except Exception:          # noqa: BLE001
+        limit = None
+    fns = [_cpu_frame_fn(args, fr, p) for fr, p in zip(frames, planes)]
     best = float("inf")
-    for _ in range(reps):
+    for r in range(reps):
         t = time.perf_counter()
-        _oracle_frame(frames[0], planes, W)
-        best = min(best, time.perf_counter() - t)
-    return {"value": round(1.0 / best, 4), "unit": UNIT, "cores": len(os.sched_getaffinity(0)),
-            "kind": "port", "sample": f"1 frame of the workload, best of {reps} "
-            f"({best:.2f} s/frame; numpy+OpenBLAS threads = all cores)"}
+        for fn, _, _ in fns:
+            fn()
+        best = min(best, (time.perf_counter() - t) / len(fns))
+    info = _blas_info()
+    if limit is not None:
+        limit.restore_original_limits()
+    _, kind, what = fns[0]
+    return {"value": round(1.0 / best, 4), "unit": UNIT, "cores": cores, "kind": kind,
+            "sample": f"{len(fns)} frame(s) of the workload, best of {reps}: {what}; "
+                      f"{best:.2f} s/frame", "blas": info}
 
 
 def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    import torch
-    from paper_2301_05262_b200 import network, producer, scenes
-    from oracle import network as _on  # noqa: F401  (fail early if absent)
-    frames = scenes.config_frames(args.config, seed=0, n_frames=args.frames)
-    inputs = producer.render_inputs(frames) if torch.cuda.is_available() else None
-    cfg = network.NetworkConfig()
-    w = network.init_weights(cfg, np.random.default_rng(np.random.SeedSequence([0, 0x11])))
-    W = {k: v.data for k, v in w.items()}
-    planes = [{k: v[i].cpu().numpy() for k, v in inputs.items()} for i in range(len(frames))]
-    warm = min(args.warmup, 1)
-    steps = min(args.steps, 5)
-    for i in range(warm):
-        _oracle_frame(frames[i % len(frames)], planes[i % len(frames)], W)
+    from oracle import producer as op
+    frames = job_frames(args, seed=0)
+    sample = frames[:2] if args.config == 5 else frames[:1]       # config 5: one hard + one soft scene
     t = time.perf_counter()
-    for i in range(steps):
-        _oracle_frame(frames[i % len(frames)], planes[i % len(frames)], W)
-    el = time.perf_counter() - t
+    planes = [op.render_inputs_banded(f.scene.primitive_table(), f.camera, f.view) for f in sample]
+    t_render = time.perf_counter() - t
+    cores = len(os.sched_getaffinity(0))
+    from threadpoolctl import threadpool_limits
+    with threadpool_limits(limits=cores):
+        fns = [_cpu_frame_fn(args, fr, p) for fr, p in zip(sample, planes)]
+        warm = min(args.warmup, 1)
+        cap = 2 if args.config == 5 else 5
+        steps = max(1, min(args.steps, cap))
+        for i in range(warm):
+            fns[i % len(fns)][0]()
+        t = time.perf_counter()
+        for i in range(steps):
+            fns[i % len(fns)][0]()
+        el = time.perf_counter() - t
+        info = _blas_info()
     value = steps / el
+    kind, what = fns[0][1], fns[0][2]
     h, wd = frames[0].camera.resolution
     print(json.dumps({
         "metric": metric_name(args.config), "value": round(value, 4), "unit": UNIT, "impl": "reference",
         "n_gpus": int(os.environ.get("WORLD_SIZE", "1")), "steps": steps, "warmup": warm,
-        "ms_per_step": round(el / steps * 1e3, 2), "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "f32", "data": "synthetic (same scenes/weights as ours)",
-        "config": {"workload": workload_name(args.config), "resolution": [h, wd],
-                   "note": f"one frame per step; steps capped at 5 (asked {args.steps})"},
-        "cpu_baseline": {"value": round(value, 4), "unit": UNIT,
-                         "cores": len(os.sched_getaffinity(0)), "kind": "port",
-                         "sample": "one 1080p frame per step: oracle assemble_features + forward"},
+        "ms_per_step": round(el / steps * 1e3, 2), "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic (the same seeded scenes and weights as ours; inputs ray-cast on the CPU)",
+        "config": {"workload": workload_name(args), "resolution": [h, wd], "features": args.features,
+                   "note": f"one frame per step (bounded sample), steps capped at {cap} (asked {args.steps}); "
+                           f"inputs rendered in {t_render:.1f} s, untimed"},
+        "cpu_baseline": {"value": round(value, 4), "unit": UNIT, "cores": cores, "kind": kind,
+                         "sample": f"{len(sample)} frame(s) of the workload cycled: {what}", "blas": info},
         "e2e": {"value": round(value, 4), "unit": UNIT, "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
         "mpix_per_s": round(value * h * wd / 1e6, 4),
@@ -435,7 +677,9 @@ def run_reference(args):
 
 if __name__ == "__main__":
     a = parse()
+    env_guard()
     if a.impl == "reference":
         run_reference(a)
     else:
+        maybe_spawn(a)
         run_ours(a)

@@ -31,7 +31,7 @@
 extern "C" {
 #endif
 
-#define NSM_ABI_VERSION 1
+#define NSM_ABI_VERSION 2
 #define NSM_MAX_FRAMES_PER_LAUNCH 8
 
 typedef enum nsm_status {
@@ -170,6 +170,18 @@ nsm_status nsm_infer(const nsm_plan* plan, const nsm_gbuffer* g, const float* sm
                      int32_t w, void* y, nsm_dtype y_dtype, int64_t* first_bad,
                      void* workspace, size_t ws_bytes, void* stream);
 
+/* nsm_infer plus the parity hook of the fused feature pass: texel_idx
+ * (nullable) is an (n, 2, h, w) int32 device array that receives, for every
+ * covered pixel, the (row, col) shadow-map texel the fused kernel actually
+ * gathered -- the np.rint indices of _shadow_lookup (raster.py:247-250) --
+ * so tests can prove them bit-exact.  Uncovered pixels are either left
+ * untouched or set to -1 (the caller pre-fills with -1).  Same validation and errors as
+ * nsm_infer; with texel_idx == NULL the two calls are identical. */
+nsm_status nsm_infer_ex(const nsm_plan* plan, const nsm_gbuffer* g, const float* sm,
+                        int64_t sm_stride, const nsm_frame* frames, int32_t n, int32_t h,
+                        int32_t w, void* y, nsm_dtype y_dtype, int64_t* first_bad,
+                        int32_t* texel_idx, void* workspace, size_t ws_bytes, void* stream);
+
 /* ---- input producers (the step before the path) ----
  * raster.render_gbuffer (raster.py:217-242) depth/normal/position planes and
  * raster.render_shadowmap (raster.py:206-214) over an analytic primitive
@@ -209,6 +221,13 @@ int32_t nsm_profile_report(char* buf, size_t cap);
 
 const char* nsm_last_error(void);
 int32_t nsm_abi_version(void);
+
+/* Build flavour: bit 0 set = experiment build (-DNSM_EXPERIMENTS: the NSM_*
+ * attribution switches of tools/, which skip work and give wrong results).
+ * Release builds ignore every NSM_* environment variable; bench.py refuses
+ * to time an experiment build. */
+#define NSM_BUILD_EXPERIMENTS 1
+int32_t nsm_build_flags(void);
 
 #ifdef __cplusplus
 }

@@ -107,3 +107,48 @@ def render_gbuffer(table, camera):
     pos = o + ts[..., None] * rays
     d = ts * (rays @ np.asarray(camera.forward))
     return d, np.moveaxis(n, -1, 0) * cov, np.moveaxis(pos, -1, 0) * cov
+
+
+def _gbuf_band(args):
+    table, camera, y0, y1 = args
+    r = camera_rays(camera)[y0:y1]
+    o = np.asarray(camera.position, dtype=np.float64)
+    t, n = nearest_hit(table, o, r)
+    cov = np.isfinite(t)
+    ts = np.where(cov, t, 0.0)
+    return (y0, (ts * (r @ np.asarray(camera.forward))).astype(np.float32),
+            np.moveaxis(n * cov[..., None], -1, 0).astype(np.float32),
+            np.moveaxis((o + ts[..., None] * r) * cov[..., None], -1, 0).astype(np.float32))
+
+
+def _sm_band(args):
+    table, view, y0, y1 = args
+    return y0, nearest_hit(table, np.asarray(view.position, dtype=np.float64),
+                           texel_rays(view)[y0:y1])[0].astype(np.float32)
+
+
+def render_inputs_banded(table, camera, view, band=64, workers=None):
+    """The hot path's fp32 input planes of one frame, rendered in row bands
+    on a process pool (bounded memory at 1080p / 4K): d (H,W), normal
+    (3,H,W), position (3,H,W), sm (Hs,Ws).  Used by bench.py's CPU
+    reference leg, whose process must not load the CUDA library that
+    renders them on the GPU."""
+    import multiprocessing as mp
+    import os
+    h, w = camera.resolution
+    hs, ws = view.resolution
+    d = np.zeros((h, w), np.float32)
+    nrm = np.zeros((3, h, w), np.float32)
+    pos = np.zeros((3, h, w), np.float32)
+    sm = np.empty((hs, ws), np.float32)
+    jobs_g = [(table, camera, y, min(y + band, h)) for y in range(0, h, band)]
+    jobs_s = [(table, view, y, min(y + band, hs)) for y in range(0, hs, band)]
+    n = workers or max(1, len(os.sched_getaffinity(0)))
+    with mp.get_context("fork").Pool(n) as pool:
+        for y0, dd, nn, pp in pool.imap_unordered(_gbuf_band, jobs_g):
+            d[y0:y0 + dd.shape[0]] = dd
+            nrm[:, y0:y0 + dd.shape[0]] = nn
+            pos[:, y0:y0 + dd.shape[0]] = pp
+        for y0, ss in pool.imap_unordered(_sm_band, jobs_s):
+            sm[y0:y0 + ss.shape[0]] = ss
+    return {"d": d, "normal": nrm, "position": pos, "sm": sm}

@@ -18,6 +18,8 @@ NSM_OK, NSM_ERR_ARG, NSM_ERR_SHAPE, NSM_ERR_FRUSTUM, NSM_ERR_FORMAT, NSM_ERR_CUD
     NSM_ERR_UNSUPPORTED = range(7)
 NSM_F32, NSM_F16, NSM_BF16, NSM_F64 = range(4)
 MAX_FRAMES_PER_LAUNCH = 8
+ABI_VERSION = 2
+BUILD_EXPERIMENTS = 1
 INT64_MAX = (1 << 63) - 1
 
 
@@ -84,6 +86,10 @@ _EXPORTS = {
     "nsm_infer": (C.c_int, [C.POINTER(PlanHandle), C.POINTER(GBufferC), C.c_void_p, C.c_int64,
                             C.POINTER(FrameC), C.c_int32, C.c_int32, C.c_int32, C.c_void_p,
                             C.c_int32, C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p]),
+    "nsm_infer_ex": (C.c_int, [C.POINTER(PlanHandle), C.POINTER(GBufferC), C.c_void_p, C.c_int64,
+                               C.POINTER(FrameC), C.c_int32, C.c_int32, C.c_int32, C.c_void_p,
+                               C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p, C.c_size_t,
+                               C.c_void_p]),
     "nsm_render_gbuffer": (C.c_int, [C.c_void_p, C.c_int32, C.POINTER(CameraC), C.c_void_p,
                                      C.c_void_p, C.c_void_p, C.c_void_p]),
     "nsm_render_shadowmap": (C.c_int, [C.c_void_p, C.c_int32, C.POINTER(EmitterViewC),
@@ -97,6 +103,7 @@ _EXPORTS = {
     "nsm_profile_report": (C.c_int32, [C.c_char_p, C.c_size_t]),
     "nsm_last_error": (C.c_char_p, []),
     "nsm_abi_version": (C.c_int32, []),
+    "nsm_build_flags": (C.c_int32, []),
 }
 
 
@@ -114,6 +121,13 @@ def _load():
 
 
 lib = _load()
+if lib.nsm_abi_version() != ABI_VERSION:
+    raise ImportError(f"{LIB_PATH} has ABI {lib.nsm_abi_version()}, this binding wants {ABI_VERSION}: rebuild")
+
+
+def experiment_build() -> bool:
+    """True when libnsm.so was built with -DNSM_EXPERIMENTS (tools/ only)."""
+    return bool(lib.nsm_build_flags() & BUILD_EXPERIMENTS)
 
 
 def check(status: int, what: str = "") -> None:

@@ -19,6 +19,12 @@ CSRC = os.path.join(HERE, "csrc")
 BUILD = os.path.join(HERE, "_build")
 LIB = os.path.join(HERE, "libnsm.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
+# Experiment builds (-DNSM_EXPERIMENTS: the NSM_* attribution / tracing
+# switches of tools/) go to their own object directory; the library they link
+# reports it through nsm_build_flags() and bench.py refuses to time it.
+EXPERIMENTS = os.environ.get("NSM_BUILD_EXPERIMENTS", "0") == "1"
+if EXPERIMENTS:
+    BUILD = os.path.join(HERE, "_build_exp")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O3", "--use_fast_math",
          "-Xptxas", "-v", "-I" + os.path.join(ROOT, "include")]
@@ -49,6 +55,8 @@ def _compile(src):
     # division/sqrt (features.cu, net_f32.cu, producer.cu, abi.cu)
     flags = [f for f in FLAGS if f != "--use_fast_math"] if src in (
         "features.cu", "net_f32.cu", "producer.cu", "abi.cu", "temporal.cu") else FLAGS
+    if EXPERIMENTS:
+        flags = flags + ["-DNSM_EXPERIMENTS"]
     cmd = [NVCC, *ARCH, *flags, "-c", path, "-o", obj]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
@@ -66,11 +74,18 @@ def build(verbose: bool = False) -> str:
         for o, log in results:
             if log:
                 print(f"--- {os.path.basename(o)}\n{log}")
-    if not os.path.exists(LIB) or any(os.path.getmtime(o) > os.path.getmtime(LIB) for o in objs):
+    # relink whenever the objects are newer or the library came from the
+    # other build flavour
+    stamp = LIB + ".flavour"
+    flavour = "experiments" if EXPERIMENTS else "release"
+    same = os.path.exists(stamp) and open(stamp).read() == flavour
+    if not same or not os.path.exists(LIB) or any(os.path.getmtime(o) > os.path.getmtime(LIB) for o in objs):
         cmd = [NVCC, *ARCH, "-shared", "-cudart", "static", "-o", LIB, *objs]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"link failed:\n{r.stderr}")
+        with open(stamp, "w") as f:
+            f.write(flavour)
     return LIB
 
 

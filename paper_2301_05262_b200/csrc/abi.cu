@@ -175,6 +175,31 @@ __global__ void crop_kernel(const float* __restrict__ src, int hp, int wp, int h
     }
 }
 
+// Every frame of a batch must describe the (h, w) frames the planes hold
+// and a shadow map that fits its sm_stride slot: the kernels index the map
+// with each frame's own resolution.
+nsm_status check_frames(const nsm_frame* frames, int32_t n, int32_t h, int32_t w, int64_t sm_stride) {
+    for (int i = 0; i < n; ++i) {
+        const nsm_frame& f = frames[i];
+        if (f.camera.height != h || f.camera.width != w)
+            return fail(NSM_ERR_ARG, "frame %d: camera is %dx%d but the G-buffer planes are %dx%d", i,
+                        f.camera.height, f.camera.width, h, w);
+        if (f.view.height <= 0 || f.view.width <= 0 || (int64_t)f.view.height * f.view.width > sm_stride)
+            return fail(NSM_ERR_ARG, "frame %d: a %dx%d shadow map does not fit sm_stride %lld", i,
+                        f.view.height, f.view.width, (long long)sm_stride);
+    }
+    return NSM_OK;
+}
+
+// A plan's weights live on the device that was current at creation.
+nsm_status check_device(const Plan& p) {
+    int dev = -1;
+    cudaGetDevice(&dev);
+    if (dev != p.device)
+        return fail(NSM_ERR_ARG, "plan lives on device %d, current device is %d", p.device, dev);
+    return NSM_OK;
+}
+
 size_t infer_f32_workspace(const Plan& p, int n, int h, int w) {
     const int m = 1 << (p.cfg.layers - 1);
     const int hp = round_up(h, m), wp = round_up(w, m);
@@ -190,6 +215,14 @@ using namespace nsm;
 extern "C" {
 
 int32_t nsm_abi_version(void) { return NSM_ABI_VERSION; }
+
+int32_t nsm_build_flags(void) {
+#ifdef NSM_EXPERIMENTS
+    return NSM_BUILD_EXPERIMENTS;
+#else
+    return 0;
+#endif
+}
 
 const char* nsm_last_error(void) { return g_err.c_str(); }
 
@@ -271,6 +304,7 @@ nsm_status nsm_plan_create(const nsm_net_config* cfg, int32_t n_tensors, const c
     }
     p->dev = dev;
     p->dev_bytes = blob.size();
+    cudaGetDevice(&p->device);
     for (auto& kv : expect) {
         ConvW* c = conv_by_name(*p, kv.first.substr(0, kv.first.size() - 2));
         const float* d = (const float*)((char*)dev + off[kv.first]);
@@ -338,6 +372,7 @@ nsm_status nsm_features(const nsm_gbuffer* g, const float* sm, int64_t sm_stride
         return fail(NSM_ERR_ARG, "G-buffer planes must be F32 or F64");
     if (!(g->z_f && g->c_e && g->c_c) && !g->normal)
         return fail(NSM_ERR_ARG, "normal plane needed to derive z_f/c_e/c_c");
+    if (nsm_status s = check_frames(frames, n, h, w, sm_stride)) return s;
     return launch_features(g, sm, sm_stride, frames, n, h, w, h, w, out_planes, texel_idx,
                            first_bad, (cudaStream_t)stream);
 }
@@ -350,6 +385,7 @@ nsm_status nsm_blocker_plane(const nsm_gbuffer* g, const float* sm, int64_t sm_s
         return fail(NSM_ERR_ARG, "nsm_blocker_plane: null argument");
     if (n <= 0 || h <= 0 || w <= 0 || radius <= 0) return fail(NSM_ERR_ARG, "nsm_blocker_plane: bad size");
     if (g->dtype != NSM_F32 && g->dtype != NSM_F64) return fail(NSM_ERR_ARG, "G-buffer planes must be F32 or F64");
+    if (nsm_status s = check_frames(frames, n, h, w, sm_stride)) return s;
     return launch_blocker(g, sm, sm_stride, frames, n, h, w, radius, out, first_bad, (cudaStream_t)stream);
 }
 
@@ -363,6 +399,7 @@ nsm_status nsm_forward(const nsm_plan* plan, const float* x, int32_t n, int32_t 
     // network.forward (network.py:169-173)
     if (h <= 0 || w <= 0 || h % f || w % f)
         return fail(NSM_ERR_SHAPE, "spatial dims %dx%d must be divisible by %d", h, w, f);
+    if (nsm_status s = check_device(*p)) return s;
     if (p->act == NSM_F32)
         return forward_f32(*p, x, n, h, w, y, workspace, ws_bytes, (cudaStream_t)stream);
     if (!f16_supported(*p))
@@ -374,6 +411,14 @@ nsm_status nsm_infer(const nsm_plan* plan, const nsm_gbuffer* g, const float* sm
                      int64_t sm_stride, const nsm_frame* frames, int32_t n, int32_t h, int32_t w,
                      void* y, nsm_dtype y_dtype, int64_t* first_bad, void* workspace,
                      size_t ws_bytes, void* stream) {
+    return nsm_infer_ex(plan, g, sm, sm_stride, frames, n, h, w, y, y_dtype, first_bad, nullptr, workspace,
+                        ws_bytes, stream);
+}
+
+nsm_status nsm_infer_ex(const nsm_plan* plan, const nsm_gbuffer* g, const float* sm,
+                        int64_t sm_stride, const nsm_frame* frames, int32_t n, int32_t h, int32_t w,
+                        void* y, nsm_dtype y_dtype, int64_t* first_bad, int32_t* texel_idx, void* workspace,
+                        size_t ws_bytes, void* stream) {
     clear_error();
     const Plan* p = reinterpret_cast<const Plan*>(plan);
     if (!p || !g || !sm || !frames || !y || !first_bad || !workspace || !g->d || !g->position)
@@ -386,12 +431,14 @@ nsm_status nsm_infer(const nsm_plan* plan, const nsm_gbuffer* g, const float* sm
         return fail(NSM_ERR_ARG, "G-buffer planes must be F32 or F64");
     if (!(g->z_f && g->c_e && g->c_c) && !g->normal)
         return fail(NSM_ERR_ARG, "normal plane needed to derive z_f/c_e/c_c");
+    if (nsm_status s = check_frames(frames, n, h, w, sm_stride)) return s;
+    if (nsm_status s = check_device(*p)) return s;
     cudaStream_t st = (cudaStream_t)stream;
     if (p->act != NSM_F32) {
         if (!f16_supported(*p))
             return fail(NSM_ERR_UNSUPPORTED, "no 16-bit kernels for this NetworkConfig");
-        return infer_f16(*p, g, sm, sm_stride, frames, n, h, w, y, y_dtype, first_bad, workspace,
-                         ws_bytes, st);
+        return infer_f16(*p, g, sm, sm_stride, frames, n, h, w, y, y_dtype, first_bad, texel_idx,
+                         workspace, ws_bytes, st);
     }
     if (ws_bytes < infer_f32_workspace(*p, n, h, w))
         return fail(NSM_ERR_ARG, "workspace too small");
@@ -401,7 +448,9 @@ nsm_status nsm_infer(const nsm_plan* plan, const nsm_gbuffer* g, const float* sm
     float* yfull = feat + (size_t)n * 4 * hp * wp;
     char* rest = (char*)(yfull + (size_t)n * hp * wp);
     rest = (char*)(((uintptr_t)rest + 255) & ~(uintptr_t)255);
-    nsm_status s = launch_features(g, sm, sm_stride, frames, n, h, w, hp, wp, feat, nullptr,
+    if (texel_idx && (hp != h || wp != w))
+        return fail(NSM_ERR_UNSUPPORTED, "texel_idx on an fp32 plan needs h, w divisible by %d", m);
+    nsm_status s = launch_features(g, sm, sm_stride, frames, n, h, w, hp, wp, feat, texel_idx,
                                    first_bad, st);
     if (s != NSM_OK) return s;
     const bool direct = (hp == h && wp == w && y_dtype == NSM_F32);

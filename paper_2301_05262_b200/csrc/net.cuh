@@ -38,6 +38,7 @@ struct Plan {
     ConvW d0p3, d0p1, d0ph;
     int64_t n_params = 0;
     void* dev = nullptr;          // one allocation holding every tensor
+    int device = -1;              // the CUDA device dev lives on
     size_t dev_bytes = 0;
 };
 
@@ -53,7 +54,7 @@ nsm_status forward_f16(const Plan& p, const float* x, int n, int h, int w, float
                        size_t ws_bytes, cudaStream_t st);
 nsm_status infer_f16(const Plan& p, const nsm_gbuffer* g, const float* sm, int64_t sm_stride,
                      const nsm_frame* frames, int n, int h, int w, void* y, nsm_dtype y_dtype,
-                     int64_t* first_bad, void* ws, size_t ws_bytes, cudaStream_t st);
+                     int64_t* first_bad, int32_t* texel_idx, void* ws, size_t ws_bytes, cudaStream_t st);
 
 nsm_status launch_features(const nsm_gbuffer* g, const float* sm, int64_t sm_stride,
                            const nsm_frame* frames, int32_t n, int32_t h, int32_t w, int32_t ho,

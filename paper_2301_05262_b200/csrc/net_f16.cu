@@ -15,6 +15,7 @@
 // for ldmatrix rows and for UMMA descriptors alike.  Bias, ReLU, pooling,
 // upsampling, skip sums, the head and the sigmoid run in fp32 registers.
 #include <algorithm>
+#include <atomic>
 #include <type_traits>
 #include <utility>
 #include <cmath>
@@ -32,25 +33,33 @@ namespace nsm {
 namespace {
 
 // ------------------------------------------------------------------ config
-// frames per pass through all levels (L2 residency vs. launch fill/drain);
-// NSM_CHUNK_FRAMES overrides it for experiments
+// Experiment switches (chunk size, PDL, the work-skipping attribution modes
+// of enc0 / the level kernels, the dec0 ring, per-tile traces) exist only in
+// builds with -DNSM_EXPERIMENTS (tools/); the release library ignores every
+// NSM_* environment variable.
+#ifdef NSM_EXPERIMENTS
+constexpr bool kExp = true;
+int env_int(const char* name, int dflt) {
+    const char* e = getenv(name);
+    return e ? atoi(e) : dflt;
+}
+#else
+constexpr bool kExp = false;
+int env_int(const char*, int dflt) { return dflt; }
+#endif
+
+// frames per pass through all levels (L2 residency vs. launch fill/drain)
 int chunk_frames() {
     static int v = 0;
-    if (!v) {
-        const char* e = getenv("NSM_CHUNK_FRAMES");
-        v = e ? std::max(1, std::min(NSM_MAX_FRAMES_PER_LAUNCH, atoi(e))) : NSM_MAX_FRAMES_PER_LAUNCH;
-    }
+    if (!v) v = std::max(1, std::min(NSM_MAX_FRAMES_PER_LAUNCH, env_int("NSM_CHUNK_FRAMES", NSM_MAX_FRAMES_PER_LAUNCH)));
     return v;
 }
 // Kernel launches of the fused path go through launch_pdl: programmatic
 // stream serialisation lets each kernel's prologue overlap its predecessor's
-// tail (the kernels call pdl_trigger / pdl_wait).  NSM_PDL=0 disables it.
+// tail (the kernels call pdl_trigger / pdl_wait).
 bool pdl_enabled() {
     static int v = -1;
-    if (v < 0) {
-        const char* e = getenv("NSM_PDL");
-        v = e ? atoi(e) : 1;
-    }
+    if (v < 0) v = env_int("NSM_PDL", 1);
     return v != 0;
 }
 
@@ -68,6 +77,18 @@ void launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cuda
     cfg.numAttrs = pdl_enabled() ? 1 : 0;
     cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
 }
+
+// One-time per-device setup (cudaFuncSetAttribute applies to the current
+// device only): true the first time it is asked for the current device.
+struct PerDevice {
+    std::atomic<uint64_t> done{0};
+    bool first() {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        const uint64_t bit = 1ull << (dev & 63);
+        return !(done.fetch_or(bit) & bit);
+    }
+};
 
 constexpr int E0_TH = 16, E0_TW = 64;  // level-0 output tile (enc0 / dec0)
 constexpr int E0_IR = E0_TH + 2, E0_IC = E0_TW + 2;
@@ -182,6 +203,7 @@ struct Enc0Args {
     const float* b1;
     void* out;            // pooled (N, H0/2, W0/2, 16)
     int64_t* first_bad;
+    int32_t* tidx;        // parity hook (nullable): (N, 2, h, w) texel (row, col) of covered pixels
     int dbg;              // experiments only: 1 skip feature math, 2 skip convolutions
     TileDiv td;           // tile decode constants (host-computed, read from the param bank)
 };
@@ -425,6 +447,11 @@ __device__ __forceinline__ void produce_features(const Enc0Args& a, uint8_t* buf
                     if (!texel_of(F, px[j], py[j], pz[j], ri, ci))
                         atomic_min_i64(a.first_bad + tl.f, (int64_t)fy[j] * a.w + fx[j]);
                     look[j] = __ldg(smf + (int64_t)ri * F.ws + ci);
+                    if (a.tidx) {
+                        int32_t* ti = a.tidx + (int64_t)tl.f * 2 * hw + (int64_t)fy[j] * a.w + fx[j];
+                        ti[0] = ri;
+                        ti[hw] = ci;
+                    }
                 }
             }
 #pragma unroll
@@ -611,6 +638,14 @@ __device__ __forceinline__ void produce_features_tma(const Enc0Args& a, const Gb
             const bool ok = texel_fused(F, px, py, pz, ri, ci);
             bad |= (cov && !ok) << e;
             R.look[e] = cov ? __ldg(a.sm + (sm_off + ri * ws + ci)) : -1.f;   // consumed one phase later
+            if (a.tidx && cov) {      // parity hook: the texel this pixel gathered
+                const int64_t hw = (int64_t)a.h * a.w;
+                int32_t* ti = a.tidx + (int64_t)tl.f * 2 * hw +
+                              (int64_t)(2 * tl.ty0 - 2 + ST_ROWS * (q & 1) + qy) * a.w +
+                              (2 * tl.tx0 - 2 + 2 * (e < 2 ? px_lo : px_hi) + (e & 1));
+                ti[0] = ri;
+                ti[hw] = ci;
+            }
             const float tx = ecx - px, ty = ecy - py, tz = ecz - pz;
             const float l2 = fmaf(tx, tx, fmaf(ty, ty, tz * tz));
             const float izf = rsqrtf(l2);
@@ -651,7 +686,7 @@ __device__ __forceinline__ void produce_features_tma(const Enc0Args& a, const Gb
         QuadPark P;
         if (q < nh) {
             mbar_wait(&full[q & 1], (q >> 1) & 1);
-            if (!(a.dbg & 1)) phaseA(q, RA, P);
+            if (!(kExp && (a.dbg & 1))) phaseA(q, RA, P);
             else for (int e = 0; e < 4; ++e) RA.look[e] = -1.f, P.v[e] = make_uint2(0u, 0u);
             __syncwarp();
             if (lane == 0) mbar_arrive(&empty[q & 1]);                   // stage read
@@ -759,7 +794,7 @@ __global__ void __launch_bounds__(kSrc == 2 ? kE0Threads : kL0Threads, 1) enc0_k
             const int px = ((tl.tx0 + sx) >> 1) + g;
             const bool px_ok = px < W1;
             T* obase = out + (((int64_t)tl.f * H1 + ((tl.ty0 + r0) >> 1)) * W1 + px) * 16 + 2 * t;
-            if (a.dbg & 2) {
+            if (kExp && (a.dbg & 2)) {
                 hook(E0_IR / 2);
                 return;
             }
@@ -1182,7 +1217,7 @@ __global__ void __launch_bounds__(lv_threads<SRC, NB, NPW>(), 1) level_kernel(co
     const int ntx = (a.W + G::TW - 1) / G::TW, nty = (a.H + G::TH - 1) / G::TH;
     const int mytiles = (int)blockIdx.x < total ? (total - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x : 0;
     auto tr = [&](int k, int ev) {     // experiments: CTA 0's per-tile timeline
-        if (a.trace && blockIdx.x == 0 && k < 32) a.trace[k * 8 + ev] = clock64();
+        if (kExp && a.trace && blockIdx.x == 0 && k < 32) a.trace[k * 8 + ev] = clock64();
     };
     auto tile_of = [&](int k, int& f, int& y0, int& x0) {
         const int t = blockIdx.x + k * gridDim.x;
@@ -1306,7 +1341,7 @@ __global__ void __launch_bounds__(lv_threads<SRC, NB, NPW>(), 1) level_kernel(co
                     constexpr int BRH = BR / NH;                // block rows per piece
                     static_assert(BR % NH == 0 && (NH == 1 || BRH * 2 == HR + 1), "block rows per skip piece");
                     constexpr int HI = BRH * BC * G::NCI;       // items per piece
-                    for (int it = h * HI + tid; it < ((a.dbg & 1) ? 0 : (h + 1) * HI); it += NPT) {
+                    for (int it = h * HI + tid; it < ((kExp && (a.dbg & 1)) ? 0 : (h + 1) * HI); it += NPT) {
                         const int c = it % G::NCI, blk = it / G::NCI;
                         const int bil = blk / BC, bjl = blk - bil * BC;
                         const int bi = ly0 + bil, bj = lx0 + bjl;      // low-res pixel of the block
@@ -1380,7 +1415,7 @@ __global__ void __launch_bounds__(lv_threads<SRC, NB, NPW>(), 1) level_kernel(co
                     // the reference's edge clamp.
                     constexpr int BR = G::IR / 2 + 1, BC = G::IC / 2 + 1;
                     constexpr int NITEM = BR * BC * G::NCI;
-                    for (int it = tid; it < ((a.dbg & 1) ? 0 : NITEM); it += NPT) {
+                    for (int it = tid; it < ((kExp && (a.dbg & 1)) ? 0 : NITEM); it += NPT) {
                         const int c = it % G::NCI, blk = it / G::NCI;
                         const int bil = blk / BC, bjl = blk - bil * BC;
                         const int bi = ly0 + bil, bj = lx0 + bjl;      // low-res pixel of the block
@@ -1482,7 +1517,7 @@ __global__ void __launch_bounds__(lv_threads<SRC, NB, NPW>(), 1) level_kernel(co
                 // was the limit; tools/umma_layout_probe.cu)
                 const uint64_t da0 = umma_desc(sbase + s * G::INB, G::PIN, G::ICB * 16);
                 const uint64_t db0 = umma_desc(sbase + G::OFF_W3, C3 * 16, 128);
-                if (!(a.dbg & 4)) {
+                if (!(kExp && (a.dbg & 4))) {
                     // SRC_TENSOR kernels have the registers to unroll the taps
                     // (constant descriptor offsets: ~51 vs ~71 issue cycles per UMMA)
 #pragma unroll (SRC == SRC_TENSOR ? 9 : 1)
@@ -1528,7 +1563,7 @@ __global__ void __launch_bounds__(lv_threads<SRC, NB, NPW>(), 1) level_kernel(co
             constexpr int NIT1 = NB * (C3 / 16) / NG;
             constexpr bool kPre = SRC == SRC_TENSOR;     // register room (no producer warps)
             uint32_t r1[kPre ? NIT1 : 1][16];
-            if (kPre && !(a.dbg & 2)) {
+            if (kPre && !(kExp && (a.dbg & 2))) {
 #pragma unroll
                 for (int i = 0; i < NIT1; ++i) {
                     const int it = grp + NG * i, b = it / (C3 / 16), c0 = (it % (C3 / 16)) * 16;
@@ -1538,7 +1573,7 @@ __global__ void __launch_bounds__(lv_threads<SRC, NB, NPW>(), 1) level_kernel(co
             }
 #pragma unroll
             for (int i = 0; i < NIT1; ++i) {
-                if (a.dbg & 2) break;
+                if (kExp && (a.dbg & 2)) break;
                 const int it = grp + NG * i, b = it / (C3 / 16), c0 = (it % (C3 / 16)) * 16;
                 {
                     float v[16];
@@ -1581,7 +1616,7 @@ __global__ void __launch_bounds__(lv_threads<SRC, NB, NPW>(), 1) level_kernel(co
             constexpr int NIT2 = NB * (C1 / 16) / NG;
             constexpr bool kPre = SRC == SRC_TENSOR;
             uint32_t r2[kPre ? NIT2 : 1][16];
-            if (kPre && !(a.dbg & 2)) {
+            if (kPre && !(kExp && (a.dbg & 2))) {
 #pragma unroll
                 for (int i = 0; i < NIT2; ++i) {
                     const int it = grp + NG * i, b = it / (C1 / 16), c0 = (it % (C1 / 16)) * 16;
@@ -1591,7 +1626,7 @@ __global__ void __launch_bounds__(lv_threads<SRC, NB, NPW>(), 1) level_kernel(co
             }
 #pragma unroll
             for (int i = 0; i < NIT2; ++i) {
-                if (a.dbg & 2) break;
+                if (kExp && (a.dbg & 2)) break;
                 const int it = grp + NG * i, b = it / (C1 / 16), c0 = (it % (C1 / 16)) * 16;
                 const int ox = x0 + b * 8 + pj;
                 const bool inside = oy < a.H && ox < a.W;
@@ -2086,8 +2121,12 @@ __global__ void __launch_bounds__(128) dec0_ring_kernel(const T* __restrict__ d1
 // first_bad[i] = INT64_MAX ("no frustum error"), PDL-chained so that enc0's
 // prologue overlaps it
 __global__ void fill_first_bad(int64_t* p, int n) {
-    pdl_trigger();
+    // trigger only after the grid dependency resolved: enc0's TMA warp
+    // streams the G-buffer before its own griddepcontrol.wait, so whatever
+    // wrote the G-buffer must be complete and visible once this kernel
+    // lets enc0 start
     pdl_wait();
+    pdl_trigger();
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i < n) p[i] = INT64_MAX;
 }
@@ -2174,11 +2213,8 @@ nsm_status launch_level(const LevelArgs& a, int nf, cudaStream_t st, const char*
     static_assert(G::SMEM <= 232448, "level kernel exceeds 227 KB of shared memory");
     constexpr int NPW = SRC == SRC_TENSOR ? 1 : 12;
     auto k = level_kernel<T, CIN, C3, C1, SRC, DST, NB, NIN, NMID, NPW>;
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, G::SMEM);
-        attr = true;
-    }
+    static PerDevice attr;
+    if (attr.first()) cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, G::SMEM);
     CUtensorMap tin, tlo;
     memset(&tin, 0, sizeof tin);
     memset(&tlo, 0, sizeof tlo);
@@ -2195,15 +2231,17 @@ nsm_status launch_level(const LevelArgs& a, int nf, cudaStream_t st, const char*
     if (!ok) return fail(NSM_ERR_CUDA, "%s: TMA tensor map encoding failed", name);
     const int total = ((a.W + G::TW - 1) / G::TW) * ((a.H + G::TH - 1) / G::TH) * nf;
     const int grid = std::min(total, num_sms());      // TMEM: 512 columns -> one CTA per SM
-    static const int dbg = getenv("NSM_LEVEL_DBG") ? atoi(getenv("NSM_LEVEL_DBG")) : 0;
-    const_cast<LevelArgs&>(a).dbg = dbg;
-    static const char* trace_name = getenv("NSM_LEVEL_TRACE");
+    const_cast<LevelArgs&>(a).dbg = env_int("NSM_LEVEL_DBG", 0);
     static long long* trace_buf = nullptr;
-    const bool trace = trace_name && !strcmp(trace_name, name);
+    bool trace = false;
+#ifdef NSM_EXPERIMENTS
+    static const char* trace_name = getenv("NSM_LEVEL_TRACE");
+    trace = trace_name && !strcmp(trace_name, name);
     if (trace) {
         if (!trace_buf) cudaMalloc(&trace_buf, 32 * 8 * sizeof(long long));
         cudaMemsetAsync(trace_buf, 0, 32 * 8 * sizeof(long long), st);
     }
+#endif
     const_cast<LevelArgs&>(a).trace = trace ? trace_buf : nullptr;
     NSM_PROF(name, st);
     launch_pdl(k, dim3(grid), dim3(lv_threads<SRC, NB, NPW>()), G::SMEM, st, a, tin, tlo, total);
@@ -2313,20 +2351,22 @@ bool encode_gbuf_maps(const GBufK& g, int nf, int h, int w, GbufMaps* m) {
 template <typename T>
 nsm_status run_l0(const Plan& p, const Bufs& b, const Enc0Args& e0, const GbufMaps& tm, int nf, int H0,
                   int W0, int h, int w, void* y, int y_f16, cudaStream_t st, int src) {
-    static bool attr = false;
-    if (!attr) {
+    static PerDevice attr;
+    if (attr.first()) {
         cudaFuncSetAttribute(enc0_kernel<T, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * E0_SMEM);
         cudaFuncSetAttribute(enc0_kernel<T, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * E0_SMEM);
         cudaFuncSetAttribute(enc0_kernel<T, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, ENC0_SMEM_TMA);
-        // setmaxnreg.inc blocks until .dec released enough of the CTA's
-        // launch allocation: refuse to launch a budget that could hang
+    }
+    // setmaxnreg.inc blocks until .dec released enough of the CTA's launch
+    // allocation: refuse to launch a budget that could hang
+    static const int launch_regs = [] {
         cudaFuncAttributes fa{};
         cudaFuncGetAttributes(&fa, enc0_kernel<T, 2>);
-        if (kE0Prod * kE0ProdRegs + (kE0Threads - kE0Prod) * kE0MmaRegs > fa.numRegs * kE0Threads)
-            return fail(NSM_ERR_CUDA, "enc0: register budget %d x %d + %d x %d exceeds launch allocation %d x %d",
-                        kE0Prod, kE0ProdRegs, kE0Threads - kE0Prod, kE0MmaRegs, kE0Threads, fa.numRegs);
-        attr = true;
-    }
+        return fa.numRegs;
+    }();
+    if (kE0Prod * kE0ProdRegs + (kE0Threads - kE0Prod) * kE0MmaRegs > launch_regs * kE0Threads)
+        return fail(NSM_ERR_CUDA, "enc0: register budget %d x %d + %d x %d exceeds launch allocation %d x %d",
+                    kE0Prod, kE0ProdRegs, kE0Threads - kE0Prod, kE0MmaRegs, kE0Threads, launch_regs);
     const int total = ((W0 + E0_TW - 1) / E0_TW) * ((H0 + E0_TH - 1) / E0_TH) * nf;
     const int pgrid = std::min(total, num_sms());
     {
@@ -2342,11 +2382,8 @@ nsm_status run_l0(const Plan& p, const Bufs& b, const Enc0Args& e0, const GbufMa
     {
         // polyphase level-0 decoder on the level-1 grid + the exact outer ring
         const int H1 = H0 / 2, W1 = W0 / 2;
-        static bool pattr = false;
-        if (!pattr) {
-            cudaFuncSetAttribute(dec0p_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, D0P_SMEM);
-            pattr = true;
-        }
+        static PerDevice pattr;
+        if (pattr.first()) cudaFuncSetAttribute(dec0p_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, D0P_SMEM);
         CUtensorMap dm;
         memset(&dm, 0, sizeof dm);
         if (!encode_cplanar_map(b.d1, std::is_same<T, __nv_bfloat16>::value, H1 + 2, W1 + 2, nf, D0P_IC, D0P_IR, &dm))
@@ -2357,7 +2394,7 @@ nsm_status run_l0(const Plan& p, const Bufs& b, const Enc0Args& e0, const GbufMa
             NSM_PROF("dec0_fused", st);
             launch_pdl(dec0p_kernel<T>, dim3(std::min(ptotal, num_sms())), dim3(D0P_THREADS), D0P_SMEM, st, dp, dm, ptotal);
         }
-        static const bool ring = !getenv("NSM_DEC0_RING") || atoi(getenv("NSM_DEC0_RING")) != 0;   // 0: timing only
+        static const bool ring = env_int("NSM_DEC0_RING", 1) != 0;   // 0: timing only (experiments)
         if (ring) {
             const int items = 2 * ((W0 + 29) / 30 + (H0 - 2 + 29) / 30) * nf;
             NSM_PROF("dec0_ring", st);
@@ -2506,7 +2543,7 @@ nsm_status pack_f16(Plan& p, std::vector<char>& blob, size_t& offset_out) {
 
 nsm_status infer_f16(const Plan& p, const nsm_gbuffer* g, const float* sm, int64_t sm_stride,
                      const nsm_frame* frames, int n, int h, int w, void* y, nsm_dtype y_dtype,
-                     int64_t* first_bad, void* ws, size_t ws_bytes, cudaStream_t st) {
+                     int64_t* first_bad, int32_t* texel_idx, void* ws, size_t ws_bytes, cudaStream_t st) {
     if (g->dtype != NSM_F32) return fail(NSM_ERR_UNSUPPORTED, "16-bit path reads fp32 G-buffer planes");
     if (g->z_f || g->c_e || g->c_c || g->coverage)
         return fail(NSM_ERR_UNSUPPORTED, "16-bit path derives z_f/c_e/c_c from the planes");
@@ -2542,8 +2579,8 @@ nsm_status infer_f16(const Plan& p, const nsm_gbuffer* g, const float* sm, int64
         e.b1 = p.lev[0].enc1.b32;
         e.out = b.p1;
         e.first_bad = first_bad + f0;
-        static const int e0dbg = getenv("NSM_ENC0_DBG") ? atoi(getenv("NSM_ENC0_DBG")) : 0;
-        e.dbg = e0dbg;
+        e.tidx = texel_idx ? texel_idx + (int64_t)f0 * 2 * h * w : nullptr;
+        e.dbg = env_int("NSM_ENC0_DBG", 0);
         void* yo = (char*)y + (size_t)f0 * h * w * (y_dtype == NSM_F16 ? 2 : 4);
         GbufMaps tm;
         memset(&tm, 0, sizeof tm);

@@ -33,6 +33,9 @@ __all__ = ["NetworkConfig", "Tensor", "Plan", "receptive_field", "layers_for_pen
            "load_network", "named_params", "level_plan"]
 
 _DTYPES = {"fp32": _lib.NSM_F32, "fp16": _lib.NSM_F16, "bf16": _lib.NSM_BF16}
+_PRECISION = {"fp32": "fp32 (reference precision, CUDA cores)",
+              "fp16": "fp16 activations and weights, fp32 accumulate",
+              "bf16": "bf16 activations and weights, fp32 accumulate"}
 
 
 @dataclass(frozen=True)
@@ -249,6 +252,9 @@ class Plan:
                                             c_dims, _DTYPES[dtype], C.byref(handle)))
         self._h = handle
         self._ws = {}
+        self.precision = _PRECISION[dtype]
+        import torch
+        self.device = torch.cuda.current_device()   # nsm_plan_create allocated here
 
     def __del__(self):
         h = getattr(self, "_h", None)
@@ -260,14 +266,18 @@ class Plan:
     def handle(self):
         return self._h
 
-    def workspace(self, n: int, h: int, w: int, device=None):
+    def workspace(self, n: int, h: int, w: int, device=None, stream=None):
+        """Scratch for nsm_forward / nsm_infer, cached per (device, stream):
+        work enqueued on different streams never shares scratch memory."""
         import torch
+        dev = torch.device("cuda", self.device) if device is None else torch.device(device)
+        if dev.index is not None and dev.index != self.device:
+            raise ValueError(f"plan lives on cuda:{self.device}, not {dev}")
         size = int(_lib.lib.nsm_workspace_size(self._h, n, h, w))
-        dev = torch.device("cuda") if device is None else torch.device(device)
-        key = (dev.index if dev.index is not None else torch.cuda.current_device())
+        key = (self.device, _lib.stream_ptr(stream))
         ws = self._ws.get(key)
         if ws is None or ws.numel() < size:
-            ws = torch.empty(size, dtype=torch.uint8, device=dev)
+            ws = torch.empty(size, dtype=torch.uint8, device=torch.device("cuda", self.device))
             self._ws[key] = ws
         return ws
 
@@ -279,6 +289,8 @@ class Plan:
         x = x.contiguous()
         if x.dtype != torch.float32 or not x.is_cuda:
             raise ValueError("Plan.forward wants an fp32 CUDA tensor")
+        if x.device.index != self.device:
+            raise ValueError(f"plan lives on cuda:{self.device}, input is on {x.device}")
         n, c, h, w = x.shape
         if c != self.cfg.in_channels:
             raise ValueError(f"input has {c} channels, config wants {self.cfg.in_channels}")
@@ -304,7 +316,8 @@ def _fingerprint(weights) -> str:
 def plan_for(weights: dict, cfg: NetworkConfig, dtype: str = "fp32") -> Plan:
     """Cached plan keyed by the weights' content (weights may be mutated
     between calls by training code; a content change re-packs)."""
-    key = (cfg, dtype, _fingerprint(weights))
+    import torch
+    key = (cfg, dtype, torch.cuda.current_device(), _fingerprint(weights))
     p = _PLAN_CACHE.get(key)
     if p is None:
         if len(_PLAN_CACHE) > 16:
@@ -331,6 +344,6 @@ def forward(weights: dict, cfg: NetworkConfig, x, dtype: str = "fp32") -> Tensor
     if hh % f or ww % f:
         raise ValueError(f"spatial dims {hh}x{ww} must be divisible by {f}")
     plan = plan_for(weights, cfg, dtype)
-    xd = torch.from_numpy(np.ascontiguousarray(a)).cuda()
+    xd = torch.from_numpy(np.ascontiguousarray(a)).to(torch.device("cuda", plan.device))
     y = plan.forward(xd[None])
     return Tensor(y[0].cpu().numpy())

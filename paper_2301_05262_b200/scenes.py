@@ -287,6 +287,10 @@ def fit_emitter_view(scene: SceneSpec, center=None, resolution=DEFAULT_SHADOW_RE
 
 LIGHT_POS = (3.0, 5.0, 2.0)
 CAMERA_POS = (0.0, 3.0, -6.0)      # BASELINE leaves it open; recorded in DESIGN.md
+# Fully covered variant: a camera looking steeply down at
+# the ground so every pixel hits geometry, as in a typical game G-buffer.
+FULL_COVER_POS = (0.0, 4.0, -0.6)
+FULL_COVER_TARGET = (0.0, 0.0, 0.4)
 CAMERA_FOV_DEG = 60.0
 GROUND_HALF = 5.0                  # 10 m breaks the frustum fit
 
@@ -334,6 +338,14 @@ def make_frame(scene: SceneSpec, resolution, shadow_res, camera_pos=CAMERA_POS,
                              resolution=tuple(resolution))
     view = fit_emitter_view(scene, resolution=shadow_res)
     return Frame(scene, cam, view)
+
+
+def full_cover(frame: Frame, offset=(0.0, 0.0, 0.0)) -> Frame:
+    """The same scene and light seen by the fully covered camera."""
+    off = np.asarray(offset, dtype=np.float64)
+    return make_frame(frame.scene, frame.camera.resolution, frame.view.resolution,
+                      camera_pos=np.asarray(FULL_COVER_POS) + off,
+                      target=np.asarray(FULL_COVER_TARGET) + off)
 
 
 def config_frames(config: int, seed: int = 0, n_frames: int | None = None) -> list[Frame]:

@@ -103,31 +103,40 @@ def test_batch_equals_single_frames():
 def test_host_pipeline_matches_device_path():
     """HostPipeline (pinned host in/out, overlapped copies, two device slots)
     returns bitwise the device-resident executor's visibility for every
-    batch, including slot reuse, and reports out-of-frustum batches."""
+    batch, including slot reuse and batches that carry their own cameras /
+    emitters, and reports out-of-frustum batches -- also one that was
+    overwritten in its slot before synchronize()."""
     import torch
     from paper_2301_05262_b200 import network, producer, scenes
     from paper_2301_05262_b200._lib import FrustumError
     from paper_2301_05262_b200.infer import HostPipeline, ShadowInference
     cfg, w = _weights()
     plan = network.Plan(w, cfg, "fp16")
-    frames = [scenes.make_frame(scenes.random_scene(8, seed=s), (96, 160), (256, 256)) for s in range(2)]
-    run = ShadowInference(plan, frames, out_dtype="fp16")
-    batches, refs = [], []
-    for b in range(3):   # three batches through two slots
+    batches, refs, poses = [], [], []
+    for b in range(4):   # four batches through two slots, each with its own scenes / cameras
+        frames = [scenes.make_frame(scenes.random_scene(8, seed=10 * b + s, emitter_radius_m=0.05 * b),
+                                    (96, 160), (256, 256), camera_pos=(0.3 * b, 3.0, -6.0 + 0.2 * s))
+                  for s in range(2)]
         inp = producer.render_inputs(frames)
-        inp["position"] = inp["position"] + 0.01 * b * (inp["d"] > 0)[:, None]
-        refs.append(run(inp).cpu().clone())
+        refs.append(ShadowInference(plan, frames, out_dtype="fp16")(inp).cpu().clone())
         batches.append({k: v.cpu().pin_memory() for k, v in inp.items()})
+        poses.append(frames)
+    run = ShadowInference(plan, poses[0], out_dtype="fp16")
     pipe = HostPipeline(run)
     outs = [torch.empty(run.y.shape, dtype=run.y.dtype, pin_memory=True) for _ in batches]
-    for hb, ho in zip(batches, outs):
-        pipe.submit(hb, ho)
+    for hb, ho, fr in zip(batches, outs, poses):
+        pipe.submit(hb, ho, frames=fr)
     pipe.synchronize()
     for ho, ref in zip(outs, refs):
         torch.testing.assert_close(ho, ref, rtol=0, atol=0)
     bad = {k: v.clone() for k, v in batches[0].items()}
     bad["position"][0, 0] += 1e4 * (bad["d"][0] > 0)      # far outside the emitter frustum
-    pipe.submit(bad, outs[0])
+    pipe.submit(bad, outs[0], frames=poses[0])             # batch 4: fails
+    pipe.submit(batches[1], outs[1], frames=poses[1])      # batch 5
+    with pytest.raises(FrustumError, match="batch 4 frame 0"):
+        pipe.submit(batches[2], outs[2], frames=poses[2])  # reuses batch 4's slot
+    pipe.synchronize()
+    pipe.submit(bad, outs[0], frames=poses[0])
     with pytest.raises(FrustumError):
         pipe.synchronize()
 

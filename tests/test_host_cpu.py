@@ -23,7 +23,9 @@ def test_library_exports_every_header_symbol():
     assert len(syms) >= 11
     for s in syms:
         assert hasattr(_lib.lib, s), s
-    assert _lib.lib.nsm_abi_version() == 1
+    assert _lib.lib.nsm_abi_version() == _lib.ABI_VERSION == 2
+    # the release library ignores NSM_* switches (experiment builds only)
+    assert not _lib.experiment_build()
 
 
 def test_receptive_field_and_depth_kats():
