@@ -153,6 +153,18 @@ nsm_status nsm_blocker_plane(const nsm_gbuffer* g, const float* sm, int64_t sm_s
                              const nsm_frame* frames, int32_t n, int32_t h, int32_t w,
                              int32_t radius, float* out, int64_t* first_bad, void* stream);
 
+/* ---- stage 1 of the 5-plane net: the 4 planes + the blocker plane ----
+ * The feature pass of NetworkConfig(in_channels=5) plans (BASELINE configs
+ * 3/4 "soft shadows"): the 4 planes of assemble_features plus the blocker-
+ * search penumbra plane (definition as nsm_blocker_plane, radius 8: a 16 x 16
+ * texel window), in one pass with the map windows staged in shared memory.
+ * out_planes: (n, 5, h, w) fp32 device.  Planes 0-3 use the fused hot path's
+ * fp32 arithmetic (nsm_features is the fp64-faithful 4-plane drop-in);
+ * texel_idx / first_bad as nsm_infer_ex / nsm_features. */
+nsm_status nsm_features5(const nsm_gbuffer* g, const float* sm, int64_t sm_stride,
+                         const nsm_frame* frames, int32_t n, int32_t h, int32_t w,
+                         float* out_planes, int32_t* texel_idx, int64_t* first_bad, void* stream);
+
 /* ---- stage 2: network.forward (network.py:165-209) ----
  * x: (n, in_channels, h, w) fp32 device, y: (n, 1, h, w) fp32 device.
  * h, w must be divisible by 2**(layers-1) (NSM_ERR_SHAPE otherwise). */
@@ -161,7 +173,9 @@ nsm_status nsm_forward(const nsm_plan* plan, const float* x, int32_t n, int32_t 
 
 /* ---- fused stages 1+2: the hot path ----
  * assemble_features then forward per frame, features never written to HBM
- * on the fp16/bf16 plans.  h need not be divisible by 2**(layers-1): rows /
+ * on the fp16/bf16 plans of 4-plane nets.  A NetworkConfig(in_channels=5)
+ * plan (16-bit only) adds the blocker-search plane (nsm_features5); its
+ * feature pass writes a 16-bit s2d tensor that the level-0 encoder reads.  h need not be divisible by 2**(layers-1): rows /
  * columns up to the next multiple are treated as uncovered (zero features,
  * the same padding the oracle applies) and cropped from y.  y: (n, 1, h, w)
  * of y_dtype (NSM_F32 or NSM_F16). */

@@ -81,6 +81,9 @@ _EXPORTS = {
     "nsm_blocker_plane": (C.c_int, [C.POINTER(GBufferC), C.c_void_p, C.c_int64, C.POINTER(FrameC),
                                     C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_void_p, C.c_void_p,
                                     C.c_void_p]),
+    "nsm_features5": (C.c_int, [C.POINTER(GBufferC), C.c_void_p, C.c_int64, C.POINTER(FrameC),
+                                C.c_int32, C.c_int32, C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p,
+                                C.c_void_p]),
     "nsm_forward": (C.c_int, [C.POINTER(PlanHandle), C.c_void_p, C.c_int32, C.c_int32,
                               C.c_int32, C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p]),
     "nsm_infer": (C.c_int, [C.POINTER(PlanHandle), C.POINTER(GBufferC), C.c_void_p, C.c_int64,

@@ -54,7 +54,7 @@ def _compile(src):
     # fast-math only where it is harmless: the parity kernels keep IEEE
     # division/sqrt (features.cu, net_f32.cu, producer.cu, abi.cu)
     flags = [f for f in FLAGS if f != "--use_fast_math"] if src in (
-        "features.cu", "net_f32.cu", "producer.cu", "abi.cu", "temporal.cu") else FLAGS
+        "features.cu", "net_f32.cu", "producer.cu", "abi.cu", "temporal.cu", "feat5.cu") else FLAGS
     if EXPERIMENTS:
         flags = flags + ["-DNSM_EXPERIMENTS"]
     cmd = [NVCC, *ARCH, *flags, "-c", path, "-o", obj]

@@ -176,15 +176,15 @@ __global__ void crop_kernel(const float* __restrict__ src, int hp, int wp, int h
 }
 
 // Every frame of a batch must describe the (h, w) frames the planes hold
-// and a shadow map that fits its sm_stride slot: the kernels index the map
-// with each frame's own resolution.
+// and a shadow map that fits its sm_stride slot (the kernels index the map
+// with each frame's own resolution; a single frame needs no stride).
 nsm_status check_frames(const nsm_frame* frames, int32_t n, int32_t h, int32_t w, int64_t sm_stride) {
     for (int i = 0; i < n; ++i) {
         const nsm_frame& f = frames[i];
         if (f.camera.height != h || f.camera.width != w)
             return fail(NSM_ERR_ARG, "frame %d: camera is %dx%d but the G-buffer planes are %dx%d", i,
                         f.camera.height, f.camera.width, h, w);
-        if (f.view.height <= 0 || f.view.width <= 0 || (int64_t)f.view.height * f.view.width > sm_stride)
+        if (f.view.height <= 0 || f.view.width <= 0 || (n > 1 && (int64_t)f.view.height * f.view.width > sm_stride))
             return fail(NSM_ERR_ARG, "frame %d: a %dx%d shadow map does not fit sm_stride %lld", i,
                         f.view.height, f.view.width, (long long)sm_stride);
     }
@@ -389,6 +389,30 @@ nsm_status nsm_blocker_plane(const nsm_gbuffer* g, const float* sm, int64_t sm_s
     return launch_blocker(g, sm, sm_stride, frames, n, h, w, radius, out, first_bad, (cudaStream_t)stream);
 }
 
+nsm_status nsm_features5(const nsm_gbuffer* g, const float* sm, int64_t sm_stride, const nsm_frame* frames,
+                         int32_t n, int32_t h, int32_t w, float* out_planes, int32_t* texel_idx,
+                         int64_t* first_bad, void* stream) {
+    clear_error();
+    if (!g || !sm || !frames || !out_planes || !first_bad || !g->d || !g->normal || !g->position)
+        return fail(NSM_ERR_ARG, "nsm_features5: null argument");
+    if (n <= 0 || h <= 0 || w <= 0) return fail(NSM_ERR_ARG, "nsm_features5: empty batch");
+    if (nsm_status s = check_frames(frames, n, h, w, sm_stride)) return s;
+    cudaStream_t st = (cudaStream_t)stream;
+    launch_fill_i64(first_bad, n, INT64_MAX, st);
+    for (int f0 = 0; f0 < n; f0 += NSM_MAX_FRAMES_PER_LAUNCH) {
+        const int nf = std::min(n - f0, NSM_MAX_FRAMES_PER_LAUNCH);
+        nsm_gbuffer gc = *g;
+        gc.d = (const float*)g->d + (int64_t)f0 * g->frame_stride;
+        gc.normal = (const float*)g->normal + (int64_t)f0 * 3 * g->frame_stride;
+        gc.position = (const float*)g->position + (int64_t)f0 * 3 * g->frame_stride;
+        nsm_status s = launch_feat5(&gc, sm + f0 * sm_stride, sm_stride, frames + f0, nf, h, w, 0, 0,
+                                    out_planes + (int64_t)f0 * 5 * h * w, 2, first_bad + f0,
+                                    texel_idx ? texel_idx + (int64_t)f0 * 2 * h * w : nullptr, st);
+        if (s != NSM_OK) return s;
+    }
+    return check_stream_err();
+}
+
 nsm_status nsm_forward(const nsm_plan* plan, const float* x, int32_t n, int32_t h, int32_t w,
                        float* y, void* workspace, size_t ws_bytes, void* stream) {
     clear_error();
@@ -425,7 +449,12 @@ nsm_status nsm_infer_ex(const nsm_plan* plan, const nsm_gbuffer* g, const float*
         return fail(NSM_ERR_ARG, "nsm_infer: null argument");
     if (n <= 0 || h <= 0 || w <= 0) return fail(NSM_ERR_ARG, "nsm_infer: empty batch");
     if (y_dtype != NSM_F32 && y_dtype != NSM_F16) return fail(NSM_ERR_ARG, "y_dtype must be F32 or F16");
-    if (p->cfg.in_channels != 4)
+    // the feature pass produces the 4 reference planes, plus the
+    // blocker-search penumbra plane for in_channels = 5 nets (16-bit plans)
+    if (p->cfg.in_channels == 5 && p->act == NSM_F32)
+        return fail(NSM_ERR_UNSUPPORTED, "fp32 plans run the 4-plane feature pass; a 5-plane net needs a 16-bit "
+                                         "plan (or nsm_features5 + nsm_forward)");
+    if (p->cfg.in_channels != 4 && p->cfg.in_channels != 5)
         return fail(NSM_ERR_SHAPE, "input has 4 channels, config wants %d", p->cfg.in_channels);
     if (g->dtype != NSM_F32 && g->dtype != NSM_F64)
         return fail(NSM_ERR_ARG, "G-buffer planes must be F32 or F64");

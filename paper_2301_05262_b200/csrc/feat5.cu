@@ -1,0 +1,332 @@
+// Stage 1 of the 5-plane network (BASELINE configs 3/4, "soft shadows" with
+// the 16x16 blocker search): the 4 reference feature planes
+// (raster.assemble_features, raster.py:266-278) plus the blocker-search
+// penumbra plane (nsm.h nsm_blocker_plane; analysis.py:240-269, 319-320), in
+// one pass over the G-buffer.
+//
+// Layout: one CTA per 8 x 32 level-0 tile (16 x 64 frame pixels), one thread
+// per level-0 pixel (its 2 x 2 frame pixels).  The texel windows of the
+// tile's covered pixels are bounded by their texel bounding box; that map
+// region is staged in shared memory (rows of the map, coalesced), and the
+// sliding 4 x 4 min / max of every staged position is built from it, so a
+// pixel's 16 x 16 window is 16 sub-blocks:
+//   zmin = min of the 16 block minima (the window minimum: a blocker exists
+//          iff it is below the threshold, and then it is the blocker minimum)
+//   block max < thr        -> every texel is a blocker: zmax candidate = max
+//   block min >= thr       -> no blocker in the block
+//   otherwise (straddling) -> its 16 texels are scanned
+// Depths are positive floats (or +inf), so they are compared as int32; the
+// threshold test and the blocker maximum fold into one DPX instruction per
+// texel: min_u32((thr - 1) - t) over the block is (thr - 1) - (max blocker).
+// The shadow map is read from HBM about once per tile; the window traffic is
+// shared-memory traffic (the roofline that bounds this kernel).
+//
+// Outputs: the hot path's level-0 input tensor, 16-bit, chunk-planar
+// (N, 3, H0, W0, 8): chunks 0-1 the space_to_depth of the 4 planes in the
+// permuted order l0.enc3's packing expects (k' = (2dy + dx) * 4 + c), chunk 2
+// the 4 blocker values of the pixel's 2 x 2 (s2d channels 16-19) and zeros;
+// or (parity / drop-in mode) fp32 planes (N, 5, h, w).
+#include <algorithm>
+#include <cfloat>
+
+#include "common.cuh"
+#include "net.cuh"
+#include "prof.cuh"
+#include "tc.cuh"
+
+namespace nsm {
+
+namespace {
+
+constexpr int F5_TY = 8, F5_TX = 32, F5_THREADS = F5_TY * F5_TX;
+constexpr int F5_R = 8;                      // window rows ri-8 .. ri+7 (16 x 16)
+constexpr int F5_MAX_TEX = 3072;             // staged texels per CTA (region + 2 block maps: 36 KB)
+constexpr int F5_SMEM = F5_MAX_TEX * 4 + F5_MAX_TEX * 8;
+constexpr int kInfBits = 0x7f800000;
+
+struct Feat5Args {
+    GBufK g;
+    const float* sm;
+    int64_t sm_stride;
+    FrameTable tab;
+    int h, w;          // frame pixels present
+    int H0, W0;        // level-0 grid (padded frame / 2)
+    void* out;         // 16-bit (N, 3, H0, W0, 8) or fp32 (N, 5, h, w)
+    int64_t* first_bad;
+    int32_t* tidx;     // parity hook (nullable): (N, 2, h, w)
+};
+
+// analysis.penumbra_extents (analysis.py:240-269) -> screen width
+// (x_a + x_b) * focal_px / d (analysis.py:319-320), fp32 (the plane is
+// rounded to 16 bits right after); 0 where the model's preconditions fail.
+__device__ __forceinline__ float penumbra_width_f(float zmin, float zmax, float zf, float re, float focal,
+                                                  float d) {
+    const float zm = 0.5f * (zmax + zmin), rs = 0.5f * (zmax - zmin);
+    const float hyp = sqrtf(zm * zm + re * re);
+    if (!(zmin > 0.f && zmax >= zmin && zf > zmax && zm > 0.f && rs <= hyp && re > 0.f)) return 0.f;
+    const float td = asinf(rs / hyp);
+    const float bq = re * (zf - zm) / zm;
+    const float th = atanf((bq + re) / zf);
+    if (!(th + td < 1.5707963267948966f)) return 0.f;
+    const float xa = zf * tanf(th - td) - re, xb = zf * tanf(th + td) - re;
+    return (xa + xb) * focal / d;
+}
+
+template <typename T, bool kF32>
+__global__ void __launch_bounds__(F5_THREADS) feat5_kernel(const __grid_constant__ Feat5Args a) {
+    extern __shared__ __align__(16) int smem5[];
+    __shared__ int bb[4];
+    const int f = blockIdx.z;
+    const int tid = threadIdx.x;
+    const int X = blockIdx.x * F5_TX + (tid & 31), Y = blockIdx.y * F5_TY + (tid >> 5);
+    const FrameK& F = a.tab.f[f];
+    if (tid == 0) {
+        bb[0] = INT32_MAX;
+        bb[1] = INT32_MIN;
+        bb[2] = INT32_MAX;
+        bb[3] = INT32_MIN;
+    }
+    const int64_t hw = (int64_t)a.h * a.w;
+    const int64_t base = (int64_t)f * a.g.frame_stride;
+    const float* gd = reinterpret_cast<const float*>(a.g.d) + base;
+    const float* gp = reinterpret_cast<const float*>(a.g.position) + 3 * base;
+    const float* gn = reinterpret_cast<const float*>(a.g.normal) + 3 * base;
+    // the 2 x 2 frame pixels of this level-0 pixel, e = 2 dy + dx
+    float dv[4], pxv[4], pyv[4], pzv[4], nxv[4], nyv[4], nzv[4];
+    int ri[4], ci[4];
+    bool cov[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+        const int y = 2 * Y + (e >> 1), x = 2 * X + (e & 1);
+        const bool in = y < a.h && x < a.w;
+        const int64_t p = (int64_t)y * a.w + x;
+        dv[e] = in ? __ldg(gd + p) : 0.f;
+        cov[e] = dv[e] > 0.f;
+        pxv[e] = pyv[e] = pzv[e] = nxv[e] = nyv[e] = nzv[e] = 0.f;
+        ri[e] = ci[e] = 0;
+        if (cov[e]) {
+            pxv[e] = __ldg(gp + p);
+            pyv[e] = __ldg(gp + hw + p);
+            pzv[e] = __ldg(gp + 2 * hw + p);
+            nxv[e] = __ldg(gn + p);
+            nyv[e] = __ldg(gn + hw + p);
+            nzv[e] = __ldg(gn + 2 * hw + p);
+        }
+    }
+    int rlo = INT32_MAX, rhi = INT32_MIN, clo = INT32_MAX, chi = INT32_MIN;
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+        if (!cov[e]) continue;
+        const bool ok = texel_fused(F, pxv[e], pyv[e], pzv[e], ri[e], ci[e]);
+        const int y = 2 * Y + (e >> 1), x = 2 * X + (e & 1);
+        if (!ok) atomic_min_i64(a.first_bad + f, (int64_t)y * a.w + x);
+        if (a.tidx) {
+            int32_t* ti = a.tidx + (int64_t)f * 2 * hw + (int64_t)y * a.w + x;
+            ti[0] = ri[e];
+            ti[hw] = ci[e];
+        }
+        rlo = min(rlo, ri[e]);
+        rhi = max(rhi, ri[e]);
+        clo = min(clo, ci[e]);
+        chi = max(chi, ci[e]);
+    }
+    rlo = __reduce_min_sync(0xffffffffu, rlo);
+    rhi = __reduce_max_sync(0xffffffffu, rhi);
+    clo = __reduce_min_sync(0xffffffffu, clo);
+    chi = __reduce_max_sync(0xffffffffu, chi);
+    __syncthreads();   // bb initialised
+    if ((tid & 31) == 0 && rlo <= rhi) {
+        atomicMin(&bb[0], rlo);
+        atomicMax(&bb[1], rhi);
+        atomicMin(&bb[2], clo);
+        atomicMax(&bb[3], chi);
+    }
+    __syncthreads();
+    const bool any = bb[0] <= bb[1];
+    // region: window rows rlo-8 .. rhi+7, cols clo-8 .. chi+7 (+inf off the map)
+    const int R0 = bb[0] - F5_R, C0 = bb[2] - F5_R;
+    const int RH = bb[1] - bb[0] + 2 * F5_R, RW = bb[3] - bb[2] + 2 * F5_R;
+    const bool staged = any && RH * RW <= F5_MAX_TEX;
+    const float* smf = a.sm + (int64_t)f * a.sm_stride;
+    int* reg = smem5;                                   // [RH][RW] depth bits
+    int2* blk = reinterpret_cast<int2*>(smem5 + F5_MAX_TEX);   // [RH-3][RW-3] sliding 4x4 (min, max)
+    if (staged) {
+        for (int i = tid; i < RH * RW; i += F5_THREADS) {
+            const int r = R0 + i / RW, c = C0 + i % RW;
+            const bool in = r >= 0 && r < F.hs && c >= 0 && c < F.ws;
+            reg[i] = in ? __float_as_int(__ldg(smf + (int64_t)r * F.ws + c)) : kInfBits;
+        }
+        __syncthreads();
+        const int BW = RW - 3, BH = RH - 3;
+        for (int i = tid; i < BH * BW; i += F5_THREADS) {
+            const int r = i / BW, c = i % BW;
+            int mn = kInfBits, mx = 0;
+#pragma unroll
+            for (int dy = 0; dy < 4; ++dy) {
+                const int* row = reg + (r + dy) * RW + c;
+                mn = __vimin3_s32(row[0], row[1], mn);
+                mn = __vimin3_s32(row[2], row[3], mn);
+                mx = __vimax3_s32(row[0], row[1], mx);
+                mx = __vimax3_s32(row[2], row[3], mx);
+            }
+            blk[i] = make_int2(mn, mx);
+        }
+        __syncthreads();
+    }
+
+    // per pixel: the 4 reference planes (fp32 math as the fused 4-plane
+    // producer) and the blocker plane
+    float feat[4][5];
+    const double bias = F.bias;
+    const float re = (float)(F.size_index * (0.5 / 2.0 / 4.0));       // scene.emitter_radius
+    const float focal = (float)((F.ch / 2.0) / F.half_h);              // CameraPose.focal_px
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+#pragma unroll
+        for (int k = 0; k < 5; ++k) feat[e][k] = 0.f;
+        if (!cov[e]) continue;
+        // z_f in fp64 as render_gbuffer (raster.py:228): the blocker test
+        // t < z_f - b must classify exactly like the fp64 oracle
+        const double tx = F.ec[0] - (double)pxv[e], ty = F.ec[1] - (double)pyv[e], tz = F.ec[2] - (double)pzv[e];
+        const double zf64 = sqrt(__dadd_rn(__dadd_rn(__dmul_rn(tx, tx), __dmul_rn(ty, ty)), __dmul_rn(tz, tz)));
+        const float zf = (float)zf64;
+        const float izf = 1.f / zf;
+        const float ftx = (float)tx, fty = (float)ty, ftz = (float)tz;
+        const float ce = __saturatef((nxv[e] * ftx + nyv[e] * fty + nzv[e] * ftz) * izf);
+        const float dx = F.fcp[0] - pxv[e], dy = F.fcp[1] - pyv[e], dz = F.fcp[2] - pzv[e];
+        const float cc = __saturatef((nxv[e] * dx + nyv[e] * dy + nzv[e] * dz) * rsqrtf(dx * dx + dy * dy + dz * dz));
+        const int tr = ri[e], tc = ci[e];
+        const float look = staged ? __int_as_float(reg[(tr - R0) * RW + (tc - C0)])
+                                  : __ldg(smf + (int64_t)tr * F.ws + tc);
+        float ch0 = 0.f, ch1 = 1.f;
+        if (look < INFINITY) {                                       // raster.py:262
+            const float m = fminf(look, zf);
+            ch0 = (m - zf) + F.fbias;
+            ch1 = (m + F.fbias) * izf;
+        }
+        feat[e][0] = ch0;
+        feat[e][1] = ch1;
+        feat[e][2] = ce + F.fsize;
+        feat[e][3] = cc / dv[e];
+        // blocker search over rows tr-8 .. tr+7, cols tc-8 .. tc+7
+        const int thr = __float_as_int(__double2float_ru(zf64 - bias));   // t < thr64 <=> t < thr (fp32 t)
+        const unsigned thr1 = (unsigned)thr - 1u;
+        int zmin = kInfBits;
+        unsigned um = 0xffffffffu;
+        if (staged) {
+            const int r0 = tr - F5_R - R0, c0 = tc - F5_R - C0, BW = RW - 3;
+            unsigned strad = 0;
+#pragma unroll
+            for (int b = 0; b < 16; ++b) {
+                const int2 mm = blk[(r0 + 4 * (b >> 2)) * BW + c0 + 4 * (b & 3)];
+                zmin = min(zmin, mm.x);
+                if (mm.y < thr) um = min(um, thr1 - (unsigned)mm.y);       // all blockers
+                else if (mm.x < thr) strad |= 1u << b;                    // straddles the threshold
+            }
+            while (strad) {
+                const int b = __ffs(strad) - 1;
+                strad &= strad - 1;
+                const int* p = reg + (r0 + 4 * (b >> 2)) * RW + c0 + 4 * (b & 3);
+#pragma unroll
+                for (int dy = 0; dy < 4; ++dy)
+#pragma unroll
+                    for (int dxx = 0; dxx < 4; ++dxx)
+                        um = __viaddmin_u32(thr1, (unsigned)(-p[dy * RW + dxx]), um);
+            }
+        } else {
+            // region too large for shared memory (grazing views): the same
+            // scan straight from global memory
+            for (int r = tr - F5_R; r < tr + F5_R; ++r) {
+                if (r < 0 || r >= F.hs) continue;
+                for (int c = tc - F5_R; c < tc + F5_R; ++c) {
+                    if (c < 0 || c >= F.ws) continue;
+                    const int t = __float_as_int(__ldg(smf + (int64_t)r * F.ws + c));
+                    zmin = min(zmin, t);
+                    um = __viaddmin_u32(thr1, (unsigned)(-t), um);
+                }
+            }
+        }
+        if (zmin < thr) {                                          // blockers exist
+            const float zmx = __int_as_float((int)(thr1 - um));
+            feat[e][4] = penumbra_width_f(__int_as_float(zmin), zmx, zf, re, focal, dv[e]);
+        }
+    }
+
+    if constexpr (kF32) {
+        float* o = reinterpret_cast<float*>(a.out) + (int64_t)f * 5 * hw;
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+            const int y = 2 * Y + (e >> 1), x = 2 * X + (e & 1);
+            if (y >= a.h || x >= a.w) continue;
+            const int64_t p = (int64_t)y * a.w + x;
+#pragma unroll
+            for (int k = 0; k < 5; ++k) o[k * hw + p] = feat[e][k];
+        }
+    } else {
+    if (Y >= a.H0 || X >= a.W0) return;
+    T* o = reinterpret_cast<T*>(a.out);
+    const int64_t plane = (int64_t)a.H0 * a.W0 * 8;
+    const int64_t at = ((int64_t)f * 3 * a.H0 * a.W0 + (int64_t)Y * a.W0 + X) * 8;
+    uint4 c0, c1, c2;
+    c0.x = Elem<T>::pack(feat[0][0], feat[0][1]);
+    c0.y = Elem<T>::pack(feat[0][2], feat[0][3]);
+    c0.z = Elem<T>::pack(feat[1][0], feat[1][1]);
+    c0.w = Elem<T>::pack(feat[1][2], feat[1][3]);
+    c1.x = Elem<T>::pack(feat[2][0], feat[2][1]);
+    c1.y = Elem<T>::pack(feat[2][2], feat[2][3]);
+    c1.z = Elem<T>::pack(feat[3][0], feat[3][1]);
+    c1.w = Elem<T>::pack(feat[3][2], feat[3][3]);
+    // 16-bit range: a degenerate penumbra (theta + theta_d -> pi/2) saturates
+    auto sat = [](float v) { return fminf(fmaxf(v, -60000.f), 60000.f); };
+    c2.x = Elem<T>::pack(sat(feat[0][4]), sat(feat[1][4]));
+    c2.y = Elem<T>::pack(sat(feat[2][4]), sat(feat[3][4]));
+    c2.z = 0u;
+    c2.w = 0u;
+    *reinterpret_cast<uint4*>(o + at) = c0;
+    *reinterpret_cast<uint4*>(o + at + plane) = c1;
+    *reinterpret_cast<uint4*>(o + at + 2 * plane) = c2;
+    }
+}
+
+}  // namespace
+
+// 16-bit mode: x5 = (nf, 3, H0, W0, 8) of the chunk's frames (fp16 / bf16);
+// fp32 mode: planes (nf, 5, h, w).  first_bad must be pre-filled.
+nsm_status launch_feat5(const nsm_gbuffer* g, const float* sm, int64_t sm_stride, const nsm_frame* frames,
+                        int nf, int h, int w, int H0, int W0, void* out, int out_kind, int64_t* first_bad,
+                        int32_t* tidx, cudaStream_t st) {
+    if (g->dtype != NSM_F32 || g->z_f || g->c_e || g->c_c || g->coverage)
+        return fail(NSM_ERR_UNSUPPORTED, "the 5-plane feature pass reads fp32 d / normal / position planes");
+    if (nf > NSM_MAX_FRAMES_PER_LAUNCH) return fail(NSM_ERR_ARG, "launch_feat5: too many frames");
+    Feat5Args a{};
+    a.g = GBufK{g->d, g->normal, g->position, nullptr, nullptr, nullptr, nullptr, g->frame_stride};
+    a.sm = sm;
+    a.sm_stride = sm_stride;
+    make_frame_table(frames, nf, a.tab);
+    a.h = h;
+    a.w = w;
+    a.H0 = H0;
+    a.W0 = W0;
+    a.out = out;
+    a.first_bad = first_bad;
+    a.tidx = tidx;
+    // 16-bit: every level-0 pixel of the padded grid; fp32: the frame's pixels
+    const int LX = out_kind == 2 ? (w + 1) / 2 : W0, LY = out_kind == 2 ? (h + 1) / 2 : H0;
+    dim3 grid((LX + F5_TX - 1) / F5_TX, (LY + F5_TY - 1) / F5_TY, nf);
+    static_assert(F5_SMEM <= 48 * 1024, "feat5 fits the default dynamic shared-memory limit");
+    NSM_PROF("feat5_blocker", st);
+    switch (out_kind) {
+        case 0:
+            feat5_kernel<__half, false><<<grid, F5_THREADS, F5_SMEM, st>>>(a);
+            break;
+        case 1:
+            feat5_kernel<__nv_bfloat16, false><<<grid, F5_THREADS, F5_SMEM, st>>>(a);
+            break;
+        default:
+            feat5_kernel<float, true><<<grid, F5_THREADS, F5_SMEM, st>>>(a);
+            break;
+    }
+    return NSM_OK;
+}
+
+}  // namespace nsm

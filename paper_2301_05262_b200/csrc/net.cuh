@@ -61,6 +61,12 @@ nsm_status launch_features(const nsm_gbuffer* g, const float* sm, int64_t sm_str
                            int32_t wo, float* out, int32_t* tidx, int64_t* first_bad,
                            cudaStream_t st);
 void launch_fill_i64(int64_t* p, int n, int64_t v, cudaStream_t st);
+// feat5.cu: the 4 planes + the blocker-search penumbra plane.  out_kind 0/1:
+// fp16 / bf16 chunk-planar level-0 tensor (nf, 3, H0, W0, 8); 2: fp32 planes
+// (nf, 5, h, w).  first_bad pre-filled by the caller.
+nsm_status launch_feat5(const nsm_gbuffer* g, const float* sm, int64_t sm_stride, const nsm_frame* frames,
+                        int nf, int h, int w, int H0, int W0, void* out, int out_kind, int64_t* first_bad,
+                        int32_t* tidx, cudaStream_t st);
 nsm_status launch_blocker(const nsm_gbuffer* g, const float* sm, int64_t sm_stride, const nsm_frame* frames,
                           int32_t n, int32_t h, int32_t w, int32_t radius, float* out, int64_t* first_bad,
                           cudaStream_t st);

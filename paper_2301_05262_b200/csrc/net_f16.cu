@@ -124,8 +124,10 @@ size_t frag_words(int taps, int cin, int cout) {
 // l0.enc3 reads a tile whose channel k' = (2dy + dx) * 4 + c holds s2d
 // channel 4c + 2dy + dx (space_to_depth, autodiff.py:290-308), so each
 // full-resolution pixel writes its 4 features contiguously.
+// With a 5th plane (cin4 = 20) the first 16 channels keep this order and
+// channels 16-19 (the blocker plane's 2 x 2) follow in s2d order.
 int perm_s2d(int kp, int cin4) {
-    if (cin4 != 16) return kp;
+    if ((cin4 != 16 && cin4 != 20) || kp >= 16) return kp;
     return 4 * (kp % 4) + kp / 4;
 }
 
@@ -536,7 +538,7 @@ struct QuadPark {
     uint2 v[4];
 };
 
-template <typename T>
+template <typename T, bool kIdx>
 __device__ __forceinline__ void produce_features_tma(const Enc0Args& a, const GbufMaps& tm, int total) {
     // Software pipeline over half-tiles q (two per tile):
     //   A(q): staged planes -> texel (fp64), z_f, (c_e + s, c_c / d) packed,
@@ -638,7 +640,7 @@ __device__ __forceinline__ void produce_features_tma(const Enc0Args& a, const Gb
             const bool ok = texel_fused(F, px, py, pz, ri, ci);
             bad |= (cov && !ok) << e;
             R.look[e] = cov ? __ldg(a.sm + (sm_off + ri * ws + ci)) : -1.f;   // consumed one phase later
-            if (a.tidx && cov) {      // parity hook: the texel this pixel gathered
+            if (kIdx && cov) {      // parity hook (own kernel variant): the texel this pixel gathered
                 const int64_t hw = (int64_t)a.h * a.w;
                 int32_t* ti = a.tidx + (int64_t)tl.f * 2 * hw +
                               (int64_t)(2 * tl.ty0 - 2 + ST_ROWS * (q & 1) + qy) * a.w +
@@ -716,7 +718,10 @@ __device__ __forceinline__ void produce_features_tma(const Enc0Args& a, const Gb
     }
 }
 
-template <typename T, int kSrc>   // kSrc: 0 = features planes, 1 = G-buffer (LDG), 2 = G-buffer (TMA)
+// kSrc: 0 = features planes, 1 = G-buffer (LDG), 2 = G-buffer (TMA).  kIdx:
+// the parity-hook variant that also writes each covered pixel's texel index
+// (a separate instantiation, so the production kernel keeps its registers).
+template <typename T, int kSrc, bool kIdx = false>
 __global__ void __launch_bounds__(kSrc == 2 ? kE0Threads : kL0Threads, 1) enc0_kernel(
     const __grid_constant__ Enc0Args a, const __grid_constant__ GbufMaps tm, int total) {
     constexpr int kProd = kSrc == 2 ? kE0Prod : kL0Prod;
@@ -747,7 +752,7 @@ __global__ void __launch_bounds__(kSrc == 2 ? kE0Threads : kL0Threads, 1) enc0_k
     constexpr int kRows = kSrc == 2 ? 16 : 8;        // output rows per consumer warp
     if (threadIdx.x < kProd) {
         if (kSrc == 2) {
-            produce_features_tma<T>(a, tm, total);
+            produce_features_tma<T, kIdx>(a, tm, total);
         } else {
             l0_produce_loop(total, [&](uint8_t* buf, int tile) {
                 produce_features<T, kSrc == 1>(a, buf, l0_tile(tile, a.td));
@@ -794,7 +799,7 @@ __global__ void __launch_bounds__(kSrc == 2 ? kE0Threads : kL0Threads, 1) enc0_k
             const int px = ((tl.tx0 + sx) >> 1) + g;
             const bool px_ok = px < W1;
             T* obase = out + (((int64_t)tl.f * H1 + ((tl.ty0 + r0) >> 1)) * W1 + px) * 16 + 2 * t;
-            if (kExp && (a.dbg & 2)) {
+            if (a.dbg & 2) {          // experiments only (dbg is 0 in release builds)
                 hook(E0_IR / 2);
                 return;
             }
@@ -848,6 +853,232 @@ __global__ void __launch_bounds__(kSrc == 2 ? kE0Threads : kL0Threads, 1) enc0_k
     } else {
         l0_consume_loop<kThreads>(total, [&](uint8_t* buf, int tile) { consume(buf, tile, NoRowHook{}); });
     }
+}
+
+// ------------------------------------------------ level 0 of the 5-plane net
+// enc0_s2d: l0.enc3 (20 -> 16, 3x3) + l0.enc1 + avg_pool2 from the 16-bit
+// chunk-planar s2d tensor (N, 3, H0, W0, 8) written by feat5_kernel (the 4
+// reference planes and the blocker-search plane).  A TMA warp streams halo'd
+// 18 x 66 tiles (three 22-pixel boxes: a TMA box row holds at most 256
+// elements) into a 3-stage ring; 8 warps run the convolutions: the K = 16
+// chunks 0-1 as m16n8k16 and chunk 2 (4 blocker channels + 4 zero) as
+// m16n8k8 per tap, the rest exactly as enc0 (pair-row pixel order, enc1 on
+// the accumulator as A fragment, the 2x2 pool in registers).
+constexpr int S24_BOXW = 22, S24_NBOX = 3;
+static_assert(S24_BOXW * S24_NBOX == E0_IC, "boxes tile the halo'd row");
+constexpr int S24_ROWB = S24_BOXW * 16;               // one box row of one chunk
+constexpr int S24_CSTR = E0_IR * S24_ROWB;             // one chunk of one box
+constexpr int S24_BOXB = 3 * S24_CSTR;                 // one box, 3 chunks
+constexpr int S24_TILE = S24_NBOX * S24_BOXB;          // 57,024 B per tile
+constexpr int S24_NS = 3;                              // ring stages
+constexpr int kS24Mma = 8, kS24Threads = 32 * (kS24Mma + 1);
+constexpr int S24_SMEM = S24_NS * S24_TILE + 64;
+
+__device__ __forceinline__ void ldsm_x2(uint32_t addr, uint32_t r[2]) {
+    asm volatile("ldmatrix.sync.aligned.m8n8.x2.shared.b16 {%0,%1}, [%2];\n" : "=r"(r[0]), "=r"(r[1]) : "r"(addr));
+}
+
+template <typename T>
+__device__ __forceinline__ void mma1688(float c[4], const uint32_t a[2], uint32_t b0) {
+    if constexpr (std::is_same<T, __half>::value)
+        asm volatile("mma.sync.aligned.m16n8k8.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5}, {%6}, {%0,%1,%2,%3};\n"
+                     : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+                     : "r"(a[0]), "r"(a[1]), "r"(b0));
+    else
+        asm volatile("mma.sync.aligned.m16n8k8.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5}, {%6}, {%0,%1,%2,%3};\n"
+                     : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+                     : "r"(a[0]), "r"(a[1]), "r"(b0));
+}
+
+// conv3_strip16 on the box-split 24-channel tile: the same sliding-window
+// schedule (each input row's three dx-shifted fragments loaded once), plus
+// the k8 chunk.  Lane addresses carry the box split (x / 22, x % 22).
+template <typename T, int ROWS, class Epi>
+__device__ __forceinline__ void conv3_strip24(uint32_t sbase, int r0, int sx, const uint32_t (&B3)[9][2][2],
+                                              const uint32_t (&B3c)[9][2], const float (&binit)[2][2],
+                                              Epi&& epi) {
+    const int lane = threadIdx.x & 31;
+    const int lm = lane >> 3, li = lane & 7;
+    uint32_t xo[3], xoc[3];
+#pragma unroll
+    for (int dx = 0; dx < 3; ++dx) {
+        const int x = sx + 2 * li + (lm & 1) + dx;           // pair-row pixel order (kPairRows)
+        const int bx = (x * 373) >> 13;                       // x / 22 for x < 66
+        const uint32_t o = bx * S24_BOXB + (x - bx * S24_BOXW) * 16;
+        xo[dx] = o + (lm >> 1) * S24_CSTR;
+        xoc[dx] = o + 2 * S24_CSTR;
+    }
+    float acc[3][2][4];
+    uint32_t Ab[2][3][4], Ac[2][3][2];
+    auto load_row = [&](int ir, uint32_t (&A)[3][4], uint32_t (&C)[3][2]) {
+        const uint32_t ro = sbase + (r0 + ir) * S24_ROWB;
+#pragma unroll
+        for (int dx = 0; dx < 3; ++dx) {
+            ldsm_x4(ro + xo[dx], A[dx]);
+            ldsm_x2(ro + xoc[dx], C[dx]);
+        }
+    };
+    load_row(0, Ab[0], Ac[0]);
+#pragma unroll
+    for (int ir = 0; ir < ROWS + 2; ++ir) {
+        if (ir + 1 < ROWS + 2) load_row(ir + 1, Ab[(ir + 1) & 1], Ac[(ir + 1) & 1]);
+        uint32_t (&A)[3][4] = Ab[ir & 1];
+        uint32_t (&Cc)[3][2] = Ac[ir & 1];
+#pragma unroll
+        for (int dx = 0; dx < 3; ++dx)
+#pragma unroll
+            for (int ky = 0; ky < 3; ++ky) {
+                const int oo = ir - ky;
+                if (oo >= 0 && oo < ROWS) {
+#pragma unroll
+                    for (int n = 0; n < 2; ++n) {
+                        const int tap = ky * 3 + dx;
+                        if (ky == 0 && dx == 0)
+                            mma16816_c<T>(acc[oo % 3][n], A[dx], B3[tap][n][0], B3[tap][n][1], binit[n][0],
+                                          binit[n][1], binit[n][0], binit[n][1]);
+                        else
+                            mma16816<T>(acc[oo % 3][n], A[dx], B3[tap][n][0], B3[tap][n][1]);
+                        mma1688<T>(acc[oo % 3][n], Cc[dx], B3c[tap][n]);
+                    }
+                }
+            }
+        if (ir >= 2) {
+            const int oo = ir - 2;
+            epi(oo, acc[oo % 3]);
+        }
+    }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(kS24Threads, 1) enc0_s2d_kernel(const __grid_constant__ Enc0Args a,
+                                                                  const __grid_constant__ CUtensorMap xm, int total) {
+    extern __shared__ __align__(128) uint8_t smem[];
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + S24_NS * S24_TILE);
+    uint64_t* empty = full + S24_NS;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < S24_NS; ++i) {
+            mbar_init(&full[i], 1);
+            mbar_init(&empty[i], kS24Mma);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) pdl_trigger();
+    pdl_wait();                                 // the s2d tensor is the previous kernel's output
+    if (warp == kS24Mma) {                      // TMA producer
+        if (lane == 0) {
+            const uint64_t pol = l2_evict_first_policy();      // read once
+            for (int k = 0;; ++k) {
+                const int tile = blockIdx.x + k * gridDim.x;
+                if (tile >= total) break;
+                const int s = k % S24_NS;
+                if (k >= S24_NS) mbar_wait(&empty[s], ((k / S24_NS) - 1) & 1);
+                const L0Tile tl = l0_tile(tile, a.td);
+                const uint32_t dst = smem_u32(smem + s * S24_TILE);
+                mbar_expect_tx(&full[s], S24_TILE);
+#pragma unroll
+                for (int b = 0; b < S24_NBOX; ++b)
+                    tma_load_3d_stream(dst + b * S24_BOXB, &xm, (tl.tx0 - 1 + b * S24_BOXW) * 8, tl.ty0 - 1,
+                                       tl.f * 3, &full[s], pol);
+            }
+        }
+        return;
+    }
+    const int H1 = a.H0 / 2, W1 = a.W0 / 2;
+    const int g = lane >> 2, t = lane & 3;
+    const int sx = (warp & 3) * 16, r0 = (warp >> 2) * 8;
+    uint32_t B3[9][2][2], B3c[9][2], B1[2][2];
+    float bias3[2][2], bias1[2][2];
+#pragma unroll
+    for (int tap = 0; tap < 9; ++tap)
+#pragma unroll
+        for (int n = 0; n < 2; ++n) {
+            const uint2 v = __ldg(a.wb3 + ((tap * 2 + 0) * 2 + n) * 32 + lane);   // K-step 0: chunks 0-1
+            B3[tap][n][0] = v.x;
+            B3[tap][n][1] = v.y;
+            B3c[tap][n] = __ldg(a.wb3 + ((tap * 2 + 1) * 2 + n) * 32 + lane).x;  // K-step 1, k 0-7: chunk 2
+        }
+#pragma unroll
+    for (int n = 0; n < 2; ++n) {
+        const uint2 v = __ldg(a.wb1 + n * 32 + lane);
+        B1[n][0] = v.x;
+        B1[n][1] = v.y;
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+            bias3[n][e] = __ldg(a.b3 + n * 8 + 2 * t + e);
+            bias1[n][e] = 0.25f * __ldg(a.b1 + n * 8 + 2 * t + e);   // pool scale folded (pack_f16)
+        }
+    }
+    T* out = reinterpret_cast<T*>(a.out);
+    for (int k = 0;; ++k) {
+        const int tile = blockIdx.x + k * gridDim.x;
+        if (tile >= total) break;
+        const int s = k % S24_NS;
+        mbar_wait(&full[s], (k / S24_NS) & 1);
+        const L0Tile tl = l0_tile(tile, a.td);
+        float pp[2][2];
+        const int px = ((tl.tx0 + sx) >> 1) + g;
+        const bool px_ok = px < W1;
+        T* obase = out + (((int64_t)tl.f * H1 + ((tl.ty0 + r0) >> 1)) * W1 + px) * 16 + 2 * t;
+        conv3_strip24<T, 8>(smem_u32(smem + s * S24_TILE), r0, sx, B3, B3c, bias3, [&](int oo, float (&acc)[2][4]) {
+            uint32_t a1[4];
+            relu_pack_a<T>(acc, a1);
+            float u[2][4];
+#pragma unroll
+            for (int n = 0; n < 2; ++n)
+                mma16816_c<T>(u[n], a1, B1[n][0], B1[n][1], bias1[n][0], bias1[n][1], bias1[n][0], bias1[n][1]);
+#pragma unroll
+            for (int n = 0; n < 2; ++n)
+#pragma unroll
+                for (int e = 0; e < 2; ++e) {
+                    const float v = fmaxf(u[n][e], 0.f) + fmaxf(u[n][e + 2], 0.f);
+                    if (oo & 1) pp[n][e] += v;
+                    else pp[n][e] = v;
+                }
+            if (oo & 1) {
+                if (((tl.ty0 + r0 + oo) >> 1) < H1 && px_ok) {
+                    T* o = obase + (oo >> 1) * W1 * 16;
+#pragma unroll
+                    for (int n = 0; n < 2; ++n)
+                        *reinterpret_cast<uint32_t*>(o + n * 8) = Elem<T>::pack(pp[n][0], pp[n][1]);
+                }
+            }
+        });
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[s]);
+    }
+}
+
+// fp32 planes (N, 5, H, W) -> the chunk-planar s2d tensor enc0_s2d reads
+// (nsm_forward of a 5-plane plan); one thread per level-0 pixel.
+template <typename T>
+__global__ void pack_s2d24_kernel(const float* __restrict__ x, int H, int W, int nf, T* __restrict__ out) {
+    const int H0 = H / 2, W0 = W / 2;
+    const int64_t n0 = (int64_t)H0 * W0;
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= n0 * nf) return;
+    const int f = (int)(i / n0);
+    const int64_t r = i - f * n0;
+    const int Y = (int)(r / W0), X = (int)(r - (int64_t)Y * W0);
+    const int64_t hw = (int64_t)H * W;
+    const float* xf = x + (int64_t)f * 5 * hw;
+    float v[4][5];
+#pragma unroll
+    for (int e = 0; e < 4; ++e)
+#pragma unroll
+        for (int c = 0; c < 5; ++c) v[e][c] = __ldg(xf + c * hw + (int64_t)(2 * Y + (e >> 1)) * W + 2 * X + (e & 1));
+    uint4 c0, c1, c2;
+    c0 = make_uint4(Elem<T>::pack(v[0][0], v[0][1]), Elem<T>::pack(v[0][2], v[0][3]), Elem<T>::pack(v[1][0], v[1][1]),
+                    Elem<T>::pack(v[1][2], v[1][3]));
+    c1 = make_uint4(Elem<T>::pack(v[2][0], v[2][1]), Elem<T>::pack(v[2][2], v[2][3]), Elem<T>::pack(v[3][0], v[3][1]),
+                    Elem<T>::pack(v[3][2], v[3][3]));
+    c2 = make_uint4(Elem<T>::pack(v[0][4], v[1][4]), Elem<T>::pack(v[2][4], v[3][4]), 0u, 0u);
+    const int64_t plane = n0 * 8;
+    T* o = out + ((int64_t)f * 3 * n0 + r) * 8;
+    *reinterpret_cast<uint4*>(o) = c0;
+    *reinterpret_cast<uint4*>(o + plane) = c1;
+    *reinterpret_cast<uint4*>(o + 2 * plane) = c2;
 }
 
 // Bilinear 2x of an NHWC 16-bit tensor at one output pixel, 8 channels
@@ -2207,6 +2438,21 @@ bool encode_nhwc_map4(const void* base, bool bf16, int C, int H, int W, int nf, 
                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+// 3-D view (x * 8 + element, y, frame * 3 + chunk) of the chunk-planar
+// s2d tensor (N, 3, H0, W0, 8); a box is 22 pixels x 18 rows x 3 chunks
+bool encode_s2d24_map(const void* base, bool bf16, int H0, int W0, int nf, CUtensorMap* m) {
+    auto enc = tensor_map_encoder();
+    if (!enc || ((uintptr_t)base % 16)) return false;
+    const cuuint64_t dims[3] = {(cuuint64_t)W0 * 8, (cuuint64_t)H0, (cuuint64_t)nf * 3};
+    const cuuint64_t strides[2] = {(cuuint64_t)W0 * 16, (cuuint64_t)H0 * W0 * 16};
+    const cuuint32_t box[3] = {(cuuint32_t)S24_BOXW * 8, (cuuint32_t)E0_IR, 3};
+    const cuuint32_t es[3] = {1, 1, 1};
+    return enc(m, bf16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 3,
+               const_cast<void*>(base), dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+               CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 template <typename T, int CIN, int C3, int C1, int SRC, int DST, int NB, int NIN, int NMID>
 nsm_status launch_level(const LevelArgs& a, int nf, cudaStream_t st, const char* name) {
     using G = LvGeom<CIN, C3, C1, NB, NIN, NMID, SRC == SRC_UP>;
@@ -2265,10 +2511,11 @@ nsm_status launch_level(const LevelArgs& a, int nf, cudaStream_t st, const char*
 struct Bufs {
     void *p1, *s1, *p2, *s2, *p3, *b3, *d2, *d1;
     __half* y;
+    void* x5;        // 5-plane nets: the chunk-planar s2d input (nf, 3, H0, W0, 8)
     size_t bytes;
 };
 
-Bufs carve(void* ws, int nf, int H0, int W0, int es) {
+Bufs carve(void* ws, int nf, int H0, int W0, int es, bool x5 = false) {
     const int H1 = H0 / 2, W1 = W0 / 2, H2 = H1 / 2, W2 = W1 / 2, H3 = H2 / 2, W3 = W2 / 2;
     Bufs b{};
     char* p = (char*)ws;
@@ -2286,6 +2533,7 @@ Bufs carve(void* ws, int nf, int H0, int W0, int es) {
     b.d2 = take((size_t)nf * H2 * W2 * 32 * es);
     b.d1 = take((size_t)nf * (H1 + 2) * (W1 + 2) * 16 * es);   // replicate-padded, chunk-planar (DST_PADREP)
     b.y = (__half*)take((size_t)nf * H0 * W0 * 8);
+    b.x5 = x5 ? take((size_t)nf * 3 * H0 * W0 * 8 * es) : nullptr;
     b.bytes = (size_t)(p - (char*)ws);
     return b;
 }
@@ -2351,18 +2599,23 @@ bool encode_gbuf_maps(const GBufK& g, int nf, int h, int w, GbufMaps* m) {
 template <typename T>
 nsm_status run_l0(const Plan& p, const Bufs& b, const Enc0Args& e0, const GbufMaps& tm, int nf, int H0,
                   int W0, int h, int w, void* y, int y_f16, cudaStream_t st, int src) {
+    // src: 0 fp32 feature planes, 1 G-buffer (LDG), 2 G-buffer (TMA),
+    // 3 the 5-plane s2d tensor b.x5 (enc0_s2d)
     static PerDevice attr;
     if (attr.first()) {
         cudaFuncSetAttribute(enc0_kernel<T, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * E0_SMEM);
         cudaFuncSetAttribute(enc0_kernel<T, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * E0_SMEM);
         cudaFuncSetAttribute(enc0_kernel<T, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, ENC0_SMEM_TMA);
+        cudaFuncSetAttribute(enc0_kernel<T, 2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, ENC0_SMEM_TMA);
+        cudaFuncSetAttribute(enc0_s2d_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, S24_SMEM);
     }
     // setmaxnreg.inc blocks until .dec released enough of the CTA's launch
     // allocation: refuse to launch a budget that could hang
     static const int launch_regs = [] {
-        cudaFuncAttributes fa{};
+        cudaFuncAttributes fa{}, fb{};
         cudaFuncGetAttributes(&fa, enc0_kernel<T, 2>);
-        return fa.numRegs;
+        cudaFuncGetAttributes(&fb, enc0_kernel<T, 2, true>);
+        return std::min(fa.numRegs, fb.numRegs);
     }();
     if (kE0Prod * kE0ProdRegs + (kE0Threads - kE0Prod) * kE0MmaRegs > launch_regs * kE0Threads)
         return fail(NSM_ERR_CUDA, "enc0: register budget %d x %d + %d x %d exceeds launch allocation %d x %d",
@@ -2370,8 +2623,16 @@ nsm_status run_l0(const Plan& p, const Bufs& b, const Enc0Args& e0, const GbufMa
     const int total = ((W0 + E0_TW - 1) / E0_TW) * ((H0 + E0_TH - 1) / E0_TH) * nf;
     const int pgrid = std::min(total, num_sms());
     {
-        NSM_PROF("enc0_fused", st);
-        if (src == 2) launch_pdl(enc0_kernel<T, 2>, dim3(pgrid), dim3(kE0Threads), ENC0_SMEM_TMA, st, e0, tm, total);
+        NSM_PROF(src == 3 ? "enc0_s2d" : "enc0_fused", st);
+        if (src == 3) {
+            CUtensorMap xm;
+            memset(&xm, 0, sizeof xm);
+            if (!encode_s2d24_map(b.x5, std::is_same<T, __nv_bfloat16>::value, H0, W0, nf, &xm))
+                return fail(NSM_ERR_CUDA, "enc0_s2d: TMA tensor map encoding failed");
+            launch_pdl(enc0_s2d_kernel<T>, dim3(pgrid), dim3(kS24Threads), S24_SMEM, st, e0, xm, total);
+        } else if (src == 2 && e0.tidx)
+            launch_pdl(enc0_kernel<T, 2, true>, dim3(pgrid), dim3(kE0Threads), ENC0_SMEM_TMA, st, e0, tm, total);
+        else if (src == 2) launch_pdl(enc0_kernel<T, 2>, dim3(pgrid), dim3(kE0Threads), ENC0_SMEM_TMA, st, e0, tm, total);
         else if (src == 1) launch_pdl(enc0_kernel<T, 1>, dim3(pgrid), dim3(kL0Threads), 2 * E0_SMEM, st, e0, tm, total);
         else launch_pdl(enc0_kernel<T, 0>, dim3(pgrid), dim3(kL0Threads), 2 * E0_SMEM, st, e0, tm, total);
     }
@@ -2418,14 +2679,14 @@ int round16(int v) { return (v + 15) / 16 * 16; }
 
 bool f16_supported(const Plan& p) {
     const nsm_net_config& c = p.cfg;
-    return c.layers == 5 && c.base_channels == 16 && c.in_channels == 4 && c.use_space_to_depth &&
-           c.channel_cap >= 128;
+    return c.layers == 5 && c.base_channels == 16 && (c.in_channels == 4 || c.in_channels == 5) &&
+           c.use_space_to_depth && c.channel_cap >= 128;
 }
 
 size_t infer_f16_workspace(const Plan& p, int n, int h, int w) {
     const int Hp = round16(h), Wp = round16(w);
     const int nf = std::min(n, chunk_frames());
-    return carve(nullptr, nf, Hp / 2, Wp / 2, 2).bytes + 1024;
+    return carve(nullptr, nf, Hp / 2, Wp / 2, 2, p.cfg.in_channels == 5).bytes + 1024;
 }
 
 nsm_status pack_f16(Plan& p, std::vector<char>& blob, size_t& offset_out) {
@@ -2552,7 +2813,8 @@ nsm_status infer_f16(const Plan& p, const nsm_gbuffer* g, const float* sm, int64
     if (sm_stride * nfmax > INT32_MAX)   // the fused feature pass indexes a chunk's maps in 32 bits
         return fail(NSM_ERR_UNSUPPORTED, "shadow maps of %lld texels x %d frames per pass exceed 2^31",
                     (long long)sm_stride, nfmax);
-    Bufs b = carve(ws, nfmax, H0, W0, 2);
+    const bool five = p.cfg.in_channels == 5;
+    Bufs b = carve(ws, nfmax, H0, W0, 2, five);
     if (ws_bytes < b.bytes) return fail(NSM_ERR_ARG, "workspace too small (%zu < %zu)", ws_bytes, b.bytes);
     {
         NSM_PROF("fill_i64", st);
@@ -2584,7 +2846,20 @@ nsm_status infer_f16(const Plan& p, const nsm_gbuffer* g, const float* sm, int64
         void* yo = (char*)y + (size_t)f0 * h * w * (y_dtype == NSM_F16 ? 2 : 4);
         GbufMaps tm;
         memset(&tm, 0, sizeof tm);
-        const int src = encode_gbuf_maps(e.g, nf, h, w, &tm) ? 2 : 1;
+        int src;
+        if (five) {
+            // 5-plane net: features + blocker search -> b.x5, then enc0_s2d
+            nsm_gbuffer gc = *g;
+            gc.d = e.g.d;
+            gc.normal = e.g.normal;
+            gc.position = e.g.position;
+            nsm_status s5 = launch_feat5(&gc, e.sm, sm_stride, frames + f0, nf, h, w, H0, W0, b.x5,
+                                         p.act == NSM_BF16 ? 1 : 0, first_bad + f0, e.tidx, st);
+            if (s5 != NSM_OK) return s5;
+            src = 3;
+        } else {
+            src = encode_gbuf_maps(e.g, nf, h, w, &tm) ? 2 : 1;
+        }
         nsm_status s = p.act == NSM_BF16
                            ? run_l0<__nv_bfloat16>(p, b, e, tm, nf, H0, W0, h, w, yo, y_dtype == NSM_F16, st, src)
                            : run_l0<__half>(p, b, e, tm, nf, H0, W0, h, w, yo, y_dtype == NSM_F16, st, src);
@@ -2599,12 +2874,13 @@ nsm_status forward_f16(const Plan& p, const float* x, int n, int h, int w, float
     if (!f16_supported(p)) return fail(NSM_ERR_UNSUPPORTED, "no 16-bit kernels for this NetworkConfig");
     const int H0 = h / 2, W0 = w / 2;
     const int nfmax = std::min(n, chunk_frames());
-    Bufs b = carve(ws, nfmax, H0, W0, 2);
+    const bool five = p.cfg.in_channels == 5;
+    Bufs b = carve(ws, nfmax, H0, W0, 2, five);
     if (ws_bytes < b.bytes) return fail(NSM_ERR_ARG, "workspace too small");
     for (int f0 = 0; f0 < n; f0 += chunk_frames()) {
         const int nf = std::min(chunk_frames(), n - f0);
         Enc0Args e{};
-        e.x = x + (int64_t)f0 * 4 * h * w;
+        e.x = x + (int64_t)f0 * p.cfg.in_channels * h * w;
         e.h = h;
         e.w = w;
         e.H0 = H0;
@@ -2619,9 +2895,19 @@ nsm_status forward_f16(const Plan& p, const float* x, int n, int h, int w, float
         float* yo = out + (size_t)f0 * h * w;
         GbufMaps tm;
         memset(&tm, 0, sizeof tm);
+        if (five) {
+            const int64_t items = (int64_t)nf * H0 * W0;
+            const int grid = (int)((items + 255) / 256);
+            NSM_PROF("pack_s2d24", st);
+            if (p.act == NSM_BF16)
+                pack_s2d24_kernel<__nv_bfloat16><<<grid, 256, 0, st>>>(e.x, h, w, nf, (__nv_bfloat16*)b.x5);
+            else
+                pack_s2d24_kernel<__half><<<grid, 256, 0, st>>>(e.x, h, w, nf, (__half*)b.x5);
+        }
+        const int src = five ? 3 : 0;
         nsm_status s = p.act == NSM_BF16
-                           ? run_l0<__nv_bfloat16>(p, b, e, tm, nf, H0, W0, h, w, yo, 0, st, 0)
-                           : run_l0<__half>(p, b, e, tm, nf, H0, W0, h, w, yo, 0, st, 0);
+                           ? run_l0<__nv_bfloat16>(p, b, e, tm, nf, H0, W0, h, w, yo, 0, st, src)
+                           : run_l0<__half>(p, b, e, tm, nf, H0, W0, h, w, yo, 0, st, src);
         if (s != NSM_OK) return s;
     }
     NSM_CUDA_TRY(cudaGetLastError());

@@ -192,6 +192,33 @@ def blocker_penumbra_batch(inputs, frames, radius: int = 8, check=True):
     return out
 
 
+def assemble_features5_batch(inputs, frames, want_idx=False, check=True):
+    """The 5-plane feature pass of NetworkConfig(in_channels=5) nets (BASELINE
+    configs 3/4): the 4 planes of :func:`assemble_features_batch` (fp32
+    arithmetic of the fused hot path) and the 16x16 blocker-search penumbra
+    plane, computed with the map windows staged in shared memory
+    (nsm_features5).  Returns (features (N,5,H,W), texel indices or None,
+    first_bad)."""
+    import torch
+    d = inputs["d"]
+    n, h, w = d.shape
+    hs, ws = inputs["sm"].shape[1:]
+    gb = _lib.GBufferC(_lib.NSM_F32, d.data_ptr(), inputs["normal"].data_ptr(),
+                       inputs["position"].data_ptr(), None, None, None, None, h * w)
+    out = torch.empty((n, 5, h, w), dtype=torch.float32, device=d.device)
+    idx = torch.full((n, 2, h, w), -1, dtype=torch.int32, device=d.device) if want_idx else None
+    bad = torch.empty(n, dtype=torch.int64, device=d.device)
+    _lib.check(_lib.lib.nsm_features5(C.byref(gb), inputs["sm"].data_ptr(), hs * ws, _lib.frames_c(frames),
+                                      n, h, w, out.data_ptr(), idx.data_ptr() if want_idx else None,
+                                      bad.data_ptr(), _lib.stream_ptr()))
+    if check:
+        for v in bad.cpu().tolist():
+            if v != _lib.INT64_MAX:
+                y, x = divmod(int(v), w)
+                raise FrustumError(f"covered pixel ({y}, {x}) projects outside the emitter frustum")
+    return out, idx, bad
+
+
 def hard_shadow_mask(stack: FeatureStack) -> np.ndarray:
     """Point-light shadow test (raster.py:281-283)."""
     return (stack.data[0] < 0.0) & stack.coverage
