@@ -44,7 +44,8 @@ def _check_planes(got, ref, cov, what):
     d = np.abs(got[:4] - ref[:4])
     assert d.max() <= 1e-4 * max(1.0, float(np.abs(ref[:4]).max())), f"{what}: planes 0-3 off by {d.max()}"
     g4, r4 = got[4], ref[4]
-    assert np.array_equal(g4 > 0, r4 > 0), f"{what}: blocker classification differs at {(g4 > 0) != (r4 > 0)).sum()} px"
+    ndiff = int(((g4 > 0) != (r4 > 0)).sum())
+    assert ndiff == 0, f"{what}: blocker classification differs at {ndiff} px"
     rel = np.abs(g4 - r4) / np.maximum(1.0, np.abs(r4))
     assert rel.max() <= 2e-3, f"{what}: penumbra plane rel err {rel.max()}"
     print(f"{what}: planes 0-3 max {d.max():.3g}, plane 4 rel {rel.max():.3g}, "
