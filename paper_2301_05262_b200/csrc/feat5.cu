@@ -27,6 +27,7 @@
 // the 4 blocker values of the pixel's 2 x 2 (s2d channels 16-19) and zeros;
 // or (parity / drop-in mode) fp32 planes (N, 5, h, w).
 #include <algorithm>
+#include <atomic>
 #include <cfloat>
 
 #include "common.cuh"
@@ -40,7 +41,7 @@ namespace {
 
 constexpr int F5_TY = 8, F5_TX = 32, F5_THREADS = F5_TY * F5_TX;
 constexpr int F5_R = 8;                      // window rows ri-8 .. ri+7 (16 x 16)
-constexpr int F5_MAX_TEX = 3072;             // staged texels per CTA (region + 2 block maps: 36 KB)
+constexpr int F5_MAX_TEX = 6144;             // staged texels per CTA (regions + block maps: 72 KB)
 constexpr int F5_SMEM = F5_MAX_TEX * 4 + F5_MAX_TEX * 8;
 constexpr int kInfBits = 0x7f800000;
 
@@ -72,20 +73,89 @@ __device__ __forceinline__ float penumbra_width_f(float zmin, float zmax, float 
     return (xa + xb) * focal / d;
 }
 
+// A staged map region: rows R0 .. R0+RH-1, cols C0 .. C0+RW-1 as depth
+// bits (+inf off the map) and its sliding 4 x 4 (min, max) map.
+struct Region {
+    int R0, C0, RH, RW;
+    bool on;
+    int* tex;
+    int2* blk;
+};
+
+__device__ __forceinline__ void stage_region(const Region& g, const float* smf, const FrameK& F, int tid) {
+    if (!g.on) return;
+    for (int i = tid; i < g.RH * g.RW; i += F5_THREADS) {
+        const int r = g.R0 + i / g.RW, c = g.C0 + i % g.RW;
+        const bool in = r >= 0 && r < F.hs && c >= 0 && c < F.ws;
+        g.tex[i] = in ? __float_as_int(__ldg(smf + (int64_t)r * F.ws + c)) : kInfBits;
+    }
+}
+
+__device__ __forceinline__ void build_blocks(const Region& g, int tid) {
+    if (!g.on) return;
+    const int BW = g.RW - 3, BH = g.RH - 3;
+    for (int i = tid; i < BH * BW; i += F5_THREADS) {
+        const int r = i / BW, c = i % BW;
+        int mn = kInfBits, mx = 0;
+#pragma unroll
+        for (int dy = 0; dy < 4; ++dy) {
+            const int* row = g.tex + (r + dy) * g.RW + c;
+            mn = __vimin3_s32(row[0], row[1], mn);
+            mn = __vimin3_s32(row[2], row[3], mn);
+            mx = __vimax3_s32(row[0], row[1], mx);
+            mx = __vimax3_s32(row[2], row[3], mx);
+        }
+        g.blk[i] = make_int2(mn, mx);
+    }
+}
+
+__device__ __forceinline__ int region_texels(const int (&b)[4]) {
+    return (b[1] - b[0] + 2 * F5_R) * (b[3] - b[2] + 2 * F5_R);
+}
+
+// Texel bounding box (row lo, hi, col lo, hi) of the CTA's covered pixels
+// of cluster k into bb[k] (warp reduction, then shared atomics).  Ends with
+// a barrier; bb[k] must not be read by anyone before the call.
+__device__ __forceinline__ void block_bbox(const int (&ri)[4], const int (&ci)[4], const bool (&cov)[4],
+                                           const int (&cl)[4], int k, int (*bb)[4], int tid) {
+    if (tid == 0) {
+        bb[k][0] = INT32_MAX;
+        bb[k][1] = INT32_MIN;
+        bb[k][2] = INT32_MAX;
+        bb[k][3] = INT32_MIN;
+    }
+    int rlo = INT32_MAX, rhi = INT32_MIN, clo = INT32_MAX, chi = INT32_MIN;
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+        if (!cov[e] || cl[e] != k) continue;
+        rlo = min(rlo, ri[e]);
+        rhi = max(rhi, ri[e]);
+        clo = min(clo, ci[e]);
+        chi = max(chi, ci[e]);
+    }
+    rlo = __reduce_min_sync(0xffffffffu, rlo);
+    rhi = __reduce_max_sync(0xffffffffu, rhi);
+    clo = __reduce_min_sync(0xffffffffu, clo);
+    chi = __reduce_max_sync(0xffffffffu, chi);
+    __syncthreads();
+    if ((tid & 31) == 0 && rlo <= rhi) {
+        atomicMin(&bb[k][0], rlo);
+        atomicMax(&bb[k][1], rhi);
+        atomicMin(&bb[k][2], clo);
+        atomicMax(&bb[k][3], chi);
+    }
+    __syncthreads();
+}
+
 template <typename T, bool kF32>
 __global__ void __launch_bounds__(F5_THREADS) feat5_kernel(const __grid_constant__ Feat5Args a) {
     extern __shared__ __align__(16) int smem5[];
-    __shared__ int bb[4];
+    __shared__ int bb[2][4];
     const int f = blockIdx.z;
     const int tid = threadIdx.x;
     const int X = blockIdx.x * F5_TX + (tid & 31), Y = blockIdx.y * F5_TY + (tid >> 5);
     const FrameK& F = a.tab.f[f];
-    if (tid == 0) {
-        bb[0] = INT32_MAX;
-        bb[1] = INT32_MIN;
-        bb[2] = INT32_MAX;
-        bb[3] = INT32_MIN;
-    }
+    if (tid == 0) bb[1][0] = INT32_MAX, bb[1][1] = INT32_MIN;   // cluster 1 empty unless split
     const int64_t hw = (int64_t)a.h * a.w;
     const int64_t base = (int64_t)f * a.g.frame_stride;
     const float* gd = reinterpret_cast<const float*>(a.g.d) + base;
@@ -113,7 +183,6 @@ __global__ void __launch_bounds__(F5_THREADS) feat5_kernel(const __grid_constant
             nzv[e] = __ldg(gn + 2 * hw + p);
         }
     }
-    int rlo = INT32_MAX, rhi = INT32_MIN, clo = INT32_MAX, chi = INT32_MIN;
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
         if (!cov[e]) continue;
@@ -125,54 +194,53 @@ __global__ void __launch_bounds__(F5_THREADS) feat5_kernel(const __grid_constant
             ti[0] = ri[e];
             ti[hw] = ci[e];
         }
-        rlo = min(rlo, ri[e]);
-        rhi = max(rhi, ri[e]);
-        clo = min(clo, ci[e]);
-        chi = max(chi, ci[e]);
     }
-    rlo = __reduce_min_sync(0xffffffffu, rlo);
-    rhi = __reduce_max_sync(0xffffffffu, rhi);
-    clo = __reduce_min_sync(0xffffffffu, clo);
-    chi = __reduce_max_sync(0xffffffffu, chi);
-    __syncthreads();   // bb initialised
-    if ((tid & 31) == 0 && rlo <= rhi) {
-        atomicMin(&bb[0], rlo);
-        atomicMax(&bb[1], rhi);
-        atomicMin(&bb[2], clo);
-        atomicMax(&bb[3], chi);
-    }
-    __syncthreads();
-    const bool any = bb[0] <= bb[1];
-    // region: window rows rlo-8 .. rhi+7, cols clo-8 .. chi+7 (+inf off the map)
-    const int R0 = bb[0] - F5_R, C0 = bb[2] - F5_R;
-    const int RH = bb[1] - bb[0] + 2 * F5_R, RW = bb[3] - bb[2] + 2 * F5_R;
-    const bool staged = any && RH * RW <= F5_MAX_TEX;
-    const float* smf = a.sm + (int64_t)f * a.sm_stride;
-    int* reg = smem5;                                   // [RH][RW] depth bits
-    int2* blk = reinterpret_cast<int2*>(smem5 + F5_MAX_TEX);   // [RH-3][RW-3] sliding 4x4 (min, max)
-    if (staged) {
-        for (int i = tid; i < RH * RW; i += F5_THREADS) {
-            const int r = R0 + i / RW, c = C0 + i % RW;
-            const bool in = r >= 0 && r < F.hs && c >= 0 && c < F.ws;
-            reg[i] = in ? __float_as_int(__ldg(smf + (int64_t)r * F.ws + c)) : kInfBits;
-        }
-        __syncthreads();
-        const int BW = RW - 3, BH = RH - 3;
-        for (int i = tid; i < BH * BW; i += F5_THREADS) {
-            const int r = i / BW, c = i % BW;
-            int mn = kInfBits, mx = 0;
+    // Texel bounding box of the tile; when its window region does not fit
+    // the shared-memory budget (a tile across an occluder edge maps to two
+    // separate map areas), the covered pixels are split in two clusters at
+    // the middle of the longer bbox side, each with its own region.
+    int cl[4] = {0, 0, 0, 0};
+    block_bbox(ri, ci, cov, cl, 0, bb, tid);
+    const bool any = bb[0][0] <= bb[0][1];
+    int nreg = 0;
+    if (any && region_texels(bb[0]) > F5_MAX_TEX) {
+        const bool by_rows = bb[0][1] - bb[0][0] >= bb[0][3] - bb[0][2];
+        const int sv = by_rows ? (bb[0][0] + bb[0][1]) >> 1 : (bb[0][2] + bb[0][3]) >> 1;
 #pragma unroll
-            for (int dy = 0; dy < 4; ++dy) {
-                const int* row = reg + (r + dy) * RW + c;
-                mn = __vimin3_s32(row[0], row[1], mn);
-                mn = __vimin3_s32(row[2], row[3], mn);
-                mx = __vimax3_s32(row[0], row[1], mx);
-                mx = __vimax3_s32(row[2], row[3], mx);
-            }
-            blk[i] = make_int2(mn, mx);
-        }
-        __syncthreads();
+        for (int e = 0; e < 4; ++e) cl[e] = ((by_rows ? ri[e] : ci[e]) > sv) ? 1 : 0;
+        __syncthreads();            // every thread has read bb[0]
+        block_bbox(ri, ci, cov, cl, 0, bb, tid);
+        block_bbox(ri, ci, cov, cl, 1, bb, tid);
+        nreg = 2;
+    } else if (any) {
+        nreg = 1;
     }
+    // regions: A = cluster 0 (or all), B = cluster 1; staged if they fit
+    const float* smf = a.sm + (int64_t)f * a.sm_stride;
+    int* regs = smem5;                                        // depth bits
+    int2* blks = reinterpret_cast<int2*>(smem5 + F5_MAX_TEX);  // sliding 4x4 (min, max)
+    Region RA, RB;
+    RA.R0 = bb[0][0] - F5_R;
+    RA.C0 = bb[0][2] - F5_R;
+    RA.RH = bb[0][1] - bb[0][0] + 2 * F5_R;
+    RA.RW = bb[0][3] - bb[0][2] + 2 * F5_R;
+    RA.on = nreg >= 1 && bb[0][0] <= bb[0][1] && RA.RH * RA.RW <= F5_MAX_TEX;
+    RA.tex = regs;
+    RA.blk = blks;
+    const int usedA = RA.on ? RA.RH * RA.RW : 0, busedA = RA.on ? (RA.RH - 3) * (RA.RW - 3) : 0;
+    RB.R0 = bb[1][0] - F5_R;
+    RB.C0 = bb[1][2] - F5_R;
+    RB.RH = bb[1][1] - bb[1][0] + 2 * F5_R;
+    RB.RW = bb[1][3] - bb[1][2] + 2 * F5_R;
+    RB.on = nreg == 2 && bb[1][0] <= bb[1][1] && usedA + RB.RH * RB.RW <= F5_MAX_TEX;
+    RB.tex = regs + usedA;
+    RB.blk = blks + busedA;
+    stage_region(RA, smf, F, tid);
+    stage_region(RB, smf, F, tid);
+    __syncthreads();
+    build_blocks(RA, tid);
+    build_blocks(RB, tid);
+    __syncthreads();
 
     // per pixel: the 4 reference planes (fp32 math as the fused 4-plane
     // producer) and the blocker plane
@@ -196,8 +264,14 @@ __global__ void __launch_bounds__(F5_THREADS) feat5_kernel(const __grid_constant
         const float dx = F.fcp[0] - pxv[e], dy = F.fcp[1] - pyv[e], dz = F.fcp[2] - pzv[e];
         const float cc = __saturatef((nxv[e] * dx + nyv[e] * dy + nzv[e] * dz) * rsqrtf(dx * dx + dy * dy + dz * dz));
         const int tr = ri[e], tc = ci[e];
-        const float look = staged ? __int_as_float(reg[(tr - R0) * RW + (tc - C0)])
-                                  : __ldg(smf + (int64_t)tr * F.ws + tc);
+        // this pixel's region
+        const bool k1 = cl[e] != 0;
+        const bool st = k1 ? RB.on : RA.on;
+        const int* reg = k1 ? RB.tex : RA.tex;
+        const int W_ = k1 ? RB.RW : RA.RW;
+        const int Rk = k1 ? RB.R0 : RA.R0, Ck = k1 ? RB.C0 : RA.C0;
+        const float look = st ? __int_as_float(reg[(tr - Rk) * W_ + (tc - Ck)])
+                              : __ldg(smf + (int64_t)tr * F.ws + tc);
         float ch0 = 0.f, ch1 = 1.f;
         if (look < INFINITY) {                                       // raster.py:262
             const float m = fminf(look, zf);
@@ -213,8 +287,9 @@ __global__ void __launch_bounds__(F5_THREADS) feat5_kernel(const __grid_constant
         const unsigned thr1 = (unsigned)thr - 1u;
         int zmin = kInfBits;
         unsigned um = 0xffffffffu;
-        if (staged) {
-            const int r0 = tr - F5_R - R0, c0 = tc - F5_R - C0, BW = RW - 3;
+        if (st) {
+            const int r0 = tr - F5_R - Rk, c0 = tc - F5_R - Ck, BW = W_ - 3;
+            const int2* blk = k1 ? RB.blk : RA.blk;
             unsigned strad = 0;
 #pragma unroll
             for (int b = 0; b < 16; ++b) {
@@ -226,16 +301,30 @@ __global__ void __launch_bounds__(F5_THREADS) feat5_kernel(const __grid_constant
             while (strad) {
                 const int b = __ffs(strad) - 1;
                 strad &= strad - 1;
-                const int* p = reg + (r0 + 4 * (b >> 2)) * RW + c0 + 4 * (b & 3);
+                const int* p = reg + (r0 + 4 * (b >> 2)) * W_ + c0 + 4 * (b & 3);
 #pragma unroll
                 for (int dy = 0; dy < 4; ++dy)
 #pragma unroll
                     for (int dxx = 0; dxx < 4; ++dxx)
-                        um = __viaddmin_u32(thr1, (unsigned)(-p[dy * RW + dxx]), um);
+                        um = __viaddmin_u32(thr1, (unsigned)(-p[dy * W_ + dxx]), um);
+            }
+        } else if (tr >= F5_R && tr + F5_R <= F.hs && tc >= F5_R && tc + F5_R <= F.ws) {
+            // window outside the staged regions, inside the map: 16 texel
+            // rows straight from global memory (L1), 16 loads in flight
+            const float* rowp = smf + (int64_t)(tr - F5_R) * F.ws + (tc - F5_R);
+            for (int r = 0; r < 2 * F5_R; ++r, rowp += F.ws) {
+                int t[16];
+#pragma unroll
+                for (int c = 0; c < 16; ++c) t[c] = __float_as_int(__ldg(rowp + c));
+#pragma unroll
+                for (int c = 0; c < 16; c += 2) {
+                    zmin = __vimin3_s32(t[c], t[c + 1], zmin);
+                    um = __viaddmin_u32(thr1, (unsigned)(-t[c]), um);
+                    um = __viaddmin_u32(thr1, (unsigned)(-t[c + 1]), um);
+                }
             }
         } else {
-            // region too large for shared memory (grazing views): the same
-            // scan straight from global memory
+            // window clipped by the map border (rare): bounds-checked scan
             for (int r = tr - F5_R; r < tr + F5_R; ++r) {
                 if (r < 0 || r >= F.hs) continue;
                 for (int c = tc - F5_R; c < tc + F5_R; ++c) {
@@ -313,7 +402,15 @@ nsm_status launch_feat5(const nsm_gbuffer* g, const float* sm, int64_t sm_stride
     // 16-bit: every level-0 pixel of the padded grid; fp32: the frame's pixels
     const int LX = out_kind == 2 ? (w + 1) / 2 : W0, LY = out_kind == 2 ? (h + 1) / 2 : H0;
     dim3 grid((LX + F5_TX - 1) / F5_TX, (LY + F5_TY - 1) / F5_TY, nf);
-    static_assert(F5_SMEM <= 48 * 1024, "feat5 fits the default dynamic shared-memory limit");
+    static std::atomic<uint64_t> attr[3];           // per device: the attribute is per-device state
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (!(attr[out_kind].fetch_or(1ull << (dev & 63)) & (1ull << (dev & 63)))) {
+        cudaFuncSetAttribute(out_kind == 0 ? (const void*)feat5_kernel<__half, false>
+                             : out_kind == 1 ? (const void*)feat5_kernel<__nv_bfloat16, false>
+                                             : (const void*)feat5_kernel<float, true>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, F5_SMEM);
+    }
     NSM_PROF("feat5_blocker", st);
     switch (out_kind) {
         case 0:

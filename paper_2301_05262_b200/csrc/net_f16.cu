@@ -868,8 +868,8 @@ constexpr int S24_BOXW = 22, S24_NBOX = 3;
 static_assert(S24_BOXW * S24_NBOX == E0_IC, "boxes tile the halo'd row");
 constexpr int S24_ROWB = S24_BOXW * 16;               // one box row of one chunk
 constexpr int S24_CSTR = E0_IR * S24_ROWB;             // one chunk of one box
-constexpr int S24_BOXB = 3 * S24_CSTR;                 // one box, 3 chunks
-constexpr int S24_TILE = S24_NBOX * S24_BOXB;          // 57,024 B per tile
+constexpr int S24_BOXB = round128(3 * S24_CSTR);       // one box, 3 chunks (TMA destinations 128-B aligned)
+constexpr int S24_TILE = S24_NBOX * S24_BOXB;          // 57,216 B per tile
 constexpr int S24_NS = 3;                              // ring stages
 constexpr int kS24Mma = 8, kS24Threads = 32 * (kS24Mma + 1);
 constexpr int S24_SMEM = S24_NS * S24_TILE + 64;
@@ -976,7 +976,7 @@ __global__ void __launch_bounds__(kS24Threads, 1) enc0_s2d_kernel(const __grid_c
                 if (k >= S24_NS) mbar_wait(&empty[s], ((k / S24_NS) - 1) & 1);
                 const L0Tile tl = l0_tile(tile, a.td);
                 const uint32_t dst = smem_u32(smem + s * S24_TILE);
-                mbar_expect_tx(&full[s], S24_TILE);
+                mbar_expect_tx(&full[s], S24_NBOX * 3 * S24_CSTR);   // bytes the three boxes deliver
 #pragma unroll
                 for (int b = 0; b < S24_NBOX; ++b)
                     tma_load_3d_stream(dst + b * S24_BOXB, &xm, (tl.tx0 - 1 + b * S24_BOXW) * 8, tl.ty0 - 1,
