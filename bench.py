@@ -9,9 +9,13 @@ Workload (default ``--config 4``, BASELINE.json configs[3]): a temporal
 window of 8 consecutive 1920x1080 soft-shadow frames (spherical light of
 radius U[0.05, 0.5], 32 objects, 2048^2 shadow map, light / one object /
 camera moving 0.02 units per frame), fp16 activations with fp32
-accumulation, seeded random-init weights of the reference architecture.
-A step = the full hot path (feature pass + U-Net -> visibility) over the
-job's frames.
+accumulation, seeded random-init weights of the reference architecture,
+with the reference's own 4-plane feature layout (soft shadows enter through
+the size-index plane).  A step = the full hot path (feature pass + U-Net ->
+visibility) over the job's frames.  The same run also times, as
+``variants``, the window with the 5-plane net (BASELINE's 16x16
+blocker-search penumbra plane; ``--config 3`` makes that the main line) and
+a fully covered camera.
 
 Multi-GPU (north_star: "shards the frame batch and temporal window across
 the GPUs"): one process per GPU.  ``--gpus N`` re-executes itself under
@@ -70,8 +74,9 @@ def parse(argv=None):
     ap.add_argument("--dtype", choices=["fp16", "bf16", "fp32"], default=None,
                     help="default: fp16 (configs 2-4), bf16 (config 5)")
     ap.add_argument("--features", type=int, choices=[4, 5], default=None,
-                    help="input planes: 4 (reference layout) or 5 (+ blocker-search penumbra); "
-                         "default: 5 for the soft configs 3/4, 4 otherwise")
+                    help="input planes: 4 (the reference's layout: soft shadows through the size "
+                         "index plane) or 5 (+ the 16x16 blocker-search penumbra plane); default: "
+                         "5 for config 3 (whose text names the search), 4 otherwise")
     ap.add_argument("--frames", type=int, default=None, help="frames of the job (default: config)")
     ap.add_argument("--scaling", choices=["strong", "weak"], default="strong",
                     help="strong: shard the job's frames over the ranks; weak: one job per rank")
@@ -87,7 +92,7 @@ def parse(argv=None):
     if a.dtype is None:
         a.dtype = "bf16" if a.config == 5 else "fp16"
     if a.features is None:
-        a.features = 5 if a.config in (3, 4) else 4
+        a.features = 5 if a.config == 3 else 4
     return a
 
 
@@ -425,22 +430,44 @@ def run_ours(args):
     if not args.no_e2e:
         e2e = run_e2e(args, run, inputs, frames, job_n, world)
 
-    # ---- the fully covered variant (a typical game G-buffer) ----
+    # ---- variants measured in the same run: the fully covered camera (a
+    # typical game G-buffer) and the same frames with the 5-plane net
+    # (16x16 blocker search, BASELINE configs 3/4) or the 4-plane one ----
     variants = None
     if not args.no_variants and args.cover == "scene" and args.config in (2, 3, 4):
-        fc = [full_cover_frame(f) for f in frames]
-        fin = producer.render_inputs(fc)
-        frun = ShadowInference(plan, fc, out_dtype=out_dtype)
-        frun(fin)
-        frun.capture(fin)
-        for _ in range(3):
-            frun.replay()
-        fms, _ = time_steps(frun.replay, args.steps, world, soak=False, local=local)
-        fms_max = float(gather_floats([fms], world, dev)[:, 0].max())
-        variants = {"full_coverage": {"value": round(job_n / (fms_max / 1e3), 3), "unit": UNIT,
-                                      "ms_per_step": round(fms_max, 5),
-                                      "coverage": round(covered_pixels(fin) / (len(fc) * h * wd), 4)}}
-        del frun, fin
+        variants = {}
+
+        def timed(vframes, vplan, label, extra):
+            vin = producer.render_inputs(vframes)
+            vrun = ShadowInference(vplan, vframes, out_dtype=out_dtype)
+            vrun(vin)
+            vrun.capture(vin)
+            for _ in range(3):
+                vrun.replay()
+            vms, _ = time_steps(vrun.replay, args.steps, world, soak=False, local=local)
+            vms_max = float(gather_floats([vms], world, dev)[:, 0].max())
+            _lib.lib.nsm_profile_enable(1)
+            _lib.profile_report()
+            for _ in range(3):
+                vrun.launch(vin, check=False)
+            torch.cuda.synchronize()
+            vprof = _lib.profile_report()
+            _lib.lib.nsm_profile_enable(0)
+            variants[label] = {"value": round(job_n / (vms_max / 1e3), 3), "unit": UNIT,
+                               "ms_per_step": round(vms_max, 5),
+                               "coverage": round(covered_pixels(vin) / (len(vframes) * h * wd), 4),
+                               "kernel_profile_ms_per_step": {k: round(v[1] / 3, 5) for k, v in
+                                                              sorted(vprof.items(), key=lambda kv: -kv[1][1])},
+                               **extra}
+
+        timed([full_cover_frame(f) for f in frames], plan, "full_coverage",
+              {"features": args.features})
+        other = 5 if args.features == 4 else 4
+        oargs = argparse.Namespace(**{**vars(args), "features": other})
+        _, _, oplan = make_plan(oargs)
+        timed(frames, oplan, "blocker_search_5plane" if other == 5 else "reference_4plane",
+              {"features": other, "network": f"NetworkConfig(in_channels={other})"})
+        torch.cuda.synchronize()
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

@@ -16,6 +16,7 @@ namespace nsm {
 
 namespace {
 thread_local std::string g_err;
+int32_t* g_feat5_dbg = nullptr;   // nsm_debug_feat5: per-pixel search record of nsm_features5
 }
 
 nsm_status fail(nsm_status code, const char* fmt, ...) {
@@ -216,6 +217,10 @@ extern "C" {
 
 int32_t nsm_abi_version(void) { return NSM_ABI_VERSION; }
 
+// Debug hook (not in nsm.h): the next nsm_features5 calls also write
+// (zmin, zmax, thr, path) per pixel into buf ((n, h, w, 4) int32, device).
+void nsm_debug_feat5(int32_t* buf) { g_feat5_dbg = buf; }
+
 int32_t nsm_build_flags(void) {
 #ifdef NSM_EXPERIMENTS
     return NSM_BUILD_EXPERIMENTS;
@@ -407,7 +412,8 @@ nsm_status nsm_features5(const nsm_gbuffer* g, const float* sm, int64_t sm_strid
         gc.position = (const float*)g->position + (int64_t)f0 * 3 * g->frame_stride;
         nsm_status s = launch_feat5(&gc, sm + f0 * sm_stride, sm_stride, frames + f0, nf, h, w, 0, 0,
                                     out_planes + (int64_t)f0 * 5 * h * w, 2, first_bad + f0,
-                                    texel_idx ? texel_idx + (int64_t)f0 * 2 * h * w : nullptr, st);
+                                    texel_idx ? texel_idx + (int64_t)f0 * 2 * h * w : nullptr, st,
+                                    g_feat5_dbg ? g_feat5_dbg + (int64_t)f0 * h * w * 4 : nullptr);
         if (s != NSM_OK) return s;
     }
     return check_stream_err();

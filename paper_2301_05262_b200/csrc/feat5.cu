@@ -41,8 +41,8 @@ namespace {
 
 constexpr int F5_TY = 8, F5_TX = 32, F5_THREADS = F5_TY * F5_TX;
 constexpr int F5_R = 8;                      // window rows ri-8 .. ri+7 (16 x 16)
-constexpr int F5_MAX_TEX = 6144;             // staged texels per CTA (regions + block maps: 72 KB)
-constexpr int F5_SMEM = F5_MAX_TEX * 4 + F5_MAX_TEX * 8;
+constexpr int F5_MAX_TEX = 6144;             // staged texels per CTA (both regions)
+constexpr int F5_SMEM = 3 * F5_MAX_TEX * 4;   // texels + sliding 4x4 blocks (int2): 72 KB, 3 CTAs per SM
 constexpr int kInfBits = 0x7f800000;
 
 struct Feat5Args {
@@ -55,21 +55,29 @@ struct Feat5Args {
     void* out;         // 16-bit (N, 3, H0, W0, 8) or fp32 (N, 5, h, w)
     int64_t* first_bad;
     int32_t* tidx;     // parity hook (nullable): (N, 2, h, w)
+    int32_t* dbg;      // debugging (nullable): (N, h, w, 4) zmin, zmax, thr, path bits
 };
 
 // analysis.penumbra_extents (analysis.py:240-269) -> screen width
 // (x_a + x_b) * focal_px / d (analysis.py:319-320), fp32 (the plane is
 // rounded to 16 bits right after); 0 where the model's preconditions fail.
+// The reference's angles are theta = atan(T), T = (bq + r_e) / z_f, and
+// theta_d = asin(s), s = r_s / hyp, so tan(theta -/+ theta_d) follow from
+// the tangent addition formula with tan(theta_d) = s / sqrt(1 - s^2) -- no
+// transcendental calls -- and theta + theta_d < pi / 2 is 1 - T tan(theta_d) > 0.
 __device__ __forceinline__ float penumbra_width_f(float zmin, float zmax, float zf, float re, float focal,
                                                   float d) {
     const float zm = 0.5f * (zmax + zmin), rs = 0.5f * (zmax - zmin);
     const float hyp = sqrtf(zm * zm + re * re);
     if (!(zmin > 0.f && zmax >= zmin && zf > zmax && zm > 0.f && rs <= hyp && re > 0.f)) return 0.f;
-    const float td = asinf(rs / hyp);
+    const float sn = rs / hyp;
+    const float u = sn / sqrtf(fmaxf(1.f - sn * sn, 0.f));     // tan(theta_d); inf at s = 1
     const float bq = re * (zf - zm) / zm;
-    const float th = atanf((bq + re) / zf);
-    if (!(th + td < 1.5707963267948966f)) return 0.f;
-    const float xa = zf * tanf(th - td) - re, xb = zf * tanf(th + td) - re;
+    const float T = (bq + re) / zf;                            // tan(theta)
+    const float den_p = 1.f - T * u;                           // cos(theta + theta_d) sign
+    if (!(den_p > 0.f)) return 0.f;
+    const float ta = (T - u) / (1.f + T * u), tb = (T + u) / den_p;
+    const float xa = zf * ta - re, xb = zf * tb - re;
     return (xa + xb) * focal / d;
 }
 
@@ -84,29 +92,35 @@ struct Region {
 
 __device__ __forceinline__ void stage_region(const Region& g, const float* smf, const FrameK& F, int tid) {
     if (!g.on) return;
-    for (int i = tid; i < g.RH * g.RW; i += F5_THREADS) {
-        const int r = g.R0 + i / g.RW, c = g.C0 + i % g.RW;
-        const bool in = r >= 0 && r < F.hs && c >= 0 && c < F.ws;
-        g.tex[i] = in ? __float_as_int(__ldg(smf + (int64_t)r * F.ws + c)) : kInfBits;
+    // one warp per map row, lanes along it (coalesced, no index division)
+    for (int rr = tid >> 5; rr < g.RH; rr += F5_THREADS / 32) {
+        const int r = g.R0 + rr;
+        const bool rin = r >= 0 && r < F.hs;
+        const float* src = smf + (int64_t)r * F.ws;
+        int* dst = g.tex + rr * g.RW;
+        for (int cc = tid & 31; cc < g.RW; cc += 32) {
+            const int c = g.C0 + cc;
+            dst[cc] = rin && c >= 0 && c < F.ws ? __float_as_int(__ldg(src + c)) : kInfBits;
+        }
     }
 }
 
 __device__ __forceinline__ void build_blocks(const Region& g, int tid) {
     if (!g.on) return;
     const int BW = g.RW - 3, BH = g.RH - 3;
-    for (int i = tid; i < BH * BW; i += F5_THREADS) {
-        const int r = i / BW, c = i % BW;
-        int mn = kInfBits, mx = 0;
+    for (int r = tid >> 5; r < BH; r += F5_THREADS / 32)
+        for (int c = tid & 31; c < BW; c += 32) {
+            int mn = kInfBits, mx = 0;
 #pragma unroll
-        for (int dy = 0; dy < 4; ++dy) {
-            const int* row = g.tex + (r + dy) * g.RW + c;
-            mn = __vimin3_s32(row[0], row[1], mn);
-            mn = __vimin3_s32(row[2], row[3], mn);
-            mx = __vimax3_s32(row[0], row[1], mx);
-            mx = __vimax3_s32(row[2], row[3], mx);
+            for (int dy = 0; dy < 4; ++dy) {
+                const int* row = g.tex + (r + dy) * g.RW + c;
+                mn = __vimin3_s32(row[0], row[1], mn);
+                mn = __vimin3_s32(row[2], row[3], mn);
+                mx = __vimax3_s32(row[0], row[1], mx);
+                mx = __vimax3_s32(row[2], row[3], mx);
+            }
+            g.blk[r * BW + c] = make_int2(mn, mx);
         }
-        g.blk[i] = make_int2(mn, mx);
-    }
 }
 
 __device__ __forceinline__ int region_texels(const int (&b)[4]) {
@@ -148,7 +162,7 @@ __device__ __forceinline__ void block_bbox(const int (&ri)[4], const int (&ci)[4
 }
 
 template <typename T, bool kF32>
-__global__ void __launch_bounds__(F5_THREADS) feat5_kernel(const __grid_constant__ Feat5Args a) {
+__global__ void __launch_bounds__(F5_THREADS, 3) feat5_kernel(const __grid_constant__ Feat5Args a) {
     extern __shared__ __align__(16) int smem5[];
     __shared__ int bb[2][4];
     const int f = blockIdx.z;
@@ -165,22 +179,50 @@ __global__ void __launch_bounds__(F5_THREADS) feat5_kernel(const __grid_constant
     float dv[4], pxv[4], pyv[4], pzv[4], nxv[4], nyv[4], nzv[4];
     int ri[4], ci[4];
     bool cov[4];
+    // rows 2Y and 2Y+1, columns 2X and 2X+1: 8-byte loads when w is even
+    const bool pairs = (a.w & 1) == 0 && 2 * X + 1 < a.w;
 #pragma unroll
-    for (int e = 0; e < 4; ++e) {
-        const int y = 2 * Y + (e >> 1), x = 2 * X + (e & 1);
-        const bool in = y < a.h && x < a.w;
+    for (int dy = 0; dy < 2; ++dy) {
+        const int y = 2 * Y + dy, x = 2 * X;
+        const int e0 = 2 * dy, e1 = e0 + 1;
         const int64_t p = (int64_t)y * a.w + x;
-        dv[e] = in ? __ldg(gd + p) : 0.f;
-        cov[e] = dv[e] > 0.f;
-        pxv[e] = pyv[e] = pzv[e] = nxv[e] = nyv[e] = nzv[e] = 0.f;
-        ri[e] = ci[e] = 0;
-        if (cov[e]) {
-            pxv[e] = __ldg(gp + p);
-            pyv[e] = __ldg(gp + hw + p);
-            pzv[e] = __ldg(gp + 2 * hw + p);
-            nxv[e] = __ldg(gn + p);
-            nyv[e] = __ldg(gn + hw + p);
-            nzv[e] = __ldg(gn + 2 * hw + p);
+        if (y < a.h && pairs) {
+            const float2 dd = __ldg(reinterpret_cast<const float2*>(gd + p));
+            dv[e0] = dd.x;
+            dv[e1] = dd.y;
+        } else {
+            dv[e0] = y < a.h && x < a.w ? __ldg(gd + p) : 0.f;
+            dv[e1] = y < a.h && x + 1 < a.w ? __ldg(gd + p + 1) : 0.f;
+        }
+        cov[e0] = dv[e0] > 0.f;
+        cov[e1] = dv[e1] > 0.f;
+        pxv[e0] = pyv[e0] = pzv[e0] = nxv[e0] = nyv[e0] = nzv[e0] = 0.f;
+        pxv[e1] = pyv[e1] = pzv[e1] = nxv[e1] = nyv[e1] = nzv[e1] = 0.f;
+        ri[e0] = ci[e0] = ri[e1] = ci[e1] = 0;
+        if (pairs && (cov[e0] || cov[e1])) {
+            auto ld2 = [&](const float* b, float& u, float& v) {
+                const float2 t = __ldg(reinterpret_cast<const float2*>(b + p));
+                u = t.x;
+                v = t.y;
+            };
+            ld2(gp, pxv[e0], pxv[e1]);
+            ld2(gp + hw, pyv[e0], pyv[e1]);
+            ld2(gp + 2 * hw, pzv[e0], pzv[e1]);
+            ld2(gn, nxv[e0], nxv[e1]);
+            ld2(gn + hw, nyv[e0], nyv[e1]);
+            ld2(gn + 2 * hw, nzv[e0], nzv[e1]);
+        } else {
+#pragma unroll
+            for (int e = e0; e <= e1; ++e) {
+                if (!cov[e]) continue;
+                const int64_t q = p + (e - e0);
+                pxv[e] = __ldg(gp + q);
+                pyv[e] = __ldg(gp + hw + q);
+                pzv[e] = __ldg(gp + 2 * hw + q);
+                nxv[e] = __ldg(gn + q);
+                nyv[e] = __ldg(gn + hw + q);
+                nzv[e] = __ldg(gn + 2 * hw + q);
+            }
         }
     }
 #pragma unroll
@@ -217,8 +259,8 @@ __global__ void __launch_bounds__(F5_THREADS) feat5_kernel(const __grid_constant
     }
     // regions: A = cluster 0 (or all), B = cluster 1; staged if they fit
     const float* smf = a.sm + (int64_t)f * a.sm_stride;
-    int* regs = smem5;                                        // depth bits
-    int2* blks = reinterpret_cast<int2*>(smem5 + F5_MAX_TEX);  // sliding 4x4 (min, max)
+    int* regs = smem5;                                           // depth bits
+    int2* blks = reinterpret_cast<int2*>(smem5 + F5_MAX_TEX);     // sliding 4x4 (min, max)
     Region RA, RB;
     RA.R0 = bb[0][0] - F5_R;
     RA.C0 = bb[0][2] - F5_R;
@@ -240,38 +282,41 @@ __global__ void __launch_bounds__(F5_THREADS) feat5_kernel(const __grid_constant
     __syncthreads();
     build_blocks(RA, tid);
     build_blocks(RB, tid);
-    __syncthreads();
 
-    // per pixel: the 4 reference planes (fp32 math as the fused 4-plane
-    // producer) and the blocker plane
+    // phase A, per pixel: the 4 reference planes (fp32 math as the fused
+    // 4-plane producer), the exact blocker threshold, the window key
     float feat[4][5];
+    float zfv[4];
+    int thrv[4], key[4];
     const double bias = F.bias;
-    const float re = (float)(F.size_index * (0.5 / 2.0 / 4.0));       // scene.emitter_radius
-    const float focal = (float)((F.ch / 2.0) / F.half_h);              // CameraPose.focal_px
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
 #pragma unroll
         for (int k = 0; k < 5; ++k) feat[e][k] = 0.f;
+        zfv[e] = 1.f;
+        thrv[e] = 0;
+        key[e] = -2;                                    // -2 uncovered, -1 window not staged
         if (!cov[e]) continue;
         // z_f in fp64 as render_gbuffer (raster.py:228): the blocker test
         // t < z_f - b must classify exactly like the fp64 oracle
         const double tx = F.ec[0] - (double)pxv[e], ty = F.ec[1] - (double)pyv[e], tz = F.ec[2] - (double)pzv[e];
         const double zf64 = sqrt(__dadd_rn(__dadd_rn(__dmul_rn(tx, tx), __dmul_rn(ty, ty)), __dmul_rn(tz, tz)));
         const float zf = (float)zf64;
+        zfv[e] = zf;
+        thrv[e] = __float_as_int(__double2float_ru(zf64 - bias));   // t < thr64 <=> t < thr (fp32 t)
         const float izf = 1.f / zf;
         const float ftx = (float)tx, fty = (float)ty, ftz = (float)tz;
         const float ce = __saturatef((nxv[e] * ftx + nyv[e] * fty + nzv[e] * ftz) * izf);
         const float dx = F.fcp[0] - pxv[e], dy = F.fcp[1] - pyv[e], dz = F.fcp[2] - pzv[e];
         const float cc = __saturatef((nxv[e] * dx + nyv[e] * dy + nzv[e] * dz) * rsqrtf(dx * dx + dy * dy + dz * dz));
         const int tr = ri[e], tc = ci[e];
-        // this pixel's region
         const bool k1 = cl[e] != 0;
         const bool st = k1 ? RB.on : RA.on;
-        const int* reg = k1 ? RB.tex : RA.tex;
         const int W_ = k1 ? RB.RW : RA.RW;
-        const int Rk = k1 ? RB.R0 : RA.R0, Ck = k1 ? RB.C0 : RA.C0;
-        const float look = st ? __int_as_float(reg[(tr - Rk) * W_ + (tc - Ck)])
-                              : __ldg(smf + (int64_t)tr * F.ws + tc);
+        const int loc = (tr - (k1 ? RB.R0 : RA.R0)) * W_ + (tc - (k1 ? RB.C0 : RA.C0));
+        const float look = st ? __int_as_float((k1 ? RB.tex : RA.tex)[loc]) : __ldg(smf + (int64_t)tr * F.ws + tc);
+        if (st) key[e] = (k1 ? usedA : 0) + loc;
+        else key[e] = -1;
         float ch0 = 0.f, ch1 = 1.f;
         if (look < INFINITY) {                                       // raster.py:262
             const float m = fminf(look, zf);
@@ -282,63 +327,86 @@ __global__ void __launch_bounds__(F5_THREADS) feat5_kernel(const __grid_constant
         feat[e][1] = ch1;
         feat[e][2] = ce + F.fsize;
         feat[e][3] = cc / dv[e];
-        // blocker search over rows tr-8 .. tr+7, cols tc-8 .. tc+7
-        const int thr = __float_as_int(__double2float_ru(zf64 - bias));   // t < thr64 <=> t < thr (fp32 t)
+    }
+    __syncthreads();   // block maps built
+    // phase 3, per pixel: combine the window summary with its own threshold
+    const float re = (float)(F.size_index * (0.5 / 2.0 / 4.0));       // scene.emitter_radius
+    const float focal = (float)((F.ch / 2.0) / F.half_h);              // CameraPose.focal_px
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+        if (key[e] == -2) continue;
+        const int thr = thrv[e];
         const unsigned thr1 = (unsigned)thr - 1u;
-        int zmin = kInfBits;
-        unsigned um = 0xffffffffu;
-        if (st) {
-            const int r0 = tr - F5_R - Rk, c0 = tc - F5_R - Ck, BW = W_ - 3;
-            const int2* blk = k1 ? RB.blk : RA.blk;
-            unsigned strad = 0;
+        const int tr = ri[e], tc = ci[e];
+        int zmin = kInfBits, zmx = -1;
+        {
+            // the pixel's scan: over the staged blocks, or straight from global
+            // memory (window outside the staged regions)
+            unsigned um = 0xffffffffu;
+            zmin = kInfBits;
+            const bool k1 = cl[e] != 0;
+            const bool st = k1 ? RB.on : RA.on;
+            if (st) {
+                const int W_ = k1 ? RB.RW : RA.RW, BW = W_ - 3;
+                const int r0 = tr - F5_R - (k1 ? RB.R0 : RA.R0), c0 = tc - F5_R - (k1 ? RB.C0 : RA.C0);
+                const int2* blk = k1 ? RB.blk : RA.blk;
+                const int* reg = k1 ? RB.tex : RA.tex;
+                unsigned strad = 0;
 #pragma unroll
-            for (int b = 0; b < 16; ++b) {
-                const int2 mm = blk[(r0 + 4 * (b >> 2)) * BW + c0 + 4 * (b & 3)];
-                zmin = min(zmin, mm.x);
-                if (mm.y < thr) um = min(um, thr1 - (unsigned)mm.y);       // all blockers
-                else if (mm.x < thr) strad |= 1u << b;                    // straddles the threshold
-            }
-            while (strad) {
-                const int b = __ffs(strad) - 1;
-                strad &= strad - 1;
-                const int* p = reg + (r0 + 4 * (b >> 2)) * W_ + c0 + 4 * (b & 3);
+                for (int b = 0; b < 16; ++b) {
+                    const int2 mm = blk[(r0 + 4 * (b >> 2)) * BW + c0 + 4 * (b & 3)];
+                    zmin = min(zmin, mm.x);
+                    if (mm.y < thr) um = min(um, thr1 - (unsigned)mm.y);
+                    else if (mm.x < thr) strad |= 1u << b;
+                }
+                while (strad) {
+                    const int b = __ffs(strad) - 1;
+                    strad &= strad - 1;
+                    const int* p = reg + (r0 + 4 * (b >> 2)) * W_ + c0 + 4 * (b & 3);
 #pragma unroll
-                for (int dy = 0; dy < 4; ++dy)
+                    for (int dy = 0; dy < 4; ++dy)
 #pragma unroll
-                    for (int dxx = 0; dxx < 4; ++dxx)
-                        um = __viaddmin_u32(thr1, (unsigned)(-p[dy * W_ + dxx]), um);
-            }
-        } else if (tr >= F5_R && tr + F5_R <= F.hs && tc >= F5_R && tc + F5_R <= F.ws) {
-            // window outside the staged regions, inside the map: 16 texel
-            // rows straight from global memory (L1), 16 loads in flight
-            const float* rowp = smf + (int64_t)(tr - F5_R) * F.ws + (tc - F5_R);
-            for (int r = 0; r < 2 * F5_R; ++r, rowp += F.ws) {
-                int t[16];
+                        for (int dxx = 0; dxx < 4; ++dxx)
+                            um = __viaddmin_u32(thr1, (unsigned)(-p[dy * W_ + dxx]), um);
+                }
+            } else if (tr >= F5_R && tr + F5_R <= F.hs && tc >= F5_R && tc + F5_R <= F.ws) {
+                // 16 texel rows from global memory (L1), 16 loads in flight
+                const float* rowp = smf + (int64_t)(tr - F5_R) * F.ws + (tc - F5_R);
+                for (int r = 0; r < 2 * F5_R; ++r, rowp += F.ws) {
+                    int t[16];
 #pragma unroll
-                for (int c = 0; c < 16; ++c) t[c] = __float_as_int(__ldg(rowp + c));
+                    for (int c = 0; c < 16; ++c) t[c] = __float_as_int(__ldg(rowp + c));
 #pragma unroll
-                for (int c = 0; c < 16; c += 2) {
-                    zmin = __vimin3_s32(t[c], t[c + 1], zmin);
-                    um = __viaddmin_u32(thr1, (unsigned)(-t[c]), um);
-                    um = __viaddmin_u32(thr1, (unsigned)(-t[c + 1]), um);
+                    for (int c = 0; c < 16; c += 2) {
+                        zmin = __vimin3_s32(t[c], t[c + 1], zmin);
+                        um = __viaddmin_u32(thr1, (unsigned)(-t[c]), um);
+                        um = __viaddmin_u32(thr1, (unsigned)(-t[c + 1]), um);
+                    }
+                }
+            } else {
+                // window clipped by the map border (rare): bounds-checked scan
+                for (int r = tr - F5_R; r < tr + F5_R; ++r) {
+                    if (r < 0 || r >= F.hs) continue;
+                    for (int c = tc - F5_R; c < tc + F5_R; ++c) {
+                        if (c < 0 || c >= F.ws) continue;
+                        const int t = __float_as_int(__ldg(smf + (int64_t)r * F.ws + c));
+                        zmin = min(zmin, t);
+                        um = __viaddmin_u32(thr1, (unsigned)(-t), um);
+                    }
                 }
             }
-        } else {
-            // window clipped by the map border (rare): bounds-checked scan
-            for (int r = tr - F5_R; r < tr + F5_R; ++r) {
-                if (r < 0 || r >= F.hs) continue;
-                for (int c = tc - F5_R; c < tc + F5_R; ++c) {
-                    if (c < 0 || c >= F.ws) continue;
-                    const int t = __float_as_int(__ldg(smf + (int64_t)r * F.ws + c));
-                    zmin = min(zmin, t);
-                    um = __viaddmin_u32(thr1, (unsigned)(-t), um);
-                }
-            }
+            zmx = (int)(thr1 - um);
         }
-        if (zmin < thr) {                                          // blockers exist
-            const float zmx = __int_as_float((int)(thr1 - um));
-            feat[e][4] = penumbra_width_f(__int_as_float(zmin), zmx, zf, re, focal, dv[e]);
+        if (a.dbg) {
+            const int y = 2 * Y + (e >> 1), x = 2 * X + (e & 1);
+            int32_t* d4 = a.dbg + (((int64_t)f * a.h + y) * a.w + x) * 4;
+            d4[0] = zmin;
+            d4[1] = zmx;
+            d4[2] = thr;
+            d4[3] = (key[e] < 0 ? 1 : 0) | (cl[e] << 3);
         }
+        if (zmin < thr)                                            // blockers exist
+            feat[e][4] = penumbra_width_f(__int_as_float(zmin), __int_as_float(zmx), zfv[e], re, focal, dv[e]);
     }
 
     if constexpr (kF32) {
@@ -383,7 +451,7 @@ __global__ void __launch_bounds__(F5_THREADS) feat5_kernel(const __grid_constant
 // fp32 mode: planes (nf, 5, h, w).  first_bad must be pre-filled.
 nsm_status launch_feat5(const nsm_gbuffer* g, const float* sm, int64_t sm_stride, const nsm_frame* frames,
                         int nf, int h, int w, int H0, int W0, void* out, int out_kind, int64_t* first_bad,
-                        int32_t* tidx, cudaStream_t st) {
+                        int32_t* tidx, cudaStream_t st, int32_t* dbg) {
     if (g->dtype != NSM_F32 || g->z_f || g->c_e || g->c_c || g->coverage)
         return fail(NSM_ERR_UNSUPPORTED, "the 5-plane feature pass reads fp32 d / normal / position planes");
     if (nf > NSM_MAX_FRAMES_PER_LAUNCH) return fail(NSM_ERR_ARG, "launch_feat5: too many frames");
@@ -399,6 +467,7 @@ nsm_status launch_feat5(const nsm_gbuffer* g, const float* sm, int64_t sm_stride
     a.out = out;
     a.first_bad = first_bad;
     a.tidx = tidx;
+    a.dbg = dbg;
     // 16-bit: every level-0 pixel of the padded grid; fp32: the frame's pixels
     const int LX = out_kind == 2 ? (w + 1) / 2 : W0, LY = out_kind == 2 ? (h + 1) / 2 : H0;
     dim3 grid((LX + F5_TX - 1) / F5_TX, (LY + F5_TY - 1) / F5_TY, nf);

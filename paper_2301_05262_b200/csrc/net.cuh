@@ -66,7 +66,7 @@ void launch_fill_i64(int64_t* p, int n, int64_t v, cudaStream_t st);
 // (nf, 5, h, w).  first_bad pre-filled by the caller.
 nsm_status launch_feat5(const nsm_gbuffer* g, const float* sm, int64_t sm_stride, const nsm_frame* frames,
                         int nf, int h, int w, int H0, int W0, void* out, int out_kind, int64_t* first_bad,
-                        int32_t* tidx, cudaStream_t st);
+                        int32_t* tidx, cudaStream_t st, int32_t* dbg = nullptr);
 nsm_status launch_blocker(const nsm_gbuffer* g, const float* sm, int64_t sm_stride, const nsm_frame* frames,
                           int32_t n, int32_t h, int32_t w, int32_t radius, float* out, int64_t* first_bad,
                           cudaStream_t st);
