@@ -469,6 +469,26 @@ def run_ours(args):
               {"features": other, "network": f"NetworkConfig(in_channels={other})"})
         torch.cuda.synchronize()
 
+    # ---- bf16 precision record (config 5's dtype cannot meet the 1e-2
+    # max-abs bar at large emitters, see tests/test_gpu_f16.py): the bf16
+    # visibility of this rank's first frames against the fp16 plan's, which
+    # the tests hold within 1e-2 / 1e-4 of the fp32 oracle ----
+    precision = None
+    if args.dtype == "bf16" and not args.no_variants:
+        sub = frames[:2]
+        sin = {k: v[:len(sub)].contiguous() for k, v in inputs.items()}
+        fargs = argparse.Namespace(**{**vars(args), "dtype": "fp16"})
+        _, _, fplan = make_plan(fargs)
+        yb = ShadowInference(plan, sub, out_dtype="fp32")(sin).double()
+        yf = ShadowInference(fplan, sub, out_dtype="fp32")(sin).double()
+        d = yb - yf
+        precision = {"bf16_vs_fp16_plan_max_abs": round(float(d.abs().max()), 5),
+                     "bf16_vs_fp16_plan_mse": float((d * d).mean()),
+                     "frames": [f"size_index {f.size_index:.2f}" for f in sub],
+                     "bars": "fp16 meets 1e-2 max-abs / 1e-4 MSE vs the fp32 oracle; bf16 meets MSE only "
+                             "(4K size_index 8: see tests/test_gpu_f16.py)"}
+        del yb, yf, fplan
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         planes = {k: v[0].cpu().numpy() for k, v in inputs.items()}
@@ -504,6 +524,7 @@ def run_ours(args):
             "cpu_baseline": cpu,
             "e2e": e2e,
             "variants": variants,
+            "precision": precision,
             "gathered": gathered,
             "gpu_launches": int(per_step * args.steps),
             "clocks": clocks,
