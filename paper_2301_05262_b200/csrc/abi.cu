@@ -201,11 +201,17 @@ nsm_status check_device(const Plan& p) {
     return NSM_OK;
 }
 
+// the unfused path of nsm_infer: fp32 feature planes (padded), the forward's
+// workspace, the padded visibility (fp32 plans and the generic 16-bit ones)
+size_t forward_any_workspace(const Plan& p, int n, int h, int w) {
+    return p.act == NSM_F32 ? forward_f32_workspace(p, n, h, w) : forward_gen16_workspace(p, n, h, w);
+}
+
 size_t infer_f32_workspace(const Plan& p, int n, int h, int w) {
     const int m = 1 << (p.cfg.layers - 1);
     const int hp = round_up(h, m), wp = round_up(w, m);
     return (size_t)n * 4 * hp * wp * 4 + (size_t)n * hp * wp * 4 + 256 +
-           forward_f32_workspace(p, n, hp, wp);
+           forward_any_workspace(p, n, hp, wp);
 }
 
 }  // namespace
@@ -361,7 +367,7 @@ size_t nsm_workspace_size(const nsm_plan* plan, int32_t n, int32_t h, int32_t w)
     // 16-bit plans run every entry point on the chunked 16-bit kernels, whose
     // workspace is bounded by the chunk, not by n
     if (p->act != NSM_F32 && f16_supported(*p)) return infer_f16_workspace(*p, n, h, w);
-    size_t a = forward_f32_workspace(*p, n, hp, wp);
+    size_t a = forward_any_workspace(*p, n, hp, wp);
     size_t b = infer_f32_workspace(*p, n, h, w);
     return std::max(a, b);
 }
@@ -432,8 +438,8 @@ nsm_status nsm_forward(const nsm_plan* plan, const float* x, int32_t n, int32_t 
     if (nsm_status s = check_device(*p)) return s;
     if (p->act == NSM_F32)
         return forward_f32(*p, x, n, h, w, y, workspace, ws_bytes, (cudaStream_t)stream);
-    if (!f16_supported(*p))
-        return fail(NSM_ERR_UNSUPPORTED, "no 16-bit kernels for this NetworkConfig");
+    if (!f16_supported(*p))   // the generic layer-by-layer 16-bit path
+        return forward_gen16(*p, x, n, h, w, y, workspace, ws_bytes, (cudaStream_t)stream);
     return forward_f16(*p, x, n, h, w, y, workspace, ws_bytes, (cudaStream_t)stream);
 }
 
@@ -457,9 +463,9 @@ nsm_status nsm_infer_ex(const nsm_plan* plan, const nsm_gbuffer* g, const float*
     if (y_dtype != NSM_F32 && y_dtype != NSM_F16) return fail(NSM_ERR_ARG, "y_dtype must be F32 or F16");
     // the feature pass produces the 4 reference planes, plus the
     // blocker-search penumbra plane for in_channels = 5 nets (16-bit plans)
-    if (p->cfg.in_channels == 5 && p->act == NSM_F32)
-        return fail(NSM_ERR_UNSUPPORTED, "fp32 plans run the 4-plane feature pass; a 5-plane net needs a 16-bit "
-                                         "plan (or nsm_features5 + nsm_forward)");
+    if (p->cfg.in_channels == 5 && (p->act == NSM_F32 || !f16_supported(*p)))
+        return fail(NSM_ERR_UNSUPPORTED, "the fused 5-plane feature pass runs with the default 16-bit net; "
+                                         "use nsm_features5 + nsm_forward");
     if (p->cfg.in_channels != 4 && p->cfg.in_channels != 5)
         return fail(NSM_ERR_SHAPE, "input has 4 channels, config wants %d", p->cfg.in_channels);
     if (g->dtype != NSM_F32 && g->dtype != NSM_F64)
@@ -469,9 +475,7 @@ nsm_status nsm_infer_ex(const nsm_plan* plan, const nsm_gbuffer* g, const float*
     if (nsm_status s = check_frames(frames, n, h, w, sm_stride)) return s;
     if (nsm_status s = check_device(*p)) return s;
     cudaStream_t st = (cudaStream_t)stream;
-    if (p->act != NSM_F32) {
-        if (!f16_supported(*p))
-            return fail(NSM_ERR_UNSUPPORTED, "no 16-bit kernels for this NetworkConfig");
+    if (p->act != NSM_F32 && f16_supported(*p)) {
         return infer_f16(*p, g, sm, sm_stride, frames, n, h, w, y, y_dtype, first_bad, texel_idx,
                          workspace, ws_bytes, st);
     }
@@ -489,8 +493,10 @@ nsm_status nsm_infer_ex(const nsm_plan* plan, const nsm_gbuffer* g, const float*
                                    first_bad, st);
     if (s != NSM_OK) return s;
     const bool direct = (hp == h && wp == w && y_dtype == NSM_F32);
-    s = forward_f32(*p, feat, n, hp, wp, direct ? (float*)y : yfull, rest,
-                    ws_bytes - (size_t)(rest - (char*)workspace), st);
+    float* yo = direct ? (float*)y : yfull;
+    const size_t rest_bytes = ws_bytes - (size_t)(rest - (char*)workspace);
+    s = p->act == NSM_F32 ? forward_f32(*p, feat, n, hp, wp, yo, rest, rest_bytes, st)
+                          : forward_gen16(*p, feat, n, hp, wp, yo, rest, rest_bytes, st);
     if (s != NSM_OK) return s;
     if (!direct) {
         const int64_t tot = (int64_t)n * h * w;

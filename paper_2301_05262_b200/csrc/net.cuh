@@ -46,6 +46,11 @@ size_t forward_f32_workspace(const Plan& p, int n, int h, int w);
 nsm_status forward_f32(const Plan& p, const float* x, int n, int h, int w, float* out, void* ws,
                        size_t ws_bytes, cudaStream_t st);
 
+// generic fp16 / bf16 tensor-core path for any NetworkConfig (net_gen16.cu)
+size_t forward_gen16_workspace(const Plan& p, int n, int h, int w);
+nsm_status forward_gen16(const Plan& p, const float* x, int n, int h, int w, float* out, void* ws,
+                         size_t ws_bytes, cudaStream_t st);
+
 // fp16 / bf16 tensor-core path (net_f16.cu)
 bool f16_supported(const Plan& p);
 size_t infer_f16_workspace(const Plan& p, int n, int h, int w);

@@ -1,0 +1,56 @@
+"""Generic 16-bit path (net_gen16.cu) for every NetworkConfig the
+reference accepts that the level-fused kernels do not cover (needs a B200).
+
+Against the reference's own network.forward outputs (tests/golden/nets.npz:
+layers 2-6, in_channels 1/5, plain (no space-to-depth) mode, channel caps,
+base 8) at the 16-bit bars of north_star: fp16 within 1e-2 max-abs and 1e-4
+MSE; bf16 within the MSE bar (its max-abs is printed: bf16 keeps 8 mantissa
+bits, see test_gpu_f16.py).  Plus the fused nsm_infer entry on a generic
+plan vs the oracle (features -> layers=4 net)."""
+
+import numpy as np
+import pytest
+
+from conftest import golden_nets, golden_camera, golden_view, load_golden
+
+pytestmark = pytest.mark.gpu
+
+NETS = golden_nets()
+
+
+@pytest.mark.parametrize("dtype", ["fp16", "bf16"])
+@pytest.mark.parametrize("name", sorted(NETS))
+def test_generic16_forward_matches_reference(name, dtype):
+    from paper_2301_05262_b200 import network
+    c = NETS[name]
+    layers, base, inc, s2d, cap = (int(v) for v in c["cfg"])
+    cfg = network.NetworkConfig(layers, base, inc, bool(s2d), cap)
+    y = network.forward(c["w"], cfg, c["x"], dtype=dtype).data
+    d = np.asarray(y, np.float64) - c["y"]
+    mx, mse = float(np.abs(d).max()), float(np.mean(d * d))
+    print(f"{name} {cfg} {dtype}: max {mx:.3g} mse {mse:.3g}")
+    assert y.shape == c["y"].shape
+    assert mse <= 1e-4
+    if dtype == "fp16":
+        assert mx <= 1e-2
+
+
+def test_generic16_infer_layers4_vs_oracle(cfg1):
+    """nsm_infer on a layers=4 fp16 plan (feature pass -> generic net ->
+    crop) vs the oracle on the reference golden frame."""
+    from types import SimpleNamespace
+    import torch
+    from oracle import network as on
+    from paper_2301_05262_b200 import network
+    from paper_2301_05262_b200.infer import ShadowInference
+    r = cfg1
+    cfg = network.NetworkConfig(layers=4)
+    w = network.init_weights(cfg, np.random.default_rng(np.random.SeedSequence([2, 0x11])))
+    fr = SimpleNamespace(camera=golden_camera(r), view=golden_view(r), size_index=float(r["size_index"]),
+                         bias=float(r["bias"]), scene=SimpleNamespace(emitter_center=r["emitter_center"]))
+    inp = {k: torch.from_numpy(np.ascontiguousarray(r[k][None])).cuda() for k in ("d", "normal", "position", "sm")}
+    y = ShadowInference(network.Plan(w, cfg, "fp16"), [fr])(inp)[0, 0].cpu().numpy()
+    ref = on.forward({k: v.data for k, v in w.items()}, r["features"], layers=4)[0]
+    d = y.astype(np.float64) - ref
+    print(f"layers=4 infer fp16: max {np.abs(d).max():.3g} mse {np.mean(d * d):.3g}")
+    assert np.abs(d).max() <= 1e-2 and np.mean(d * d) <= 1e-4
