@@ -308,7 +308,8 @@ def ncu_traffic(kernel, algo_bytes, frames_per_launch, workload):
     if not os.path.exists(p):
         return None
     with open(p) as f:
-        t = json.load(f).get(kernel)
+        tab = json.load(f)
+    t = tab.get(kernel) if workload == "cfg4-1080p-soft-window8" else tab.get(f"{kernel}@{workload}")
     if not t or t.get("workload") != workload:
         return None
     bpf = t["dram_bytes_per_frame"]

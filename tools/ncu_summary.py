@@ -96,18 +96,22 @@ def full(path):
 
 
 KMAP = {"enc0_kernel": "enc0_fused", "dec0p_kernel": "dec0_fused", "dec0_ring_kernel": "dec0_ring",
-        "recon_kernel": "recon"}
+        "recon_kernel": "recon", "feat5_kernel": "feat5_blocker", "enc0_s2d_kernel": "enc0_s2d"}
 
 
 def traffic(path, frames_per_launch, out, source, workload="cfg4-1080p-soft-window8"):
     """profiles/traffic.json for bench.py's roofline.traffic: DRAM bytes per
     frame of each kernel's first launch in a --set full report."""
     _, recs = full(path)
-    res = {}
+    import os
+    res = json.load(open(out)) if os.path.exists(out) else {}
+    res = {k: v for k, v in res.items() if v.get("workload") != workload}   # replace this workload's rows
+    seen = set()
     for r in recs:
         for k, name in KMAP.items():
-            if k in r["kernel"] and name not in res and "dram_read_MB" in r:
-                res[name] = {"dram_bytes_per_frame": (r["dram_read_MB"] + r["dram_write_MB"]) * 1e6 /
+            if k in r["kernel"] and name not in seen and "dram_read_MB" in r:
+                seen.add(name)
+                res[name if workload == "cfg4-1080p-soft-window8" else f"{name}@{workload}"] = {"dram_bytes_per_frame": (r["dram_read_MB"] + r["dram_write_MB"]) * 1e6 /
                              frames_per_launch, "source": source, "workload": workload}
     json.dump(res, open(out, "w"), indent=1)
     print(json.dumps(res, indent=1))
@@ -115,8 +119,8 @@ def traffic(path, frames_per_launch, out, source, workload="cfg4-1080p-soft-wind
 
 if __name__ == "__main__":
     mode, path = sys.argv[1], sys.argv[2]
-    if mode == "traffic":      # traffic <report> <frames_per_launch> <out.json> <source-label>
-        traffic(path, int(sys.argv[3]), sys.argv[4], sys.argv[5])
+    if mode == "traffic":      # traffic <report> <frames_per_launch> <out.json> <source-label> [workload]
+        traffic(path, int(sys.argv[3]), sys.argv[4], sys.argv[5], *sys.argv[6:7])
     elif mode == "launches":
         print(launches(path))
     else:
