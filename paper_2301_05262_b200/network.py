@@ -258,7 +258,7 @@ class Plan:
 
     def __del__(self):
         h = getattr(self, "_h", None)
-        if h:
+        if h and _lib is not None and getattr(_lib, "lib", None) is not None:   # not at interpreter teardown
             _lib.lib.nsm_plan_destroy(h)
             self._h = None
 

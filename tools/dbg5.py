@@ -26,3 +26,14 @@ for y, x in bad[:10]:
     print(y, x, "idx", I[:, y, x], (r, c), "gpu zmin/zmax/thr/path", D[y, x], "exact zmin", W.min(), "zmax", bl.max() if len(bl) else -1)
 P = D[..., 3][cov]
 print("covered", cov.sum(), "not staged", (P & 1).mean(), "alone", ((P & 2) > 0).mean(), "owners", ((P & 4) > 0).mean(), "cluster1", ((P >> 3) & 1).mean())
+ns = np.argwhere(cov & ((D[..., 3] & 1) == 1))
+print("not staged sample", [(int(y), int(x), int(I[0, y, x]), int(I[1, y, x])) for y, x in ns[:8]])
+tiles = {}
+for y, x in ns:
+    tiles.setdefault((y // 16, x // 64), 0)
+    tiles[(y // 16, x // 64)] += 1
+print("tiles", len(tiles), sorted(tiles.items(), key=lambda kv: -kv[1])[:6])
+t0 = sorted(tiles.items(), key=lambda kv: -kv[1])[0][0]
+m = cov[t0[0]*16:(t0[0]+1)*16, t0[1]*64:(t0[1]+1)*64]
+rr = I[0, t0[0]*16:(t0[0]+1)*16, t0[1]*64:(t0[1]+1)*64][m]; cc = I[1, t0[0]*16:(t0[0]+1)*16, t0[1]*64:(t0[1]+1)*64][m]
+print("tile", t0, "covered", m.sum(), "rows", rr.min(), rr.max(), "cols", cc.min(), cc.max())

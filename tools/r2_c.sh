@@ -1,5 +1,5 @@
 mkdir -p gpurun_out
-timeout 400 python -m pytest tests/test_gpu_blocker5.py -m gpu -q -rf -x > gpurun_out/pytest_c.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_c.log
+[ -n "$SKIPT" ] || timeout 400 python -m pytest tests/test_gpu_blocker5.py -m gpu -q -rf -x > gpurun_out/pytest_c.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_c.log
 timeout 120 python bench.py --steps 20 --warmup 5 --no-cpu-baseline --no-e2e --no-variants "$@" > gpurun_out/bench_c.log 2>&1; echo "rc=$?" >> gpurun_out/bench_c.log
 tail -4 gpurun_out/pytest_c.log
 python - <<PY
