@@ -350,6 +350,25 @@ def time_steps(step, steps, world, soak=True, local=0):
     return e0.elapsed_time(e1) / steps, clk.summary()
 
 
+def profile_kernels(launch, steps):
+    """{kernel: (launches, total ms)} of ``steps`` eager launches, each
+    kernel bracketed by CUDA events on its stream (nsm_profile_*).  A spin
+    kernel queued first keeps the GPU busy while the host enqueues every
+    launch, so the events measure device time, not host launch latency."""
+    import torch
+    from paper_2301_05262_b200 import _lib
+    torch.cuda.synchronize()
+    _lib.lib.nsm_profile_enable(1)
+    _lib.profile_report()
+    torch.cuda._sleep(int(2e6) * (10 + 4 * steps))      # ~1 ms per step of lead at ~2 GHz
+    for _ in range(steps):
+        launch()
+    torch.cuda.synchronize()
+    prof = _lib.profile_report()
+    _lib.lib.nsm_profile_enable(0)
+    return prof
+
+
 def run_ours(args):
     import torch
     from paper_2301_05262_b200 import _lib, producer
@@ -397,13 +416,7 @@ def run_ours(args):
         dist.barrier()
 
     # ---- per-kernel timing (eager, traced launches on the same stream) ----
-    _lib.lib.nsm_profile_enable(1)
-    _lib.profile_report()
-    for _ in range(args.steps):
-        run.launch(inputs, check=False)
-    torch.cuda.synchronize()
-    prof = _lib.profile_report()
-    _lib.lib.nsm_profile_enable(0)
+    prof = profile_kernels(lambda: run.launch(inputs, check=False), args.steps)
     models, step_bytes, step_flops = kernel_models(frames, inputs, cfg, args.dtype, args.features)
     hbm, tfl, src = peaks()
     dom = max(prof, key=lambda k: prof[k][1]) if prof else None
@@ -447,13 +460,7 @@ def run_ours(args):
                 vrun.replay()
             vms, _ = time_steps(vrun.replay, args.steps, world, soak=False, local=local)
             vms_max = float(gather_floats([vms], world, dev)[:, 0].max())
-            _lib.lib.nsm_profile_enable(1)
-            _lib.profile_report()
-            for _ in range(3):
-                vrun.launch(vin, check=False)
-            torch.cuda.synchronize()
-            vprof = _lib.profile_report()
-            _lib.lib.nsm_profile_enable(0)
+            vprof = profile_kernels(lambda: vrun.launch(vin, check=False), 3)
             variants[label] = {"value": round(job_n / (vms_max / 1e3), 3), "unit": UNIT,
                                "ms_per_step": round(vms_max, 5),
                                "coverage": round(covered_pixels(vin) / (len(vframes) * h * wd), 4),
