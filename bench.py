@@ -378,6 +378,10 @@ def run_ours(args):
         sys.exit("bench.py: libnsm.so is an experiment build (NSM_EXPERIMENTS); rebuild the release library")
     rank, world, local = dist_setup()
     dev = torch.device("cuda", local)
+    if world > 1 and rank == 0:
+        nv = torch.cuda.nccl.version()
+        print(f"bench.py: NCCL {'.'.join(map(str, nv)) if isinstance(nv, tuple) else nv} communicator, "
+              f"{world} ranks, one GPU each", file=sys.stderr)
     frames, (lo, hi), job_n, scaling = rank_frames(args, rank, world)
     n = len(frames)
     inputs = producer.render_inputs(frames)
