@@ -370,14 +370,18 @@ __global__ void __launch_bounds__(F5_THREADS, 3) feat5_kernel(const __grid_const
                             um = __viaddmin_u32(thr1, (unsigned)(-p[dy * W_ + dxx]), um);
                 }
             } else if (tr >= F5_R && tr + F5_R <= F.hs && tc >= F5_R && tc + F5_R <= F.ws) {
-                // 16 texel rows from global memory (L1), 16 loads in flight
+                // 16 texel rows from global memory (L1 / L2), two rows (32
+                // loads) in flight per round trip
                 const float* rowp = smf + (int64_t)(tr - F5_R) * F.ws + (tc - F5_R);
-                for (int r = 0; r < 2 * F5_R; ++r, rowp += F.ws) {
-                    int t[16];
+                for (int r = 0; r < 2 * F5_R; r += 2, rowp += 2 * F.ws) {
+                    int t[32];
 #pragma unroll
-                    for (int c = 0; c < 16; ++c) t[c] = __float_as_int(__ldg(rowp + c));
+                    for (int c = 0; c < 16; ++c) {
+                        t[c] = __float_as_int(__ldg(rowp + c));
+                        t[16 + c] = __float_as_int(__ldg(rowp + F.ws + c));
+                    }
 #pragma unroll
-                    for (int c = 0; c < 16; c += 2) {
+                    for (int c = 0; c < 32; c += 2) {
                         zmin = __vimin3_s32(t[c], t[c + 1], zmin);
                         um = __viaddmin_u32(thr1, (unsigned)(-t[c]), um);
                         um = __viaddmin_u32(thr1, (unsigned)(-t[c + 1]), um);
