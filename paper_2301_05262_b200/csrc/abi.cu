@@ -16,7 +16,11 @@ namespace nsm {
 
 namespace {
 thread_local std::string g_err;
+#ifdef NSM_EXPERIMENTS
 int32_t* g_feat5_dbg = nullptr;   // nsm_debug_feat5: per-pixel search record of nsm_features5
+#else
+constexpr int32_t* g_feat5_dbg = nullptr;
+#endif
 }
 
 nsm_status fail(nsm_status code, const char* fmt, ...) {
@@ -223,9 +227,12 @@ extern "C" {
 
 int32_t nsm_abi_version(void) { return NSM_ABI_VERSION; }
 
-// Debug hook (not in nsm.h): the next nsm_features5 calls also write
-// (zmin, zmax, thr, path) per pixel into buf ((n, h, w, 4) int32, device).
+#ifdef NSM_EXPERIMENTS
+// Debug hook of experiment builds (not in nsm.h): the next nsm_features5
+// calls also write (zmin, zmax, thr, path) per pixel into buf ((n, h, w, 4)
+// int32, device); tools/dbg5.py.
 void nsm_debug_feat5(int32_t* buf) { g_feat5_dbg = buf; }
+#endif
 
 int32_t nsm_build_flags(void) {
 #ifdef NSM_EXPERIMENTS

@@ -14,6 +14,7 @@
 // pooling, bilinear upsampling + skip, the head reconstruction and the
 // sigmoid are small fp32-math kernels between the convs.
 #include <algorithm>
+#include <atomic>
 #include <type_traits>
 
 #include "common.cuh"
@@ -230,15 +231,28 @@ nsm_status g16_conv_launch(const T* x, int n, int h, int w, int cinp, const Conv
     if (smem > 227 * 1024) return fail(NSM_ERR_UNSUPPORTED, "generic conv: %d input channels exceed shared memory", cinp);
     dim3 grid((w + G_PX - 1) / G_PX, h, n * ((coutp + G_CO - 1) / G_CO));
     const uint2* wb = (const uint2*)c.wpk;
+    // the opt-in shared-memory size is per-device state: set it once per
+    // (device, instantiation) for the largest tile this process has used
+    auto opt_in = [&](const void* k) {
+        static std::atomic<int> set_bytes[64][3];
+        int dev = 0;
+        cudaGetDevice(&dev);
+        const int slot = (K == 3 ? 0 : f32out ? 2 : 1);
+        std::atomic<int>& cur = set_bytes[dev & 63][slot];
+        if (smem > cur.load()) {
+            cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+            cur.store(227 * 1024);
+        }
+    };
     NSM_PROF("g16_conv", st);
     if (K == 3 && !f32out) {
-        cudaFuncSetAttribute(g16_conv<T, 3, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        opt_in((const void*)g16_conv<T, 3, false>);
         g16_conv<T, 3, false><<<grid, G_THREADS, smem, st>>>(x, h, w, cinp, wb, c.b32, c.cout, coutp, relu, y);
     } else if (K == 1 && !f32out) {
-        cudaFuncSetAttribute(g16_conv<T, 1, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        opt_in((const void*)g16_conv<T, 1, false>);
         g16_conv<T, 1, false><<<grid, G_THREADS, smem, st>>>(x, h, w, cinp, wb, c.b32, c.cout, coutp, relu, y);
     } else if (K == 1) {
-        cudaFuncSetAttribute(g16_conv<T, 1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        opt_in((const void*)g16_conv<T, 1, true>);
         g16_conv<T, 1, true><<<grid, G_THREADS, smem, st>>>(x, h, w, cinp, wb, c.b32, c.cout, coutp, relu, y);
     } else {
         return fail(NSM_ERR_UNSUPPORTED, "generic conv: k=%d head", K);

@@ -219,7 +219,9 @@ class HostPipeline:
         """Enqueue one batch: ``host_inputs`` as for ShadowInference (pinned
         CPU tensors), ``host_y`` a pinned CPU tensor shaped like ``run.y``,
         ``frames`` this batch's frames (list or ``run.frame_table``; default
-        the executor's)."""
+        the executor's).  Reusing a slot first retires its previous batch:
+        if that batch had an out-of-frustum pixel, FrustumError is raised
+        and THIS batch is not enqueued (submit it again to continue)."""
         import torch
         s = self._i % self.slots
         self._retire(s)                 # the slot's previous batch (raises if it failed)

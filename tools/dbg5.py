@@ -1,3 +1,6 @@
+"""Debug dump of nsm_features5's per-pixel blocker search vs the oracle on a
+config-3 frame.  Needs an experiment build (NSM_BUILD_EXPERIMENTS=1): the
+nsm_debug_feat5 hook is not in the release library."""
 import sys, numpy as np, torch, ctypes as C
 sys.path.insert(0, '.')
 from paper_2301_05262_b200 import producer, scenes, _lib
