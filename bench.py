@@ -480,6 +480,7 @@ def run_ours(args):
         timed(frames, oplan, "blocker_search_5plane" if other == 5 else "reference_4plane",
               {"features": other, "network": f"NetworkConfig(in_channels={other})"})
         torch.cuda.synchronize()
+        variants["torch_cudnn_comparator"] = torch_comparator(args, w, frames, inputs, world, dev, local, job_n)
 
     # ---- bf16 precision record (config 5's dtype cannot meet the 1e-2
     # max-abs bar at large emitters, see tests/test_gpu_f16.py): the bf16
@@ -545,6 +546,70 @@ def run_ours(args):
     if world > 1:
         import torch.distributed as dist
         dist.destroy_process_group()
+
+
+def torch_comparator(args, w, frames, inputs, world, dev, local, job_n):
+    """The obvious library path, as a yardstick (hard part 7): the
+    same network in PyTorch ops (cuDNN convolutions, channels-last, fp16,
+    one CUDA graph) on feature planes computed beforehand by nsm_features --
+    i.e. the U-Net alone, without the feature pass our fused path includes.
+    Not the product and not a bar."""
+    import torch
+    import torch.nn.functional as F
+    from paper_2301_05262_b200.raster import assemble_features_batch
+    if args.features != 4 or args.dtype != "fp16":
+        return None
+    torch.backends.cudnn.benchmark = True
+    h, wd = frames[0].camera.resolution
+    hp = (h + 15) // 16 * 16
+    feats, _, _ = assemble_features_batch(inputs, [(f.camera, f.view, f.scene.emitter_center, f.size_index,
+                                                    f.bias) for f in frames])
+    x = torch.zeros((len(frames), 4, hp, wd), dtype=torch.float16, device=dev)
+    x[:, :, :h] = feats.half()
+    x = x.contiguous(memory_format=torch.channels_last)
+    W = {k: torch.from_numpy(np.asarray(v.data)).to(dev).half() for k, v in w.items()}
+    W = {k: (v.contiguous(memory_format=torch.channels_last) if v.dim() == 4 else v) for k, v in W.items()}
+
+    def conv(t, n, relu=True):
+        wt = W[n + ".w"]
+        y = F.conv2d(t, wt, W[n + ".b"], padding=wt.shape[-1] // 2)
+        return F.relu(y) if relu else y
+
+    def net(t):
+        t = F.pixel_unshuffle(t, 2)
+        skips = []
+        for j in range(3):
+            t = conv(conv(t, f"l{j}.enc3"), f"l{j}.enc1")
+            skips.append(t)
+            t = F.avg_pool2d(t, 2)
+        t = conv(conv(t, "l3.enc3"), "l3.enc1")
+        for j in (2, 1, 0):
+            t = F.interpolate(t, scale_factor=2, mode="bilinear", align_corners=False)
+            if j > 0:
+                t = t + skips[j]
+            t = conv(conv(t, f"l{j}.dec3"), f"l{j}.dec1")
+        y = conv(t, "head", relu=False)
+        base = F.interpolate(y[:, :1], scale_factor=2, mode="bilinear", align_corners=False)
+        det = y.clone()
+        det[:, 0] = 0
+        return torch.sigmoid(base + F.pixel_shuffle(det, 2))
+
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        for _ in range(3):
+            net(x)
+    torch.cuda.current_stream().wait_stream(s)
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        out = net(x)
+    for _ in range(3):
+        g.replay()
+    ms, _ = time_steps(g.replay, args.steps, world, soak=False, local=local)
+    ms_max = float(gather_floats([ms], world, dev)[:, 0].max())
+    return {"value": round(job_n / (ms_max / 1e3), 3), "unit": UNIT, "ms_per_step": round(ms_max, 5),
+            "what": "PyTorch/cuDNN fp16 U-Net only (features precomputed, CUDA graph, channels-last)",
+            "output_shape": list(out.shape)}
 
 
 def run_e2e(args, run, inputs, frames, job_n, world):
