@@ -30,9 +30,9 @@ for ln in dis.splitlines():
         continue
     if not inside:
         continue
-    m = re.search(r'line (\d+)', ln)
+    m = re.search(r'File "([^"]+)", line (\d+)', ln)
     if "//##" in ln and m:
-        cur = int(m.group(1))
+        cur = f"{m.group(1).split('/')[-1]}:{m.group(2)}"
         continue
     m = re.match(r'\s*/\*([0-9a-f]+)\*/', ln)
     if m and cur is not None:
@@ -46,4 +46,4 @@ for r, a in zip(R, addrs):
 tot_i, tot_s = sum(ins.values()), sum(smp.values())
 print(f"warp instructions {tot_i}, samples {tot_s}")
 for l, v in sorted(smp.items(), key=lambda kv: -kv[1])[:top]:
-    print(f"line {l:5d}: samples {100 * v / tot_s:5.1f}%  instr {100 * ins[l] / tot_i:5.1f}%")
+    print(f"{str(l):28s} samples {100 * v / tot_s:5.1f}%  instr {100 * ins[l] / tot_i:5.1f}%")
