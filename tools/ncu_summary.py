@@ -53,8 +53,8 @@ def launches(path):
         unit = d.get("Metric Unit", "")
         us = v / 1000.0 if unit in ("nsecond", "ns") else (v * 1000.0 if unit in ("msecond", "ms") else v)
         k = short(d["Kernel Name"])
-        if "gbuffer_kernel" in k or "shadowmap_kernel" in k:
-            continue                      # input producers: untimed setup
+        if "gbuffer_kernel" in k or "shadowmap_kernel" in k or "spin_kernel" in k:
+            continue                      # input producers (untimed setup); bench's profiling spin
         agg[k][0] += 1
         agg[k][1] += us
     tot = sum(v[1] for v in agg.values())
