@@ -54,3 +54,39 @@ def test_generic16_infer_layers4_vs_oracle(cfg1):
     d = y.astype(np.float64) - ref
     print(f"layers=4 infer fp16: max {np.abs(d).max():.3g} mse {np.mean(d * d):.3g}")
     assert np.abs(d).max() <= 1e-2 and np.mean(d * d) <= 1e-4
+
+
+@pytest.mark.parametrize("dtype", ["fp16", "bf16"])
+def test_generic16_batch_independent(dtype):
+    """A batch through the generic path equals its frames one by one
+    (bitwise), for a layers=6 plan (not covered by the fused kernels)."""
+    import torch
+    from paper_2301_05262_b200 import network
+    cfg = network.NetworkConfig(layers=6, base_channels=8)
+    w = network.init_weights(cfg, np.random.default_rng(np.random.SeedSequence([9, 0x11])))
+    plan = network.Plan(w, cfg, dtype)
+    g = torch.Generator().manual_seed(1)
+    x = (torch.rand((3, 4, 64, 96), generator=g) * 2).cuda()
+    yb = plan.forward(x).cpu().numpy()
+    for i in range(3):
+        np.testing.assert_array_equal(plan.forward(x[i:i + 1]).cpu().numpy()[0], yb[i])
+
+
+def test_five_plane_window_two_chunks():
+    """More frames than one chunk (8) through the 5-plane fused path: the
+    per-chunk feat5 / enc0_s2d launches and the frame offsets of every
+    output, against single-frame runs (bitwise)."""
+    import torch
+    from paper_2301_05262_b200 import network, producer, scenes
+    from paper_2301_05262_b200.infer import ShadowInference
+    cfg = network.NetworkConfig(in_channels=5)
+    w = network.init_weights(cfg, np.random.default_rng(np.random.SeedSequence([0, 0x11])))
+    plan = network.Plan(w, cfg, "fp16")
+    frames = [scenes.make_frame(scenes.random_scene(8, seed=s, emitter_radius_m=0.1 + 0.02 * s), (64, 96),
+                                (256, 256)) for s in range(10)]
+    inp = producer.render_inputs(frames)
+    yb = ShadowInference(plan, frames, out_dtype="fp16")(inp).cpu().clone()
+    for i in (0, 7, 8, 9):
+        one = {k: v[i:i + 1].contiguous() for k, v in inp.items()}
+        y1 = ShadowInference(plan, [frames[i]], out_dtype="fp16")(one).cpu()
+        torch.testing.assert_close(y1[0], yb[i], rtol=0, atol=0)
