@@ -3,7 +3,7 @@
 BUILD EXTENSION -- PARITY UNPINNED. The reference has no blocker search
 (PCSS is out of scope); BASELINE configs 3/4 ask for a
 "blocker-search penumbra estimate" plane feeding the same U-Net. This is the
-definition the CUDA kernel (csrc/blocker.cu) implements, restated here in
+definition the CUDA kernels (csrc/features.cu blocker_kernel, csrc/feat5.cu) implement, restated here in
 numpy, built from reference pieces:
 
 1. nearest texel (ri, ci) exactly as ``_shadow_lookup`` (raster.py:247-250)

@@ -13,64 +13,86 @@ namespace nsm {
 
 namespace {
 
-constexpr int kTile = 16;   // output pixels per CTA edge
-constexpr int kCo = 8;      // output channels per CTA
-constexpr int kCi = 8;      // input channels staged per step
+constexpr int kTX = 32, kTY = 16;   // output pixels per CTA (x, y): 2 per thread, x and x + 16
+constexpr int kThr = 256;
+constexpr int kCo = 16;             // output channels per CTA
+constexpr int kCi = 8;              // input channels staged per step
 
 // autodiff.conv2d (autodiff.py:146-166): zero-padded cross-correlation,
 // k in {1, 3}, stride 1, + bias, optional ReLU (autodiff.py:190-191).
+// Register-blocked: each thread accumulates 2 pixels x 16 output channels;
+// per (input channel, tap) it reads 2 staged inputs and the 16 weights as 4
+// broadcast 16-B loads, i.e. 32 FMAs per 6 shared loads.
 template <int K>
-__global__ void __launch_bounds__(kTile * kTile) conv_f32_kernel(
+__global__ void __launch_bounds__(kThr) conv_f32_kernel(
     const float* __restrict__ x, int cin, int h, int w, const float* __restrict__ wt,
     const float* __restrict__ bias, int cout, int relu, float* __restrict__ y,
     int64_t x_nstride, int64_t y_nstride) {
     constexpr int P = (K - 1) / 2;
-    constexpr int T = kTile + 2 * P;
-    __shared__ float sx[kCi][T][T + 1];
-    __shared__ float sw[kCo][kCi][K * K];
-    const int tx = threadIdx.x % kTile, ty = threadIdx.x / kTile;
-    const int ox = blockIdx.x * kTile + tx, oy = blockIdx.y * kTile + ty;
+    constexpr int TY = kTY + 2 * P, TX = kTX + 2 * P;
+    __shared__ float sx[kCi][TY][TX + 1];
+    __shared__ __align__(16) float sw[kCi][K * K][kCo];
+    const int tx = threadIdx.x % 16, ty = threadIdx.x / 16;
+    const int ox = blockIdx.x * kTX + tx, oy = blockIdx.y * kTY + ty;
     const int ngrp = (cout + kCo - 1) / kCo;
     const int n = blockIdx.z / ngrp, co0 = (blockIdx.z % ngrp) * kCo;
     const float* xn = x + n * x_nstride;
-    float acc[kCo];
+    float acc[2][kCo];
 #pragma unroll
-    for (int o = 0; o < kCo; ++o) acc[o] = 0.f;
+    for (int o = 0; o < kCo; ++o) acc[0][o] = acc[1][o] = 0.f;
     for (int ci0 = 0; ci0 < cin; ci0 += kCi) {
         __syncthreads();
-        for (int i = threadIdx.x; i < kCi * T * T; i += kTile * kTile) {
-            const int c = i / (T * T), r = (i / T) % T, q = i % T;
-            const int gy = blockIdx.y * kTile + r - P, gx = blockIdx.x * kTile + q - P;
+        for (int i = threadIdx.x; i < kCi * TY * TX; i += kThr) {
+            const int c = i / (TY * TX), r = (i / TX) % TY, q = i % TX;
+            const int gy = blockIdx.y * kTY + r - P, gx = blockIdx.x * kTX + q - P;
             float v = 0.f;
             if (ci0 + c < cin && gy >= 0 && gy < h && gx >= 0 && gx < w)
                 v = xn[(int64_t)(ci0 + c) * h * w + (int64_t)gy * w + gx];
             sx[c][r][q] = v;
         }
-        for (int i = threadIdx.x; i < kCo * kCi * K * K; i += kTile * kTile) {
-            const int o = i / (kCi * K * K), c = (i / (K * K)) % kCi, t = i % (K * K);
+        for (int i = threadIdx.x; i < kCi * K * K * kCo; i += kThr) {
+            const int o = i % kCo, t = (i / kCo) % (K * K), c = i / (kCo * K * K);
             float v = 0.f;
             if (co0 + o < cout && ci0 + c < cin)
                 v = wt[((int64_t)(co0 + o) * cin + ci0 + c) * K * K + t];
-            sw[o][c][t] = v;
+            sw[c][t][o] = v;
         }
         __syncthreads();
-        for (int c = 0; c < kCi; ++c) {
+        const int cn = min(kCi, cin - ci0);
+        for (int c = 0; c < cn; ++c) {
 #pragma unroll
             for (int t = 0; t < K * K; ++t) {
-                const float v = sx[c][ty + t / K][tx + t % K];
+                const float v0 = sx[c][ty + t / K][tx + t % K];
+                const float v1 = sx[c][ty + t / K][tx + 16 + t % K];
+                const float4* wq = reinterpret_cast<const float4*>(sw[c][t]);
 #pragma unroll
-                for (int o = 0; o < kCo; ++o) acc[o] = fmaf(sw[o][c][t], v, acc[o]);
+                for (int q = 0; q < kCo / 4; ++q) {
+                    const float4 ww = wq[q];
+                    acc[0][4 * q + 0] = fmaf(ww.x, v0, acc[0][4 * q + 0]);
+                    acc[0][4 * q + 1] = fmaf(ww.y, v0, acc[0][4 * q + 1]);
+                    acc[0][4 * q + 2] = fmaf(ww.z, v0, acc[0][4 * q + 2]);
+                    acc[0][4 * q + 3] = fmaf(ww.w, v0, acc[0][4 * q + 3]);
+                    acc[1][4 * q + 0] = fmaf(ww.x, v1, acc[1][4 * q + 0]);
+                    acc[1][4 * q + 1] = fmaf(ww.y, v1, acc[1][4 * q + 1]);
+                    acc[1][4 * q + 2] = fmaf(ww.z, v1, acc[1][4 * q + 2]);
+                    acc[1][4 * q + 3] = fmaf(ww.w, v1, acc[1][4 * q + 3]);
+                }
             }
         }
     }
-    if (ox >= w || oy >= h) return;
+    if (oy >= h) return;
     float* yn = y + n * y_nstride;
 #pragma unroll
-    for (int o = 0; o < kCo; ++o) {
-        if (co0 + o >= cout) break;
-        float v = acc[o] + bias[co0 + o];
-        if (relu) v = fmaxf(v, 0.f);
-        yn[(int64_t)(co0 + o) * h * w + (int64_t)oy * w + ox] = v;
+    for (int hx = 0; hx < 2; ++hx) {
+        const int px = ox + 16 * hx;
+        if (px >= w) continue;
+#pragma unroll
+        for (int o = 0; o < kCo; ++o) {
+            if (co0 + o >= cout) break;
+            float v = acc[hx][o] + bias[co0 + o];
+            if (relu) v = fmaxf(v, 0.f);
+            yn[(int64_t)(co0 + o) * h * w + (int64_t)oy * w + px] = v;
+        }
     }
 }
 
@@ -179,17 +201,17 @@ int grid_for(int64_t total) {
 
 void conv_f32(const float* x, int n, int cin, int h, int w, const ConvW& c, int relu, float* y,
               cudaStream_t st) {
-    dim3 grd((w + kTile - 1) / kTile, (h + kTile - 1) / kTile, n * ((c.cout + kCo - 1) / kCo));
+    dim3 grd((w + kTX - 1) / kTX, (h + kTY - 1) / kTY, n * ((c.cout + kCo - 1) / kCo));
     const int64_t xs = (int64_t)cin * h * w, ys = (int64_t)c.cout * h * w;
     if (c.k == 3)
         {
             NSM_PROF("conv_f32_kernel", st);
-            conv_f32_kernel<3><<<grd, kTile * kTile, 0, st>>>(x, cin, h, w, c.w32, c.b32, c.cout, relu, y, xs, ys);
+            conv_f32_kernel<3><<<grd, kThr, 0, st>>>(x, cin, h, w, c.w32, c.b32, c.cout, relu, y, xs, ys);
         }
     else
         {
             NSM_PROF("conv_f32_kernel", st);
-            conv_f32_kernel<1><<<grd, kTile * kTile, 0, st>>>(x, cin, h, w, c.w32, c.b32, c.cout, relu, y, xs, ys);
+            conv_f32_kernel<1><<<grd, kThr, 0, st>>>(x, cin, h, w, c.w32, c.b32, c.cout, relu, y, xs, ys);
         }
 }
 
