@@ -148,17 +148,25 @@ def env_guard():
         sys.exit(f"bench.py: refusing to run with {bad} set (experiment switches; unset them)")
 
 
+def spawn_command(args, argv, port):
+    """The torchrun command line that runs this script on ``args.gpus`` ranks."""
+    return [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+            "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + list(argv)
+
+
 def maybe_spawn(args):
     """--gpus N without a torchrun environment: re-exec under torchrun."""
     if args.gpus <= 1 or "WORLD_SIZE" in os.environ:
         return
     import socket
+    import torch
+    have = torch.cuda.device_count()
+    if have < args.gpus:
+        sys.exit(f"bench.py: --gpus {args.gpus} but only {have} CUDA device(s) are visible")
     with socket.socket() as s:
         s.bind(("127.0.0.1", 0))
         port = s.getsockname()[1]
-    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
-           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
-    sys.exit(subprocess.call(cmd))
+    sys.exit(subprocess.call(spawn_command(args, sys.argv[1:], port)))
 
 
 # --------------------------------------------------------------------------

@@ -131,3 +131,16 @@ def test_reference_leg_never_loads_the_cuda_library():
     r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=300)
     assert r.returncode == 0, r.stderr
     assert r.stdout.strip() in ("reference", "port")
+
+
+def test_spawn_command_and_device_check(monkeypatch):
+    """--gpus N re-executes bench.py under torchrun (127.0.0.1 rendezvous,
+    one process per GPU) and refuses more ranks than visible devices."""
+    args = bench.parse(["--gpus", "4", "--config", "5"])
+    cmd = bench.spawn_command(args, ["--gpus", "4", "--config", "5"], 29511)
+    assert cmd[1:4] == ["-m", "torch.distributed.run", "--nnodes=1"]
+    assert "--nproc-per-node=4" in cmd and "--master-addr=127.0.0.1" in cmd and "--master-port=29511" in cmd
+    assert cmd[-3:] == ["--gpus", "4", "--config", "5"][-3:] and cmd[-5].endswith("bench.py")
+    monkeypatch.delenv("WORLD_SIZE", raising=False)
+    with pytest.raises(SystemExit, match="CUDA device"):
+        bench.maybe_spawn(args)          # no GPU in the build container
