@@ -110,16 +110,15 @@ __device__ __forceinline__ void build_blocks(const Region& g, int tid) {
     const int BW = g.RW - 3, BH = g.RH - 3;
     for (int r = tid >> 5; r < BH; r += F5_THREADS / 32)
         for (int c = tid & 31; c < BW; c += 32) {
-            int mn = kInfBits, mx = 0;
+            int mn[4], mx[4];
 #pragma unroll
             for (int dy = 0; dy < 4; ++dy) {
                 const int* row = g.tex + (r + dy) * g.RW + c;
-                mn = __vimin3_s32(row[0], row[1], mn);
-                mn = __vimin3_s32(row[2], row[3], mn);
-                mx = __vimax3_s32(row[0], row[1], mx);
-                mx = __vimax3_s32(row[2], row[3], mx);
+                mn[dy] = min(__vimin3_s32(row[0], row[1], row[2]), row[3]);
+                mx[dy] = max(__vimax3_s32(row[0], row[1], row[2]), row[3]);
             }
-            g.blk[r * BW + c] = make_int2(mn, mx);
+            g.blk[r * BW + c] = make_int2(min(__vimin3_s32(mn[0], mn[1], mn[2]), mn[3]),
+                                          max(__vimax3_s32(mx[0], mx[1], mx[2]), mx[3]));
         }
 }
 
@@ -330,6 +329,7 @@ __global__ void __launch_bounds__(F5_THREADS, 3) feat5_kernel(const __grid_const
     }
     __syncthreads();   // block maps built
     // phase 3, per pixel: combine the window summary with its own threshold
+    const bool vec4 = (F.ws & 3) == 0 && (reinterpret_cast<uintptr_t>(smf) & 15) == 0;
     const float re = (float)(F.size_index * (0.5 / 2.0 / 4.0));       // scene.emitter_radius
     const float focal = (float)((F.ch / 2.0) / F.half_h);              // CameraPose.focal_px
 #pragma unroll
@@ -352,13 +352,19 @@ __global__ void __launch_bounds__(F5_THREADS, 3) feat5_kernel(const __grid_const
                 const int2* blk = k1 ? RB.blk : RA.blk;
                 const int* reg = k1 ? RB.tex : RA.tex;
                 unsigned strad = 0;
+                int zq[4] = {kInfBits, kInfBits, kInfBits, kInfBits};
+                unsigned ub[4] = {um, um, um, um};
 #pragma unroll
                 for (int b = 0; b < 16; ++b) {
                     const int2 mm = blk[(r0 + 4 * (b >> 2)) * BW + c0 + 4 * (b & 3)];
-                    zmin = min(zmin, mm.x);
-                    if (mm.y < thr) um = min(um, thr1 - (unsigned)mm.y);
+                    zq[b & 3] = min(zq[b & 3], mm.x);
+                    if (mm.y < thr) ub[b & 3] = min(ub[b & 3], thr1 - (unsigned)mm.y);
                     else if (mm.x < thr) strad |= 1u << b;
                 }
+                zmin = min(min(zq[0], zq[1]), min(zq[2], zq[3]));
+                um = min(min(ub[0], ub[1]), min(ub[2], ub[3]));
+                // one accumulator per block row: four independent DPX chains
+                unsigned uq[4] = {um, 0xffffffffu, 0xffffffffu, 0xffffffffu};
                 while (strad) {
                     const int b = __ffs(strad) - 1;
                     strad &= strad - 1;
@@ -367,12 +373,55 @@ __global__ void __launch_bounds__(F5_THREADS, 3) feat5_kernel(const __grid_const
                     for (int dy = 0; dy < 4; ++dy)
 #pragma unroll
                         for (int dxx = 0; dxx < 4; ++dxx)
-                            um = __viaddmin_u32(thr1, (unsigned)(-p[dy * W_ + dxx]), um);
+                            uq[dy] = __viaddmin_u32(thr1, (unsigned)(-p[dy * W_ + dxx]), uq[dy]);
                 }
+                um = min(min(uq[0], uq[1]), min(uq[2], uq[3]));
+            } else if (vec4 && tr >= F5_R && tr + F5_R <= F.hs && tc >= F5_R && tc + F5_R <= F.ws) {
+                // 16 texel rows from global memory (L1 / L2) as the aligned
+                // 16-B blocks covering each window row (4 or 5 per row; map
+                // rows are a multiple of 4 texels, so no block crosses a row),
+                // the compiler keeps two rows in flight; texels outside the
+                // window are masked to +inf (neutral for both scans)
+                const int cs = tc - F5_R, m = cs & 3;
+                const float4* rowp = reinterpret_cast<const float4*>(smf + (int64_t)(tr - F5_R) * F.ws + (cs - m));
+                const int rq = F.ws >> 2;
+                int zq[4] = {kInfBits, kInfBits, kInfBits, kInfBits};
+                unsigned uq[4] = {um, um, um, um};
+#pragma unroll 2
+                for (int r = 0; r < 2 * F5_R; ++r, rowp += rq) {
+                    float4 v[5];
+#pragma unroll
+                    for (int b = 0; b < 4; ++b) v[b] = __ldg(rowp + b);
+                    v[4] = m ? __ldg(rowp + 4) : make_float4(INFINITY, INFINITY, INFINITY, INFINITY);
+                    int t[20];
+#pragma unroll
+                    for (int b = 0; b < 5; ++b) {
+                        t[4 * b] = __float_as_int(v[b].x);
+                        t[4 * b + 1] = __float_as_int(v[b].y);
+                        t[4 * b + 2] = __float_as_int(v[b].z);
+                        t[4 * b + 3] = __float_as_int(v[b].w);
+                    }
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) {
+                        if (j < m) t[j] = kInfBits;             // left of the window
+                        if (j >= m) t[16 + j] = kInfBits;       // right of it
+                    }
+#pragma unroll
+                    for (int c = 0; c < 20; c += 2) {
+                        const int q = (c >> 1) & 3;
+                        zq[q] = __vimin3_s32(t[c], t[c + 1], zq[q]);
+                        uq[q] = __viaddmin_u32(thr1, (unsigned)(-t[c]), uq[q]);
+                        uq[q] = __viaddmin_u32(thr1, (unsigned)(-t[c + 1]), uq[q]);
+                    }
+                }
+                zmin = min(min(zq[0], zq[1]), min(zq[2], zq[3]));
+                um = min(min(uq[0], uq[1]), min(uq[2], uq[3]));
             } else if (tr >= F5_R && tr + F5_R <= F.hs && tc >= F5_R && tc + F5_R <= F.ws) {
                 // 16 texel rows from global memory (L1 / L2), two rows (32
                 // loads) in flight per round trip
                 const float* rowp = smf + (int64_t)(tr - F5_R) * F.ws + (tc - F5_R);
+                int zq[4] = {kInfBits, kInfBits, kInfBits, kInfBits};
+                unsigned uq[4] = {um, um, um, um};
                 for (int r = 0; r < 2 * F5_R; r += 2, rowp += 2 * F.ws) {
                     int t[32];
 #pragma unroll
@@ -382,11 +431,13 @@ __global__ void __launch_bounds__(F5_THREADS, 3) feat5_kernel(const __grid_const
                     }
 #pragma unroll
                     for (int c = 0; c < 32; c += 2) {
-                        zmin = __vimin3_s32(t[c], t[c + 1], zmin);
-                        um = __viaddmin_u32(thr1, (unsigned)(-t[c]), um);
-                        um = __viaddmin_u32(thr1, (unsigned)(-t[c + 1]), um);
+                        zq[(c >> 1) & 3] = __vimin3_s32(t[c], t[c + 1], zq[(c >> 1) & 3]);
+                        uq[(c >> 1) & 3] = __viaddmin_u32(thr1, (unsigned)(-t[c]), uq[(c >> 1) & 3]);
+                        uq[(c >> 1) & 3] = __viaddmin_u32(thr1, (unsigned)(-t[c + 1]), uq[(c >> 1) & 3]);
                     }
                 }
+                zmin = min(min(zq[0], zq[1]), min(zq[2], zq[3]));
+                um = min(min(uq[0], uq[1]), min(uq[2], uq[3]));
             } else {
                 // window clipped by the map border (rare): bounds-checked scan
                 for (int r = tr - F5_R; r < tr + F5_R; ++r) {
