@@ -58,6 +58,12 @@ struct Feat5Args {
     int32_t* dbg;      // debugging (nullable): (N, h, w, 4) zmin, zmax, thr, path bits
 };
 
+__device__ __forceinline__ float rcp_approx(float x) {
+    float r;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
+}
+
 // analysis.penumbra_extents (analysis.py:240-269) -> screen width
 // (x_a + x_b) * focal_px / d (analysis.py:319-320), fp32 (the plane is
 // rounded to 16 bits right after); 0 where the model's preconditions fail.
@@ -65,20 +71,21 @@ struct Feat5Args {
 // theta_d = asin(s), s = r_s / hyp, so tan(theta -/+ theta_d) follow from
 // the tangent addition formula with tan(theta_d) = s / sqrt(1 - s^2) -- no
 // transcendental calls -- and theta + theta_d < pi / 2 is 1 - T tan(theta_d) > 0.
-__device__ __forceinline__ float penumbra_width_f(float zmin, float zmax, float zf, float re, float focal,
-                                                  float d) {
+__device__ __forceinline__ float penumbra_width_f(float zmin, float zmax, float zf, float izf, float re,
+                                                  float focal, float d) {
     const float zm = 0.5f * (zmax + zmin), rs = 0.5f * (zmax - zmin);
-    const float hyp = sqrtf(zm * zm + re * re);
-    if (!(zmin > 0.f && zmax >= zmin && zf > zmax && zm > 0.f && rs <= hyp && re > 0.f)) return 0.f;
-    const float sn = rs / hyp;
-    const float u = sn / sqrtf(fmaxf(1.f - sn * sn, 0.f));     // tan(theta_d); inf at s = 1
-    const float bq = re * (zf - zm) / zm;
-    const float T = (bq + re) / zf;                            // tan(theta)
+    const float hyp2 = zm * zm + re * re;
+    if (!(zmin > 0.f && zmax >= zmin && zf > zmax && zm > 0.f && rs * rs <= hyp2 && re > 0.f)) return 0.f;
+    // MUFU reciprocals / square roots (the plane is rounded to 16 bits)
+    const float sn = fminf(rs * rsqrtf(hyp2), 1.f);
+    const float u = sn * rsqrtf(fmaxf(1.f - sn * sn, 0.f));    // tan(theta_d); inf at s = 1
+    const float bq = re * (zf - zm) * rcp_approx(zm);
+    const float T = (bq + re) * izf;                           // tan(theta)
     const float den_p = 1.f - T * u;                           // cos(theta + theta_d) sign
     if (!(den_p > 0.f)) return 0.f;
-    const float ta = (T - u) / (1.f + T * u), tb = (T + u) / den_p;
+    const float ta = __fdividef(T - u, 1.f + T * u), tb = __fdividef(T + u, den_p);
     const float xa = zf * ta - re, xb = zf * tb - re;
-    return (xa + xb) * focal / d;
+    return __fdividef((xa + xb) * focal, d);
 }
 
 // A staged map region: rows R0 .. R0+RH-1, cols C0 .. C0+RW-1 as depth
@@ -89,6 +96,29 @@ struct Region {
     int* tex;
     int2* blk;
 };
+
+// 16-B chunk variant: C0 and RW are multiples of 4, map rows a multiple of 4
+// texels (a chunk is wholly on or off the map); asynchronous copies, waited
+// for before the barrier that ends staging.
+__device__ __forceinline__ void stage_region16(const Region& g, const float* smf, const FrameK& F, int tid) {
+    if (!g.on) return;
+    const int RQ = g.RW >> 2;
+    for (int rr = tid >> 5; rr < g.RH; rr += F5_THREADS / 32) {
+        const int r = g.R0 + rr;
+        const bool rin = r >= 0 && r < F.hs;
+        const float* src = smf + (int64_t)r * F.ws;
+        int* dst = g.tex + rr * g.RW;
+        for (int q = tid & 31; q < RQ; q += 32) {
+            const int c = g.C0 + 4 * q;
+            if (rin && c >= 0 && c < F.ws) {
+                const unsigned d = (unsigned)__cvta_generic_to_shared(dst + 4 * q);
+                asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d), "l"(src + c) : "memory");
+            } else {
+                *reinterpret_cast<int4*>(dst + 4 * q) = make_int4(kInfBits, kInfBits, kInfBits, kInfBits);
+            }
+        }
+    }
+}
 
 __device__ __forceinline__ void stage_region(const Region& g, const float* smf, const FrameK& F, int tid) {
     if (!g.on) return;
@@ -260,24 +290,34 @@ __global__ void __launch_bounds__(F5_THREADS, 3) feat5_kernel(const __grid_const
     const float* smf = a.sm + (int64_t)f * a.sm_stride;
     int* regs = smem5;                                           // depth bits
     int2* blks = reinterpret_cast<int2*>(smem5 + F5_MAX_TEX);     // sliding 4x4 (min, max)
+    // 16-B staging when map rows are 16-B aligned: region columns widened
+    // to whole chunks
+    const bool vec4 = (F.ws & 3) == 0 && (reinterpret_cast<uintptr_t>(smf) & 15) == 0;
+    const int cmask = vec4 ? ~3 : ~0;
     Region RA, RB;
     RA.R0 = bb[0][0] - F5_R;
-    RA.C0 = bb[0][2] - F5_R;
+    RA.C0 = (bb[0][2] - F5_R) & cmask;
     RA.RH = bb[0][1] - bb[0][0] + 2 * F5_R;
-    RA.RW = bb[0][3] - bb[0][2] + 2 * F5_R;
+    RA.RW = ((bb[0][3] + F5_R - RA.C0) + ~cmask) & cmask;
     RA.on = nreg >= 1 && bb[0][0] <= bb[0][1] && RA.RH * RA.RW <= F5_MAX_TEX;
     RA.tex = regs;
     RA.blk = blks;
     const int usedA = RA.on ? RA.RH * RA.RW : 0, busedA = RA.on ? (RA.RH - 3) * (RA.RW - 3) : 0;
     RB.R0 = bb[1][0] - F5_R;
-    RB.C0 = bb[1][2] - F5_R;
+    RB.C0 = (bb[1][2] - F5_R) & cmask;
     RB.RH = bb[1][1] - bb[1][0] + 2 * F5_R;
-    RB.RW = bb[1][3] - bb[1][2] + 2 * F5_R;
+    RB.RW = ((bb[1][3] + F5_R - RB.C0) + ~cmask) & cmask;
     RB.on = nreg == 2 && bb[1][0] <= bb[1][1] && usedA + RB.RH * RB.RW <= F5_MAX_TEX;
     RB.tex = regs + usedA;
     RB.blk = blks + busedA;
-    stage_region(RA, smf, F, tid);
-    stage_region(RB, smf, F, tid);
+    if (vec4) {
+        stage_region16(RA, smf, F, tid);
+        stage_region16(RB, smf, F, tid);
+        asm volatile("cp.async.wait_all;" ::: "memory");
+    } else {
+        stage_region(RA, smf, F, tid);
+        stage_region(RB, smf, F, tid);
+    }
     __syncthreads();
     build_blocks(RA, tid);
     build_blocks(RB, tid);
@@ -303,7 +343,7 @@ __global__ void __launch_bounds__(F5_THREADS, 3) feat5_kernel(const __grid_const
         const float zf = (float)zf64;
         zfv[e] = zf;
         thrv[e] = __float_as_int(__double2float_ru(zf64 - bias));   // t < thr64 <=> t < thr (fp32 t)
-        const float izf = 1.f / zf;
+        const float izf = rcp_approx(zf);
         const float ftx = (float)tx, fty = (float)ty, ftz = (float)tz;
         const float ce = __saturatef((nxv[e] * ftx + nyv[e] * fty + nzv[e] * ftz) * izf);
         const float dx = F.fcp[0] - pxv[e], dy = F.fcp[1] - pyv[e], dz = F.fcp[2] - pzv[e];
@@ -325,11 +365,10 @@ __global__ void __launch_bounds__(F5_THREADS, 3) feat5_kernel(const __grid_const
         feat[e][0] = ch0;
         feat[e][1] = ch1;
         feat[e][2] = ce + F.fsize;
-        feat[e][3] = cc / dv[e];
+        feat[e][3] = cc * rcp_approx(dv[e]);
     }
     __syncthreads();   // block maps built
     // phase 3, per pixel: combine the window summary with its own threshold
-    const bool vec4 = (F.ws & 3) == 0 && (reinterpret_cast<uintptr_t>(smf) & 15) == 0;
     const float re = (float)(F.size_index * (0.5 / 2.0 / 4.0));       // scene.emitter_radius
     const float focal = (float)((F.ch / 2.0) / F.half_h);              // CameraPose.focal_px
 #pragma unroll
@@ -461,7 +500,8 @@ __global__ void __launch_bounds__(F5_THREADS, 3) feat5_kernel(const __grid_const
             d4[3] = (key[e] < 0 ? 1 : 0) | (cl[e] << 3);
         }
         if (zmin < thr)                                            // blockers exist
-            feat[e][4] = penumbra_width_f(__int_as_float(zmin), __int_as_float(zmx), zfv[e], re, focal, dv[e]);
+            feat[e][4] = penumbra_width_f(__int_as_float(zmin), __int_as_float(zmx), zfv[e], rcp_approx(zfv[e]), re, focal,
+                                           dv[e]);
     }
 
     if constexpr (kF32) {
