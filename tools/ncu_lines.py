@@ -10,8 +10,9 @@ import sys
 
 rep, kre, cubin, fname = sys.argv[1:5]
 top = int(sys.argv[5]) if len(sys.argv) > 5 else 30
-out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass", "-k", "regex:" + kre,
-                      "--launch-count", "1"], capture_output=True, text=True).stdout
+# kernel_regex is matched against the mangled name (template arguments select one instantiation)
+out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass", "--kernel-name-base",
+                      "mangled", "-k", "regex:" + kre, "--launch-count", "1"], capture_output=True, text=True).stdout
 lines = [ln for ln in out.splitlines() if not ln.startswith('"Kernel Name"')]
 rows = list(csv.reader(io.StringIO("\n".join(lines))))
 hdr = rows[0]
