@@ -41,8 +41,10 @@ namespace {
 
 constexpr int F5_TY = 8, F5_TX = 32, F5_THREADS = F5_TY * F5_TX;
 constexpr int F5_R = 8;                      // window rows ri-8 .. ri+7 (16 x 16)
-constexpr int F5_MAX_TEX = 6144;             // staged texels per CTA (both regions)
-constexpr int F5_SMEM = 3 * F5_MAX_TEX * 4;   // texels + sliding 4x4 blocks (int2): 72 KB, 3 CTAs per SM
+constexpr int F5_MAX_TEX = 3584;             // staged texels per CTA (both regions)
+constexpr int F5_SMEM = 3 * F5_MAX_TEX * 4;   // texels + sliding 4x4 blocks (int2): 42 KB; 3 CTAs per SM (registers)
+// leave ~125 KB of L1 for the global-memory window scans (measured: 6144 texels
+// per CTA, 72 KB, 481 us; 3584: 458 us; 3072: 463 us; 2048: 482 us)
 constexpr int kInfBits = 0x7f800000;
 
 struct Feat5Args {
