@@ -182,7 +182,9 @@ def dist_setup(backend=None):
         backend = "nccl"
     if backend == "nccl":
         torch.cuda.set_device(local)
-    if world > 1:
+    # a process group whenever torchrun launched us (also at world size 1, so
+    # the NCCL timing / --gather path runs on a one-GPU box too)
+    if world > 1 or "TORCHELASTIC_RUN_ID" in os.environ:
         import torch.distributed as dist
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
         kw = {"device_id": torch.device("cuda", local)} if backend == "nccl" else {}
@@ -190,8 +192,13 @@ def dist_setup(backend=None):
     return rank, world, local
 
 
+def dist_on():
+    import torch.distributed as dist
+    return dist.is_available() and dist.is_initialized()
+
+
 def barrier(world):
-    if world > 1:
+    if dist_on():
         import torch.distributed as dist
         dist.barrier()
 
@@ -200,7 +207,7 @@ def gather_floats(vals, world, device):
     """All-gather a small float vector from every rank -> (world, len)."""
     import torch
     t = torch.tensor([float(v) for v in vals], dtype=torch.float64, device=device)
-    if world == 1:
+    if not dist_on():
         return t[None].cpu().numpy()
     import torch.distributed as dist
     out = [torch.empty_like(t) for _ in range(world)]
@@ -386,7 +393,7 @@ def run_ours(args):
         sys.exit("bench.py: libnsm.so is an experiment build (NSM_EXPERIMENTS); rebuild the release library")
     rank, world, local = dist_setup()
     dev = torch.device("cuda", local)
-    if world > 1 and rank == 0:
+    if dist_on() and rank == 0:
         nv = torch.cuda.nccl.version()
         print(f"bench.py: NCCL {'.'.join(map(str, nv)) if isinstance(nv, tuple) else nv} communicator, "
               f"{world} ranks, one GPU each", file=sys.stderr)
@@ -418,7 +425,7 @@ def run_ours(args):
     value = job_n / (ms_max / 1e3)
 
     gathered = None
-    if args.gather and world > 1:
+    if args.gather and dist_on():
         from paper_2301_05262_b200 import shard
         import torch.distributed as dist
         full = shard.gather_frames(run.y, job_n if scaling == "strong" else n * world)
@@ -551,7 +558,7 @@ def run_ours(args):
             "clocks": clocks,
         }
         print(json.dumps(line))
-    if world > 1:
+    if dist_on():
         import torch.distributed as dist
         dist.destroy_process_group()
 

@@ -70,7 +70,7 @@ def gather_frames(local, n_frames: int, device=None):
     batch in frame order (shards may differ in size by one frame)."""
     import torch
     import torch.distributed as dist
-    if not dist.is_initialized() or dist.get_world_size() == 1:
+    if not dist.is_initialized():
         return local
     world, rank = dist.get_world_size(), dist.get_rank()
     sizes = [shard_bounds(n_frames, r, world) for r in range(world)]
