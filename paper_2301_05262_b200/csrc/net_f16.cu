@@ -1430,9 +1430,10 @@ __global__ void __launch_bounds__(lv_threads<SRC, NB, NPW>(), 1) level_kernel(co
     uint64_t* a1_full = bar + 16;
     uint64_t* a1_empty = bar + 18;
     uint64_t* wbar = bar + 20;        // weights landed
-    uint64_t* skf = bar + 21;         // SRC_UP: skip tile landed in in[s] [NIN <= 2]
-    uint64_t* lof = bar + 23;         // SRC_UP: low-res tile landed, double-buffered [2]
-    uint64_t* lo_empty = bar + 25;    // SRC_UP: producers done with low-res buffer [2]
+    uint64_t* skf = bar + 21;         // SRC_UP: skip tile landed in in[s] [NIN <= 3]
+    uint64_t* lof = bar + 24;         // SRC_UP: low-res tile landed, double-buffered [2]
+    uint64_t* lo_empty = bar + 26;    // SRC_UP: producers done with low-res buffer [2]
+    static_assert(SRC != SRC_UP || G::STAGED || NIN <= 3, "skip barrier slots");
     uint32_t* tptr = reinterpret_cast<uint32_t*>(smem + G::OFF_BAR + 224);
     float* sb3 = reinterpret_cast<float*>(smem + G::OFF_B);
     float* sb1 = sb3 + C3;
@@ -1473,8 +1474,8 @@ __global__ void __launch_bounds__(lv_threads<SRC, NB, NPW>(), 1) level_kernel(co
             mbar_init(&a1_empty[i], NE * 32);
         }
         mbar_init(wbar, 1);
+        for (int i = 0; i < 3; ++i) mbar_init(&skf[i], 1);
         for (int i = 0; i < 2; ++i) {
-            mbar_init(&skf[i], 1);
             mbar_init(&lof[i], 1);
             mbar_init(&lo_empty[i], NPW);
         }
