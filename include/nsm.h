@@ -147,7 +147,8 @@ nsm_status nsm_features(const nsm_gbuffer* g, const float* sm, int64_t sm_stride
  * (2*radius)^2 texel window, blockers = finite depths < z_f - bias,
  * (z_min, z_max) -> analysis.penumbra_extents (analysis.py:240-269) with
  * r_e = size_index * 0.0625 m, width (x_a + x_b) * focal_px / d
- * (analysis.py:319-320).  out: (n, h, w) fp32, the 5th input plane of a
+ * (analysis.py:319-320) in units of the focal length: (x_a + x_b) / d
+ * (resolution independent).  out: (n, h, w) fp32, the 5th input plane of a
  * NetworkConfig(in_channels=5) net.  first_bad as nsm_features. */
 nsm_status nsm_blocker_plane(const nsm_gbuffer* g, const float* sm, int64_t sm_stride,
                              const nsm_frame* frames, int32_t n, int32_t h, int32_t w,

@@ -14,8 +14,14 @@ numpy, built from reference pieces:
 4. (z_min, z_max) over blockers -> ``analysis.penumbra_extents`` with the
    emitter radius r_e (analysis.py:240-269; its ValueError cases give 0 here,
    pre-masked as penumbra_histogram does, analysis.py:313)
-5. screen width (x_a + x_b) * focal_px / d (analysis.py:319-320); 0 where
-   there are no blockers, uncovered pixels, or a point light.
+5. screen width (x_a + x_b) * focal_px / d (analysis.py:319-320), divided by
+   focal_px: the plane is the penumbra's screen width in units of the focal
+   length, (x_a + x_b) / d -- resolution independent and O(0.1).  In pixels
+   (up to ~130 at 1080p, size_index ~7) the plane drove the first layers'
+   activations of a random-init in_channels=5 net to ~100, where fp16's
+   absolute rounding (ulp 0.06) put the 16-bit visibility 0.10 max-abs off
+   the fp32 oracle (north_star's bar: 1e-2); 0 where there are no blockers,
+   uncovered pixels, or a point light.
 """
 
 from __future__ import annotations
@@ -47,7 +53,7 @@ def penumbra_widths(z_min, z_max, z_f, r_e, focal_px, d):
 
 
 def blocker_plane(d, position, z_f, coverage, sm_depth, view, bias, size_index, focal_px, radius=8):
-    """(H, W) fp32 penumbra-width plane."""
+    """(H, W) fp32 penumbra-width plane (screen width / focal_px)."""
     hs, ws = view.resolution
     ri, ci, _ = texel_indices(view, position, coverage)
     sm = np.asarray(sm_depth, dtype=np.float64)
@@ -68,4 +74,4 @@ def blocker_plane(d, position, z_f, coverage, sm_depth, view, bias, size_index, 
         w = penumbra_widths(np.where(have, zmin, 1.0), np.where(have, zmax, 1.0),
                             np.asarray(z_f, dtype=np.float64), r_e, focal_px,
                             np.where(coverage, np.asarray(d, dtype=np.float64), 1.0))
-    return np.where(have, w, 0.0).astype(np.float32)
+    return np.where(have, w / float(focal_px), 0.0).astype(np.float32)

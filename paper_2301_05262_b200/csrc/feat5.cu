@@ -67,14 +67,15 @@ __device__ __forceinline__ float rcp_approx(float x) {
 }
 
 // analysis.penumbra_extents (analysis.py:240-269) -> screen width
-// (x_a + x_b) * focal_px / d (analysis.py:319-320), fp32 (the plane is
-// rounded to 16 bits right after); 0 where the model's preconditions fail.
+// (x_a + x_b) * focal_px / d (analysis.py:319-320) in units of the focal
+// length, (x_a + x_b) / d, fp32 (the plane is rounded to 16 bits right
+// after); 0 where the model's preconditions fail.
 // The reference's angles are theta = atan(T), T = (bq + r_e) / z_f, and
 // theta_d = asin(s), s = r_s / hyp, so tan(theta -/+ theta_d) follow from
 // the tangent addition formula with tan(theta_d) = s / sqrt(1 - s^2) -- no
 // transcendental calls -- and theta + theta_d < pi / 2 is 1 - T tan(theta_d) > 0.
 __device__ __forceinline__ float penumbra_width_f(float zmin, float zmax, float zf, float izf, float re,
-                                                  float focal, float d) {
+                                                  float d) {
     const float zm = 0.5f * (zmax + zmin), rs = 0.5f * (zmax - zmin);
     const float hyp2 = zm * zm + re * re;
     if (!(zmin > 0.f && zmax >= zmin && zf > zmax && zm > 0.f && rs * rs <= hyp2 && re > 0.f)) return 0.f;
@@ -87,7 +88,7 @@ __device__ __forceinline__ float penumbra_width_f(float zmin, float zmax, float 
     if (!(den_p > 0.f)) return 0.f;
     const float ta = __fdividef(T - u, 1.f + T * u), tb = __fdividef(T + u, den_p);
     const float xa = zf * ta - re, xb = zf * tb - re;
-    return __fdividef((xa + xb) * focal, d);
+    return __fdividef(xa + xb, d);
 }
 
 // A staged map region: rows R0 .. R0+RH-1, cols C0 .. C0+RW-1 as depth
@@ -372,7 +373,6 @@ __global__ void __launch_bounds__(F5_THREADS, 3) feat5_kernel(const __grid_const
     __syncthreads();   // block maps built
     // phase 3, per pixel: combine the window summary with its own threshold
     const float re = (float)(F.size_index * (0.5 / 2.0 / 4.0));       // scene.emitter_radius
-    const float focal = (float)((F.ch / 2.0) / F.half_h);              // CameraPose.focal_px
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
         if (key[e] == -2) continue;
@@ -502,7 +502,7 @@ __global__ void __launch_bounds__(F5_THREADS, 3) feat5_kernel(const __grid_const
             d4[3] = (key[e] < 0 ? 1 : 0) | (cl[e] << 3);
         }
         if (zmin < thr)                                            // blockers exist
-            feat[e][4] = penumbra_width_f(__int_as_float(zmin), __int_as_float(zmx), zfv[e], rcp_approx(zfv[e]), re, focal,
+            feat[e][4] = penumbra_width_f(__int_as_float(zmin), __int_as_float(zmx), zfv[e], rcp_approx(zfv[e]), re,
                                            dv[e]);
     }
 

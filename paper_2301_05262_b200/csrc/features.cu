@@ -172,10 +172,12 @@ nsm_status launch_features(const nsm_gbuffer* g, const float* sm, int64_t sm_str
 // blockers = finite depths < z_f - b, (z_min, z_max) -> the bounding-sphere
 // penumbra model of analysis.penumbra_extents (analysis.py:240-269) with the
 // emitter radius, and the screen-space width (x_a + x_b) * focal_px / d
-// (analysis.py:319-320).  0 where uncovered / no blockers / invalid geometry.
+// (analysis.py:319-320) in units of the focal length, i.e. (x_a + x_b) / d
+// (resolution independent, O(0.1): see oracle/blocker.py for why not pixels).
+// 0 where uncovered / no blockers / invalid geometry.
 namespace nsm {
 
-__device__ double penumbra_width(double zmin, double zmax, double zf, double re, double focal, double d) {
+__device__ double penumbra_width(double zmin, double zmax, double zf, double re, double d) {
     const double zm = (zmax + zmin) / 2.0, rs = (zmax - zmin) / 2.0;
     const double hyp = sqrt(zm * zm + re * re);
     if (!(zmin > 0.0 && zmax >= zmin && zf > zmax && zm > 0.0 && rs <= hyp && re > 0.0)) return 0.0;
@@ -184,7 +186,7 @@ __device__ double penumbra_width(double zmin, double zmax, double zf, double re,
     const double th = atan((bq + re) / zf);
     if (!(th + td < 1.5707963267948966)) return 0.0;
     const double xa = zf * tan(th - td) - re, xb = zf * tan(th + td) - re;
-    return (xa + xb) * focal / d;
+    return (xa + xb) / d;
 }
 
 template <typename T>
@@ -228,8 +230,7 @@ __global__ void __launch_bounds__(256) blocker_kernel(GBufK g, const float* __re
     double wv = 0.0;
     if (zmin <= zmax) {
         const double re = f.size_index * (0.5 / 2.0 / 4.0);          // scene.emitter_radius
-        const double focal = (f.ch / 2.0) / f.half_h;                  // CameraPose.focal_px
-        wv = penumbra_width(zmin, zmax, zf, re, focal, d);
+        wv = penumbra_width(zmin, zmax, zf, re, d);
     }
     *o = (float)wv;
 }

@@ -170,7 +170,8 @@ def assemble_features_batch(inputs, frames, want_idx=False, check=True):
 def blocker_penumbra_batch(inputs, frames, radius: int = 8, check=True):
     """Blocker-search penumbra-width plane (N, H, W) fp32 -- the 5th input
     plane of BASELINE configs 3/4 (a build extension: the reference has no
-    blocker search; see include/nsm.h nsm_blocker_plane and oracle/blocker.py).
+    blocker search; see include/nsm.h nsm_blocker_plane and oracle/blocker.py):
+    the penumbra's screen width in units of the focal length, (x_a + x_b) / d.
     ``frames`` as for :func:`assemble_features_batch`; size_index sets the
     emitter radius (0.0625 m per unit, scene.py:54-58)."""
     import torch
