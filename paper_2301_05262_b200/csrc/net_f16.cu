@@ -208,7 +208,16 @@ struct Enc0Args {
     int32_t* tidx;        // parity hook (nullable): (N, 2, h, w) texel (row, col) of covered pixels
     int dbg;              // experiments only: 1 skip feature math, 2 skip convolutions
     TileDiv td;           // tile decode constants (host-computed, read from the param bank)
+    long long* trace;     // experiments only (NSM_ENC0_TRACE): per-CTA globaltimer start / end
+    int* tile_ctr;        // TMA kernel: [0] tiles claimed beyond the first round, [1] CTAs done
+                          // claiming (zeroed by fill_first_bad; the last CTA re-zeroes both)
 };
+
+__device__ __forceinline__ long long globaltimer_ns() {
+    long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
 
 // Stage-1 per-pixel math of the fused kernel: fp64 projection for the texel
 // index (bit-exact np.rint), fp32 for the rest (the values are rounded to
@@ -513,6 +522,11 @@ __device__ __forceinline__ void produce_features(const Enc0Args& a, uint8_t* buf
 //   empty[s]    producers -> TMA       (19 arrivals: stage s read by phase A)
 //   half[b][h]  producers -> consumers (19: rows of half h of tile buffer b)
 //   freed[b]    consumers -> producers (4: tile buffer b consumed)
+// The TMA thread also picks the tiles: blockIdx.x first, then one global
+// counter (tiles differ in cost with their coverage, and static round-robin
+// left the slowest CTA 14 % above the mean); the k-th tile's index goes into
+// a shared ring (tring[k & 7], -1 = none) that the producers read after
+// full[] and the consumers after half[].
 // setmaxnreg moves registers from the producer/TMA warps (-> 72) to the MMA
 // warps (-> 112); the budget is checked against the kernel's launch
 // register count on the host (run_l0).
@@ -554,17 +568,41 @@ __device__ __forceinline__ void produce_features_tma(const Enc0Args& a, const Gb
     uint64_t* empty = full + 2;
     uint64_t* half = full + 4;     // [buffer][half]
     uint64_t* freed = full + 8;
+    int* tring = reinterpret_cast<int*>(full + 10);   // tile of the CTA's k-th tile (k & 7), -1: none
     const int ptid = threadIdx.x;
     const int lane = ptid & 31;
-    const int mytiles = (int)blockIdx.x < total ? (total - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x : 0;
-    const int nh = 2 * mytiles;
     if (ptid >= kE0Feat) {                         // TMA warp
         if (lane == 0) {
             const uint64_t pol = l2_evict_first_policy();      // the G-buffer is read once
-            for (int q = 0; q < nh; ++q) {
+            // The CTA's tiles: the first is blockIdx.x, the rest come from
+            // one counter, claimed when the tile is due (claiming earlier
+            // balances worse: measured), so CTAs whose tiles turn out cheap
+            // (uncovered) take more of them
+            int cur = -1;
+            for (int q = 0;; ++q) {
                 const int sidx = q & 1;
                 if (q >= 2) mbar_wait(&empty[sidx], ((q - 2) >> 1) & 1);
-                const L0Tile tl = l0_tile(blockIdx.x + (q >> 1) * gridDim.x, a.td);
+                if (!(q & 1)) {
+                    const int k = q >> 1;
+                    if (k == 0) {
+                        cur = blockIdx.x;                        // grid <= total
+                    } else {
+                        if (k == 1) pdl_wait();                  // the counter was zeroed by fill_first_bad
+                        cur = (int)gridDim.x + atomicAdd(a.tile_ctr, 1);
+                        if (cur >= total) cur = -1;
+                    }
+                    tring[k & 7] = cur;
+                    if (cur < 0) {
+                        mbar_arrive(&full[sidx]);                // no data: the producers read the sentinel
+                        // the last CTA done claiming re-zeroes the counters for the next launch
+                        if (atomicAdd(a.tile_ctr + 1, 1) == (int)gridDim.x - 1) {
+                            a.tile_ctr[0] = 0;
+                            a.tile_ctr[1] = 0;
+                        }
+                        break;
+                    }
+                }
+                const L0Tile tl = l0_tile(cur, a.td);
                 const uint32_t dst = smem_u32(stage + sidx * ST_BYTES);
                 const int x = 2 * tl.tx0 - 4, y = 2 * tl.ty0 - 2 + ST_ROWS * (q & 1);
                 mbar_expect_tx(&full[sidx], ST_TX);
@@ -586,6 +624,7 @@ __device__ __forceinline__ void produce_features_tma(const Enc0Args& a, const Gb
     const int lds_lo = qy * ST_TCOLS * 4 + 8 + 8 * px_lo, lds_hi = qy * ST_TCOLS * 4 + 8 + 8 * px_hi;
     const int sts_row = (qy & 1) * E0_PLANE + (qy >> 1) * E0_IC * 16;
     const int slot_lo = sts_row + px_lo * 16, slot_hi = sts_row + px_hi * 16;
+    auto tile_q = [&](int q) { return l0_tile(tring[(q >> 1) & 7], a.td); };
     auto park = [&](int q, const QuadPark& P) {
         if (!active) return;
         uint8_t* tdst = smem + ((q >> 1) & 1) * E0_SMEM + (q & 1) * (ST_ROWS / 2) * E0_IC * 16;
@@ -594,7 +633,7 @@ __device__ __forceinline__ void produce_features_tma(const Enc0Args& a, const Gb
             *reinterpret_cast<uint2*>(tdst + (e < 2 ? slot_lo : slot_hi) + (e & 1) * 8) = P.v[e];
     };
     auto phaseA = [&](int q, QuadRegs& R, QuadPark& P) {
-        const L0Tile tl = l0_tile(blockIdx.x + (q >> 1) * gridDim.x, a.td);
+        const L0Tile tl = tile_q(q);
         const int sidx = q & 1;
         if (!active) return;
         const FrameK& F = a.tab.f[tl.f];
@@ -668,7 +707,7 @@ __device__ __forceinline__ void produce_features_tma(const Enc0Args& a, const Gb
     };
     auto phaseB = [&](int q, const QuadRegs& R) {
         if (!active) return;
-        const L0Tile tl = l0_tile(blockIdx.x + (q >> 1) * gridDim.x, a.td);
+        const L0Tile tl = tile_q(q);
         const float bias = a.tab.f[tl.f].fbias;
         uint8_t* dst = smem + ((q >> 1) & 1) * E0_SMEM + (q & 1) * (ST_ROWS / 2) * E0_IC * 16;
 #pragma unroll
@@ -684,10 +723,11 @@ __device__ __forceinline__ void produce_features_tma(const Enc0Args& a, const Gb
             *slot = Elem<T>::pack(ch0, ch1);
         }
     };
-    auto step = [&](int q, QuadRegs& RA, QuadRegs& RB) {
+    // live: half q belongs to a claimed tile (the TMA thread's sentinel, -1,
+    // ends the loop after the last half's phase B)
+    auto step = [&](int q, bool live, QuadRegs& RA, QuadRegs& RB) {
         QuadPark P;
-        if (q < nh) {
-            mbar_wait(&full[q & 1], (q >> 1) & 1);
+        if (live) {
             if (!(kExp && (a.dbg & 1))) phaseA(q, RA, P);
             else for (int e = 0; e < 4; ++e) RA.look[e] = -1.f, P.v[e] = make_uint2(0u, 0u);
             __syncwarp();
@@ -700,7 +740,12 @@ __device__ __forceinline__ void produce_features_tma(const Enc0Args& a, const Gb
             __syncwarp();
             if (lane == 0) mbar_arrive(&half[(k & 1) * 2 + (qb & 1)]);   // rows of half qb&1 done
         }
-        if (q < nh && !(q & 1)) {
+        if (!live) {
+            // no tile k: wake the consumers, which read the sentinel
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&half[((q >> 1) & 1) * 2]);
+        }
+        if (live && !(q & 1)) {
             // a tile's first half: wait for the consumers to release the
             // buffer (after finishing the previous tile above), then park
             const int k = q >> 1;
@@ -710,8 +755,11 @@ __device__ __forceinline__ void produce_features_tma(const Enc0Args& a, const Gb
     };
     QuadRegs RA, RB;
 #pragma unroll 1
-    for (int q = 0; q <= nh; ++q) {
-        step(q, RA, RB);
+    for (int q = 0;; ++q) {
+        mbar_wait(&full[q & 1], (q >> 1) & 1);             // data (or the sentinel) for half q
+        const bool live = tring[(q >> 1) & 7] >= 0;
+        step(q, live, RA, RB);
+        if (!live) break;
         const QuadRegs t = RA;
         RA = RB;
         RB = t;
@@ -727,6 +775,12 @@ __global__ void __launch_bounds__(kSrc == 2 ? kE0Threads : kL0Threads, 1) enc0_k
     constexpr int kProd = kSrc == 2 ? kE0Prod : kL0Prod;
     constexpr int kThreads = kSrc == 2 ? kE0Threads : kL0Threads;
     if (threadIdx.x == 0) pdl_trigger();
+    if (kExp && a.trace && threadIdx.x == 0 && blockIdx.x < 512) {
+        a.trace[2 * blockIdx.x] = globaltimer_ns();
+        uint32_t smid;
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+        a.trace[1024 + blockIdx.x] = smid;
+    }
     if constexpr (kSrc == 2) {
         extern __shared__ __align__(128) uint8_t smem[];
         uint64_t* bars = reinterpret_cast<uint64_t*>(smem + 2 * E0_SMEM + 2 * ST_BYTES);
@@ -838,18 +892,20 @@ __global__ void __launch_bounds__(kSrc == 2 ? kE0Threads : kL0Threads, 1) enc0_k
         uint64_t* freed = bars + 8;
         // the producers signal each half of a tile (level-0 rows 0-8 and
         // 9-17), so the convolution starts one half-tile earlier
+        const int* tring = reinterpret_cast<const int*>(bars + 10);
         for (int k = 0;; ++k) {
-            const int tile = blockIdx.x + k * gridDim.x;
-            if (tile >= total) break;
             const int s = k & 1;
             const uint32_t par = (k >> 1) & 1;
             mbar_wait(&half[s * 2], par);
+            const int tile = tring[k & 7];
+            if (tile < 0) break;
             consume(smem + s * E0_SMEM, tile, [&](int ir) {
                 if (ir == E0_IR / 2) mbar_wait(&half[s * 2 + 1], par);
             });
             __syncwarp();
             if (lane == 0) mbar_arrive(&freed[s]);
         }
+        if (kExp && a.trace && threadIdx.x == kProd && blockIdx.x < 512) a.trace[2 * blockIdx.x + 1] = globaltimer_ns();
     } else {
         l0_consume_loop<kThreads>(total, [&](uint8_t* buf, int tile) { consume(buf, tile, NoRowHook{}); });
     }
@@ -2352,7 +2408,7 @@ __global__ void __launch_bounds__(128) dec0_ring_kernel(const T* __restrict__ d1
 
 // first_bad[i] = INT64_MAX ("no frustum error"), PDL-chained so that enc0's
 // prologue overlaps it
-__global__ void fill_first_bad(int64_t* p, int n) {
+__global__ void fill_first_bad(int64_t* p, int n, int* tile_ctr) {
     // trigger only after the grid dependency resolved: enc0's TMA warp
     // streams the G-buffer before its own griddepcontrol.wait, so whatever
     // wrote the G-buffer must be complete and visible once this kernel
@@ -2361,6 +2417,7 @@ __global__ void fill_first_bad(int64_t* p, int n) {
     pdl_trigger();
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i < n) p[i] = INT64_MAX;
+    if (tile_ctr && i < 2) tile_ctr[i] = 0;     // enc0's dynamic tile counters (first launch)
 }
 
 // ------------------------------------------------------------------ host side
@@ -2513,6 +2570,7 @@ struct Bufs {
     void *p1, *s1, *p2, *s2, *p3, *b3, *d2, *d1;
     __half* y;
     void* x5;        // 5-plane nets: the chunk-planar s2d input (nf, 3, H0, W0, 8)
+    int* ctr;        // enc0's dynamic tile counters (2 ints)
     size_t bytes;
 };
 
@@ -2535,6 +2593,7 @@ Bufs carve(void* ws, int nf, int H0, int W0, int es, bool x5 = false) {
     b.d1 = take((size_t)nf * (H1 + 2) * (W1 + 2) * 16 * es);   // replicate-padded, chunk-planar (DST_PADREP)
     b.y = (__half*)take((size_t)nf * H0 * W0 * 8);
     b.x5 = x5 ? take((size_t)nf * 3 * H0 * W0 * 8 * es) : nullptr;
+    b.ctr = (int*)take(2 * sizeof(int));
     b.bytes = (size_t)(p - (char*)ws);
     return b;
 }
@@ -2839,7 +2898,7 @@ nsm_status infer_f16(const Plan& p, const nsm_gbuffer* g, const float* sm, int64
     if (ws_bytes < b.bytes) return fail(NSM_ERR_ARG, "workspace too small (%zu < %zu)", ws_bytes, b.bytes);
     {
         NSM_PROF("fill_i64", st);
-        launch_pdl(fill_first_bad, dim3((n + 127) / 128), dim3(128), 0, st, first_bad, n);
+        launch_pdl(fill_first_bad, dim3((n + 127) / 128), dim3(128), 0, st, first_bad, n, b.ctr);
     }
     for (int f0 = 0; f0 < n; f0 += chunk_frames()) {
         const int nf = std::min(chunk_frames(), n - f0);
@@ -2861,9 +2920,19 @@ nsm_status infer_f16(const Plan& p, const nsm_gbuffer* g, const float* sm, int64
         e.b3 = p.lev[0].enc3.b32;
         e.b1 = p.lev[0].enc1.b32;
         e.out = b.p1;
+        e.tile_ctr = b.ctr;
         e.first_bad = first_bad + f0;
         e.tidx = texel_idx ? texel_idx + (int64_t)f0 * 2 * h * w : nullptr;
         e.dbg = env_int("NSM_ENC0_DBG", 0);
+        e.trace = nullptr;
+#ifdef NSM_EXPERIMENTS
+        static long long* e0_trace = nullptr;
+        if (getenv("NSM_ENC0_TRACE")) {
+            if (!e0_trace) cudaMalloc(&e0_trace, 2048 * sizeof(long long));
+            cudaMemsetAsync(e0_trace, 0, 2048 * sizeof(long long), st);
+            e.trace = e0_trace;
+        }
+#endif
         void* yo = (char*)y + (size_t)f0 * h * w * (y_dtype == NSM_F16 ? 2 : 4);
         GbufMaps tm;
         memset(&tm, 0, sizeof tm);
@@ -2885,6 +2954,32 @@ nsm_status infer_f16(const Plan& p, const nsm_gbuffer* g, const float* sm, int64
                            ? run_l0<__nv_bfloat16>(p, b, e, tm, nf, H0, W0, h, w, yo, y_dtype == NSM_F16, st, src)
                            : run_l0<__half>(p, b, e, tm, nf, H0, W0, h, w, yo, y_dtype == NSM_F16, st, src);
         if (s != NSM_OK) return s;
+#ifdef NSM_EXPERIMENTS
+        if (e.trace) {   // experiments only: per-CTA spans of enc0 (globaltimer), stalls the stream
+            static long long hb[2048];
+            cudaMemcpyAsync(hb, e.trace, sizeof hb, cudaMemcpyDeviceToHost, st);
+            cudaStreamSynchronize(st);
+            long long s0 = 0, e1 = 0;
+            int nc = 0;
+            double dsum = 0, dmax = 0, dmin = 1e30;
+            for (int c = 0; c < 512; ++c) {
+                const long long a0 = hb[2 * c], a1 = hb[2 * c + 1];
+                if (!a0 || !a1) continue;
+                ++nc;
+                if (!s0 || a0 < s0) s0 = a0;
+                if (a1 > e1) e1 = a1;
+                const double d = (a1 - a0) / 1e3;
+                dsum += d, dmax = std::max(dmax, d), dmin = std::min(dmin, d);
+            }
+            fprintf(stderr, "enc0 CTAs %d: first start -> last end %.2f us; CTA span min/avg/max %.2f/%.2f/%.2f us\n", nc,
+                    (e1 - s0) / 1e3, dmin, dsum / std::max(nc, 1), dmax);
+            if (getenv("NSM_ENC0_TRACE_ALL")) {
+                fprintf(stderr, "enc0 per-CTA span (us):");
+                for (int c = 0; c < nc; ++c) fprintf(stderr, " %.1f/%lld", (hb[2 * c + 1] - hb[2 * c]) / 1e3, hb[1024 + c]);
+                fprintf(stderr, "\n");
+            }
+        }
+#endif
     }
     NSM_CUDA_TRY(cudaGetLastError());
     return NSM_OK;
