@@ -1515,6 +1515,7 @@ __global__ void __launch_bounds__(lv_threads<SRC, NB, NPW>(), 1) level_kernel(co
     };
 
     if (tid == 0) pdl_trigger();
+    if (kExp && a.trace && tid == 0 && blockIdx.x < 256) a.trace[256 + 2 * blockIdx.x] = globaltimer_ns();
     if (warp == EW0) tmem_alloc<G::TCOLS>(tptr);
     if (tid == 0) {
         for (int i = 0; i < NIN; ++i) {
@@ -2002,6 +2003,7 @@ __global__ void __launch_bounds__(lv_threads<SRC, NB, NPW>(), 1) level_kernel(co
     tc_fence_before();
     __syncthreads();
     if (warp == EW0) tmem_dealloc<G::TCOLS>(tmem);
+    if (kExp && a.trace && tid == 0 && blockIdx.x < 256) a.trace[257 + 2 * blockIdx.x] = globaltimer_ns();
 }
 
 // ------------------------------------------------------------- level 0 decoder, polyphase (tcgen05)
@@ -2542,17 +2544,33 @@ nsm_status launch_level(const LevelArgs& a, int nf, cudaStream_t st, const char*
     static const char* trace_name = getenv("NSM_LEVEL_TRACE");
     trace = trace_name && !strcmp(trace_name, name);
     if (trace) {
-        if (!trace_buf) cudaMalloc(&trace_buf, 32 * 8 * sizeof(long long));
-        cudaMemsetAsync(trace_buf, 0, 32 * 8 * sizeof(long long), st);
+        if (!trace_buf) cudaMalloc(&trace_buf, 1024 * sizeof(long long));
+        cudaMemsetAsync(trace_buf, 0, 1024 * sizeof(long long), st);
     }
 #endif
     const_cast<LevelArgs&>(a).trace = trace ? trace_buf : nullptr;
     NSM_PROF(name, st);
     launch_pdl(k, dim3(grid), dim3(lv_threads<SRC, NB, NPW>()), G::SMEM, st, a, tin, tlo, total);
     if (trace) {   // experiments only: print CTA 0's timeline (us at 1.965 GHz) and stall the stream
-        long long h[32 * 8];
+        static long long h[1024];
         cudaMemcpyAsync(h, trace_buf, sizeof h, cudaMemcpyDeviceToHost, st);
         cudaStreamSynchronize(st);
+        {
+            long long s0 = 0, e1 = 0;
+            double dsum = 0, dmin = 1e30, dmax = 0;
+            int nc = 0;
+            for (int c = 0; c < 256; ++c) {
+                const long long a0 = h[256 + 2 * c], a1 = h[257 + 2 * c];
+                if (!a0 || !a1) continue;
+                ++nc;
+                if (!s0 || a0 < s0) s0 = a0;
+                if (a1 > e1) e1 = a1;
+                const double d = (a1 - a0) / 1e3;
+                dsum += d, dmin = std::min(dmin, d), dmax = std::max(dmax, d);
+            }
+            fprintf(stderr, "%s CTAs %d: first start -> last end %.2f us; CTA span min/avg/max %.2f/%.2f/%.2f us\n", name,
+                    nc, (e1 - s0) / 1e3, dmin, dsum / std::max(nc, 1), dmax);
+        }
         long long t0 = 0;
         for (long long v : h) if (v && (!t0 || v < t0)) t0 = v;
         fprintf(stderr, "%s CTA0 (us): tile prod_start prod_done mma3_issue mma1_issued epi1_start epi1_end epi2_start epi2_end\n", name);
