@@ -135,3 +135,35 @@ def test_per_batch_frames_and_input_validation():
     big = [scenes.make_frame(scenes.random_scene(8, seed=1), (96, 160), (512, 512))]
     with pytest.raises(ValueError):
         run.launch(ia, frames=big)
+
+
+def test_multichunk_launch_equals_single_frames():
+    """11 frames in one launch (two enc0 chunks, 8 + 3, each with its own
+    dynamically scheduled tiles and the shared tile counter re-zeroed
+    between them) give every frame bit-for-bit what a one-frame launch gives,
+    twice in a row; the texel indices of the fused pass match too."""
+    import torch
+    from paper_2301_05262_b200 import network, producer, scenes
+    from paper_2301_05262_b200.infer import ShadowInference
+    cfg, w = _weights()
+    plan = network.Plan(w, cfg, "fp16")
+    frames = [scenes.make_frame(scenes.random_scene(6 + i % 4, seed=40 + i, emitter_radius_m=0.05 * (i % 5)),
+                                (96, 160), (256, 256), camera_pos=(0.3 * (i % 3), 3.0, -5.5 - 0.1 * i))
+              for i in range(11)]
+    inp = producer.render_inputs(frames)
+    run = ShadowInference(plan, frames, out_dtype="fp16")
+    idx = torch.full((11, 2, 96, 160), -1, dtype=torch.int32, device="cuda")
+    run.launch(inp, texel_idx=idx)
+    run.check_frustum()
+    y1 = run.y.clone()
+    run.launch(inp)
+    run.check_frustum()
+    torch.testing.assert_close(run.y, y1, rtol=0, atol=0)
+    for i in (0, 5, 8, 10):
+        one = {k: v[i:i + 1].contiguous() for k, v in inp.items()}
+        r1 = ShadowInference(plan, [frames[i]], out_dtype="fp16")
+        i1 = torch.full((1, 2, 96, 160), -1, dtype=torch.int32, device="cuda")
+        r1.launch(one, texel_idx=i1)
+        r1.check_frustum()
+        torch.testing.assert_close(r1.y[0], y1[i], rtol=0, atol=0)
+        torch.testing.assert_close(i1[0], idx[i], rtol=0, atol=0)
