@@ -112,6 +112,33 @@ def test_fused_frustum_error_first_pixel(cfg1, dtype):
         run(_inputs(r))
 
 
+@pytest.mark.parametrize("dtype", ["fp16", "bf16"])
+def test_fused5_frustum_error_first_pixel(cfg1, dtype):
+    """The 5-plane fused pass (feat5 inside nsm_infer) and nsm_features5 also
+    name the reference's first out-of-frustum pixel (raster.py:251-255)."""
+    from types import SimpleNamespace
+    from oracle import features as of
+    from paper_2301_05262_b200 import network
+    from paper_2301_05262_b200._lib import FrustumError
+    from paper_2301_05262_b200.infer import ShadowInference
+    from paper_2301_05262_b200.raster import assemble_features5_batch
+    r = cfg1
+    v = golden_view(r)
+    narrow = SimpleNamespace(**{**v.__dict__, "tan_half": v.tan_half / 20})
+    cov = r["d"] > 0
+    _, _, first = of.texel_indices(narrow, r["position"], cov)
+    y, x = divmod(first, cov.shape[1])
+    cfg = network.NetworkConfig(in_channels=5)
+    w = network.init_weights(cfg, np.random.default_rng(np.random.SeedSequence([0, 0x11])))
+    fr = _frame_ns(r, narrow)
+    run = ShadowInference(network.Plan(w, cfg, dtype), [fr])
+    with pytest.raises(FrustumError, match=rf"covered pixel \({y}, {x}\) projects outside"):
+        run(_inputs(r))
+    with pytest.raises(FrustumError, match=rf"covered pixel \({y}, {x}\) projects outside"):
+        assemble_features5_batch(_inputs(r), [(fr.camera, fr.view, fr.scene.emitter_center, fr.size_index,
+                                                fr.bias)])
+
+
 def test_per_batch_frames_and_input_validation():
     """A launch may carry its own frames (ADVICE: per-batch poses); results
     equal an executor built for those frames; bad inputs raise ValueError."""
