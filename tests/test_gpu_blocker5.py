@@ -186,3 +186,31 @@ def test_fp32_plan_five_planes_infer_unsupported():
     run = ShadowInference(network.Plan(w, cfg, "fp32"), [fr])
     with pytest.raises(NotImplementedError):
         run(producer.render_inputs([fr]))
+
+
+def test_host_pipeline_five_planes():
+    """HostPipeline (pinned host buffers, overlapped copies) on a 5-plane
+    plan returns bitwise the device-resident executor's visibility, batch
+    by batch, each batch with its own scenes."""
+    import torch
+    from paper_2301_05262_b200 import network, producer, scenes
+    from paper_2301_05262_b200.infer import HostPipeline, ShadowInference
+    cfg, w = _weights5(seed=2)
+    plan = network.Plan(w, cfg, "fp16")
+    batches, refs, poses = [], [], []
+    for b in range(3):
+        frames = [scenes.make_frame(scenes.random_scene(8, seed=70 + 10 * b + s, emitter_radius_m=0.1 + 0.1 * b),
+                                    (96, 160), (256, 256), camera_pos=(0.2 * b, 3.0, -6.0 + 0.2 * s))
+                  for s in range(2)]
+        inp = producer.render_inputs(frames)
+        refs.append(ShadowInference(plan, frames, out_dtype="fp16")(inp).cpu().clone())
+        batches.append({k: v.cpu().pin_memory() for k, v in inp.items()})
+        poses.append(frames)
+    run = ShadowInference(plan, poses[0], out_dtype="fp16")
+    pipe = HostPipeline(run)
+    outs = [torch.empty(run.y.shape, dtype=run.y.dtype, pin_memory=True) for _ in batches]
+    for hb, ho, fr in zip(batches, outs, poses):
+        pipe.submit(hb, ho, frames=fr)
+    pipe.synchronize()
+    for ho, ref in zip(outs, refs):
+        torch.testing.assert_close(ho, ref, rtol=0, atol=0)
