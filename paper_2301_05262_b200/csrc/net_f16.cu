@@ -107,7 +107,7 @@ constexpr int round128(int v) { return (v + 127) / 128 * 128; }
 constexpr int ST_OFF_N = round128(ST_PLANE);              // TMA destinations 128-B aligned
 constexpr int ST_OFF_P = ST_OFF_N + round128(3 * ST_PLANE);
 constexpr int ST_BYTES = round128(ST_OFF_P + 3 * ST_PLANE);
-constexpr int ENC0_SMEM_TMA = 2 * E0_SMEM + 2 * ST_BYTES + 128;
+constexpr int ENC0_SMEM_TMA = 2 * E0_SMEM + 2 * ST_BYTES + 256;   // + 10 mbarriers, tile ring, bias ring
 static_assert(E0_SMEM % 128 == 0, "stage base alignment");
 
 struct GbufMaps {
@@ -569,6 +569,7 @@ __device__ __forceinline__ void produce_features_tma(const Enc0Args& a, const Gb
     uint64_t* half = full + 4;     // [buffer][half]
     uint64_t* freed = full + 8;
     int* tring = reinterpret_cast<int*>(full + 10);   // tile of the CTA's k-th tile (k & 7), -1: none
+    float* tbias = reinterpret_cast<float*>(full + 14);   // and its frame's shadow bias (phase B)
     const int ptid = threadIdx.x;
     const int lane = ptid & 31;
     if (ptid >= kE0Feat) {                         // TMA warp
@@ -592,6 +593,7 @@ __device__ __forceinline__ void produce_features_tma(const Enc0Args& a, const Gb
                         if (cur >= total) cur = -1;
                     }
                     tring[k & 7] = cur;
+                    if (cur >= 0) tbias[k & 7] = a.tab.f[l0_tile(cur, a.td).f].fbias;
                     if (cur < 0) {
                         mbar_arrive(&full[sidx]);                // no data: the producers read the sentinel
                         // the last CTA done claiming re-zeroes the counters for the next launch
@@ -624,7 +626,6 @@ __device__ __forceinline__ void produce_features_tma(const Enc0Args& a, const Gb
     const int lds_lo = qy * ST_TCOLS * 4 + 8 + 8 * px_lo, lds_hi = qy * ST_TCOLS * 4 + 8 + 8 * px_hi;
     const int sts_row = (qy & 1) * E0_PLANE + (qy >> 1) * E0_IC * 16;
     const int slot_lo = sts_row + px_lo * 16, slot_hi = sts_row + px_hi * 16;
-    auto tile_q = [&](int q) { return l0_tile(tring[(q >> 1) & 7], a.td); };
     auto park = [&](int q, const QuadPark& P) {
         if (!active) return;
         uint8_t* tdst = smem + ((q >> 1) & 1) * E0_SMEM + (q & 1) * (ST_ROWS / 2) * E0_IC * 16;
@@ -632,8 +633,8 @@ __device__ __forceinline__ void produce_features_tma(const Enc0Args& a, const Gb
         for (int e = 0; e < 4; ++e)
             *reinterpret_cast<uint2*>(tdst + (e < 2 ? slot_lo : slot_hi) + (e & 1) * 8) = P.v[e];
     };
-    auto phaseA = [&](int q, QuadRegs& R, QuadPark& P) {
-        const L0Tile tl = tile_q(q);
+    auto phaseA = [&](int q, int tile, QuadRegs& R, QuadPark& P) {
+        const L0Tile tl = l0_tile(tile, a.td);
         const int sidx = q & 1;
         if (!active) return;
         const FrameK& F = a.tab.f[tl.f];
@@ -707,8 +708,7 @@ __device__ __forceinline__ void produce_features_tma(const Enc0Args& a, const Gb
     };
     auto phaseB = [&](int q, const QuadRegs& R) {
         if (!active) return;
-        const L0Tile tl = tile_q(q);
-        const float bias = a.tab.f[tl.f].fbias;
+        const float bias = tbias[(q >> 1) & 7];
         uint8_t* dst = smem + ((q >> 1) & 1) * E0_SMEM + (q & 1) * (ST_ROWS / 2) * E0_IC * 16;
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
@@ -725,10 +725,11 @@ __device__ __forceinline__ void produce_features_tma(const Enc0Args& a, const Gb
     };
     // live: half q belongs to a claimed tile (the TMA thread's sentinel, -1,
     // ends the loop after the last half's phase B)
-    auto step = [&](int q, bool live, QuadRegs& RA, QuadRegs& RB) {
+    auto step = [&](int q, int tile, QuadRegs& RA, QuadRegs& RB) {
+        const bool live = tile >= 0;
         QuadPark P;
         if (live) {
-            if (!(kExp && (a.dbg & 1))) phaseA(q, RA, P);
+            if (!(kExp && (a.dbg & 1))) phaseA(q, tile, RA, P);
             else for (int e = 0; e < 4; ++e) RA.look[e] = -1.f, P.v[e] = make_uint2(0u, 0u);
             __syncwarp();
             if (lane == 0) mbar_arrive(&empty[q & 1]);                   // stage read
@@ -757,9 +758,9 @@ __device__ __forceinline__ void produce_features_tma(const Enc0Args& a, const Gb
 #pragma unroll 1
     for (int q = 0;; ++q) {
         mbar_wait(&full[q & 1], (q >> 1) & 1);             // data (or the sentinel) for half q
-        const bool live = tring[(q >> 1) & 7] >= 0;
-        step(q, live, RA, RB);
-        if (!live) break;
+        const int tile = tring[(q >> 1) & 7];
+        step(q, tile, RA, RB);
+        if (tile < 0) break;
         const QuadRegs t = RA;
         RA = RB;
         RB = t;
