@@ -214,3 +214,28 @@ def test_host_pipeline_five_planes():
     pipe.synchronize()
     for ho, ref in zip(outs, refs):
         torch.testing.assert_close(ho, ref, rtol=0, atol=0)
+
+
+@pytest.mark.parametrize("hw", [(100, 164), (72, 250), (130, 96)])
+def test_infer5_odd_shapes_vs_oracle(hw):
+    """The fused 5-plane path on frames whose size is not a multiple of 16
+    (padded level-0 grid, partial feat5 / enc0_s2d tiles, widths that are
+    not a multiple of 4 -> scalar G-buffer loads) vs the oracle forward on
+    the oracle's 5 planes, fp16 bars."""
+    from oracle import network as on
+    from paper_2301_05262_b200 import network, producer, scenes
+    from paper_2301_05262_b200.infer import ShadowInference
+    h, wd = hw
+    fr = scenes.make_frame(scenes.random_scene(12, seed=h + wd, emitter_radius_m=0.3), (h, wd), (512, 512))
+    inp = producer.render_inputs([fr])
+    cfg, w = _weights5(seed=4)
+    y = ShadowInference(network.Plan(w, cfg, "fp16"), [fr], out_dtype="fp32")(inp)[0, 0].cpu().numpy()
+    ref5, cov, _ = _oracle5(fr, inp)
+    hp, wp = (h + 15) // 16 * 16, (wd + 15) // 16 * 16
+    xp = np.zeros((5, hp, wp), np.float32)
+    xp[:, :h, :wd] = ref5
+    ref = on.forward({k: v.data for k, v in w.items()}, xp)[0, :h, :wd]
+    d = y.astype(np.float64) - ref
+    mx, mse = float(np.abs(d).max()), float(np.mean(d * d))
+    print(f"{hw} 5-plane fp16: max {mx:.3g} mse {mse:.3g}")
+    assert mx <= MAX_ABS and mse <= MAX_MSE
