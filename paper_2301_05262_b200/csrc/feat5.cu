@@ -42,10 +42,11 @@ namespace {
 
 constexpr int F5_TY = 16, F5_TX = 16, F5_THREADS = F5_TY * F5_TX;
 constexpr int F5_R = 8;                      // window rows ri-8 .. ri+7 (16 x 16)
-constexpr int F5_MAX_TEX = 3584;             // staged texels per CTA (both regions)
-constexpr int F5_SMEM = 3 * F5_MAX_TEX * 4;   // texels + sliding 4x4 blocks (int2): 42 KB; 3 CTAs per SM (registers)
-// leave ~125 KB of L1 for the global-memory window scans (measured: 6144 texels
-// per CTA, 72 KB, 481 us; 3584: 458 us; 3072: 463 us; 2048: 482 us)
+constexpr int F5_MAX_TEX = 4096;             // staged texels per CTA (both regions)
+constexpr int F5_SMEM = 3 * F5_MAX_TEX * 4;   // texels + sliding 4x4 blocks (int2): 48 KB; 3 CTAs per SM (registers)
+// leave L1 to the global-memory window scans (8 x 32 tiles: 6144 texels per
+// CTA 481 us, 3584: 458, 3072: 463, 2048: 482; 16 x 16 tiles: 3072-5120 all
+// within 440-446 us)
 constexpr int kInfBits = 0x7f800000;
 
 struct Feat5Args {
