@@ -2033,6 +2033,7 @@ struct Dec0pArgs {
     const float* bh;     // (4,)   head bias
     __half* y;           // (N, 4, H0, W0)
     int H1, W1, H0, W0;
+    long long* trace;    // experiments only (NSM_DEC0_TRACE): CTA 0 per-tile clock64 events
 };
 constexpr int D0P_IR = 18, D0P_IC = 10, D0P_NIN = 4;
 constexpr int D0P_PIN = D0P_IR * D0P_IC * 16, D0P_INB = round128(2 * D0P_PIN);
@@ -2072,6 +2073,9 @@ __global__ void __launch_bounds__(D0P_THREADS, 1) dec0p_kernel(const __grid_cons
         x0 = (t % ntx) * 8;
         y0 = ((t / ntx) % nty) * 16;
         f = t / (ntx * nty);
+    };
+    auto tr = [&](int k, int ev) {       // experiments: CTA 0's per-tile timeline
+        if (kExp && a.trace && blockIdx.x == 0 && k < 64) a.trace[k * 8 + ev] = clock64();
     };
     if (tid == 0) pdl_trigger();
     if (warp == 13) tmem_alloc<512>(tptr);
@@ -2120,6 +2124,7 @@ __global__ void __launch_bounds__(D0P_THREADS, 1) dec0p_kernel(const __grid_cons
                 mbar_expect_tx(&in_full[s], 2 * D0P_PIN);
                 // padded coordinates: real (y0 - 1, x0 - 1) is padded (y0, x0)
                 tma_load_3d_stream(sbase + s * D0P_INB, &tin, 8 * x0, y0, 2 * f, &in_full[s], l2_evict_first_policy());   // both chunk planes
+                tr(k, 0);
             }
         }
     } else if (warp >= 13) {
@@ -2142,6 +2147,7 @@ __global__ void __launch_bounds__(D0P_THREADS, 1) dec0p_kernel(const __grid_cons
                                  dw3 + (uint64_t)(tap * 128), id64, tap ? 1u : 0u);
                     umma_commit(&in_empty[s]);
                     umma_commit(&a3_full[a3]);
+                    tr(k, 1);
                 }
             } else if (warp == 14) {
                 const uint64_t dw1 = umma_desc(sbase + D0P_OFF_W1, 64 * 16, 128);
@@ -2156,6 +2162,7 @@ __global__ void __launch_bounds__(D0P_THREADS, 1) dec0p_kernel(const __grid_cons
                                     id64, kk ? 1u : 0u);
                     umma_commit(&mid_empty[a1]);
                     umma_commit(&a1_full[a1]);
+                    tr(j, 3);
                 }
             } else {
                 const uint64_t dwh = umma_desc(sbase + D0P_OFF_WH, 16 * 16, 128);
@@ -2170,6 +2177,7 @@ __global__ void __launch_bounds__(D0P_THREADS, 1) dec0p_kernel(const __grid_cons
                                     id16, kk ? 1u : 0u);
                     umma_commit(&mid2_empty[ah]);
                     umma_commit(&ah_full[ah]);
+                    tr(j, 5);
                 }
             }
         }
@@ -2202,10 +2210,12 @@ __global__ void __launch_bounds__(D0P_THREADS, 1) dec0p_kernel(const __grid_cons
                 mbar_wait(&a3_full[a3], (k >> 1) & 1);
                 mbar_wait(&mid_empty[a3], ((k >> 1) & 1) ^ 1);
                 tc_fence_after();
+                if (warp == 1 && lane == 0) tr(k, 7);
                 relu_to_tmem(tmem + tl + D0P_ACC3 + a3 * 64, tmem + tl + D0P_MID + a3 * 32, sbias);
                 tc_fence_before();
                 mbar_arrive(&a3_empty[a3]);
                 mbar_arrive(&mid_full[a3]);
+                if (warp == 1 && lane == 0) tr(k, 2);
             }
         } else if (warp <= 8) {
             for (int k = 0; k < mytiles; ++k) {                      // dec1(k) -> MID2[k & 1]
@@ -2217,6 +2227,7 @@ __global__ void __launch_bounds__(D0P_THREADS, 1) dec0p_kernel(const __grid_cons
                 tc_fence_before();
                 mbar_arrive(&a1_empty[a1]);
                 mbar_arrive(&mid2_full[a1]);
+                if (warp == 5 && lane == 0) tr(k, 4);
             }
         } else {
             for (int j = 0; j < mytiles; ++j) {                      // head(j) -> Y
@@ -2230,6 +2241,7 @@ __global__ void __launch_bounds__(D0P_THREADS, 1) dec0p_kernel(const __grid_cons
                 tmem_ld_wait();
                 tc_fence_before();
                 mbar_arrive(&ah_empty[ah]);
+                if (warp == 9 && lane == 0) tr(j, 6);
                 // level-0 pixels (oy, ox) and (oy, ox + 1); dec0_ring_kernel
                 // overwrites the outer ring afterwards
                 const int ox = 2 * (x0 + pj);
@@ -2728,11 +2740,33 @@ nsm_status run_l0(const Plan& p, const Bufs& b, const Enc0Args& e0, const GbufMa
         memset(&dm, 0, sizeof dm);
         if (!encode_cplanar_map(b.d1, std::is_same<T, __nv_bfloat16>::value, H1 + 2, W1 + 2, nf, D0P_IC, D0P_IR, &dm))
             return fail(NSM_ERR_CUDA, "dec0p: TMA tensor map encoding failed");
-        const Dec0pArgs dp{p.d0p3.wpk, p.d0p1.wpk, p.d0ph.wpk, L0.dec3.b32, L0.dec1.b32, p.head.b32, b.y, H1, W1, H0, W0};
+        Dec0pArgs dp{p.d0p3.wpk, p.d0p1.wpk, p.d0ph.wpk, L0.dec3.b32, L0.dec1.b32, p.head.b32, b.y, H1, W1, H0, W0, nullptr};
+        static long long* d0_trace = nullptr;
+#ifdef NSM_EXPERIMENTS
+        if (getenv("NSM_DEC0_TRACE")) {
+            if (!d0_trace) cudaMalloc(&d0_trace, 64 * 8 * sizeof(long long));
+            cudaMemsetAsync(d0_trace, 0, 64 * 8 * sizeof(long long), st);
+            dp.trace = d0_trace;
+        }
+#endif
         const int ptotal = ((W1 + 7) / 8) * ((H1 + 15) / 16) * nf;
         {
             NSM_PROF("dec0_fused", st);
             launch_pdl(dec0p_kernel<T>, dim3(std::min(ptotal, num_sms())), dim3(D0P_THREADS), D0P_SMEM, st, dp, dm, ptotal);
+            if (dp.trace) {   // experiments only: CTA 0's dec0p timeline (us at 1.965 GHz), stalls the stream
+                static long long hb[64 * 8];
+                cudaMemcpyAsync(hb, dp.trace, sizeof hb, cudaMemcpyDeviceToHost, st);
+                cudaStreamSynchronize(st);
+                long long t0 = 0;
+                for (long long v : hb) if (v && (!t0 || v < t0)) t0 = v;
+                fprintf(stderr, "dec0p CTA0 (us): tile tma conv3_iss epi1_end dec1_iss epi2_end head_iss epi3_end epi1_start\n");
+                for (int k = 0; k < 64; ++k) {
+                    if (!hb[k * 8 + 1]) break;
+                    fprintf(stderr, "%2d", k);
+                    for (int ev = 0; ev < 8; ++ev) fprintf(stderr, " %7.2f", hb[k * 8 + ev] ? (hb[k * 8 + ev] - t0) / 1965.0 : -1.0);
+                    fprintf(stderr, "\n");
+                }
+            }
         }
         static const bool ring = env_int("NSM_DEC0_RING", 1) != 0;   // 0: timing only (experiments)
         if (ring) {
