@@ -274,6 +274,18 @@ def peaks():
     return 6650.0, 1590.0, "fallback"
 
 
+def sustained_tflops():
+    """Dense bf16 TFLOP/s sustained under the power cap (the denominator for
+    kernels timed inside a long step); the recipe's fallback otherwise."""
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            j = json.load(f)
+        if "bf16_tflops_sustained" in j:
+            return j["bf16_tflops_sustained"], "measured"
+    return 1400.0, "fallback"
+
+
 # --------------------------------------------------------------------------
 # algorithmic cost models (DESIGN.md section 7, "roofline accounting")
 # --------------------------------------------------------------------------
@@ -313,6 +325,52 @@ def kernel_models(frames, inputs, cfg, dtype, features):
     step_bytes = 28 * px + 4 * cov + px * act
     step_flops = 2.0 * n * hp * wp * sum(s["flops_per_pixel"] for s in st)
     return models, step_bytes, step_flops
+
+
+# tensor-core kernels of the 16-bit path -> (level, convolutions they run);
+# dec0 = dec0_fused (polyphase tcgen05 interior) + dec0_ring (outer ring)
+LEVEL_KERNELS = {
+    "enc0_fused": (0, ("enc3", "enc1")), "enc0_s2d": (0, ("enc3", "enc1")),
+    "lv1_enc": (1, ("enc3", "enc1")), "lv2_enc": (2, ("enc3", "enc1")), "lv3_bott": (3, ("enc3", "enc1")),
+    "lv2_dec": (2, ("dec3", "dec1")), "lv1_dec": (1, ("dec3", "dec1")),
+    "dec0_fused+dec0_ring": (0, ("dec3", "dec1", "head")),
+}
+
+
+def kernel_flops(cfg, hp, wp, n):
+    """Algorithmic flops (2 x MACs) per step of each tensor-core kernel of
+    the fused 16-bit path, from the reference's level plan (network.py:44-118,
+    the same per-level terms as net_stats); they sum to the step's flops."""
+    from paper_2301_05262_b200 import network
+    plan, head = network.level_plan(cfg)
+    shift = 1 if cfg.use_space_to_depth else 0
+    ks = dict(network._TAGS)
+    out = {}
+    for name, (j, tags) in LEVEL_KERNELS.items():
+        if j >= len(plan):
+            continue
+        r = (hp >> (j + shift)) * (wp >> (j + shift))
+        macs = sum(plan[j][t][0] * plan[j][t][1] * ks[t] ** 2 for t in tags if t in plan[j])
+        if "head" in tags:
+            macs += head[0] * head[1]
+        out[name] = 2.0 * n * macs * r
+    return out
+
+
+def kernel_rooflines(prof, flops, steps, tflops_peak):
+    """Achieved TFLOP/s of each modelled tensor-core kernel (eager per-kernel
+    profile, CUDA events on the launching stream) against the sustained bf16
+    dense peak."""
+    rows = {}
+    for name, fl in flops.items():
+        parts = name.split("+")
+        if not all(p in prof for p in parts):
+            continue
+        ms = sum(prof[p][1] for p in parts) / steps
+        t = fl / (ms / 1e3) / 1e12
+        rows[name] = {"ms": round(ms, 5), "gflop": round(fl / 1e9, 2), "tflops": round(t, 1),
+                      "frac": round(t / tflops_peak, 4)}
+    return rows
 
 
 def ncu_traffic(kernel, algo_bytes, frames_per_launch, workload):
@@ -438,6 +496,9 @@ def run_ours(args):
     prof = profile_kernels(lambda: run.launch(inputs, check=False), args.steps)
     models, step_bytes, step_flops = kernel_models(frames, inputs, cfg, args.dtype, args.features)
     hbm, tfl, src = peaks()
+    tsus, tsrc = sustained_tflops()
+    kflops = (kernel_flops(cfg, (h + 15) // 16 * 16, (wd + 15) // 16 * 16, n)
+              if args.dtype != "fp32" else {})
     dom = max(prof, key=lambda k: prof[k][1]) if prof else None
     step_prof_ms = sum(v[1] for v in prof.values()) / max(args.steps, 1)
     # the roofline names the dominant kernel we have an algorithmic model for
@@ -549,6 +610,8 @@ def run_ours(args):
                               "tflops": round(step_flops / (ms / 1e3) / 1e12, 2)},
             "kernel_profile_ms_per_step": {k: round(v[1] / args.steps, 5) for k, v in
                                            sorted(prof.items(), key=lambda kv: -kv[1][1])},
+            "kernel_rooflines": {"peak_tflops": tsus, "peak": "bf16 dense sustained (" + tsrc + ")",
+                                 "kernels": kernel_rooflines(prof, kflops, args.steps, tsus)},
             "cpu_baseline": cpu,
             "e2e": e2e,
             "variants": variants,

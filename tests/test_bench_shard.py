@@ -144,3 +144,21 @@ def test_spawn_command_and_device_check(monkeypatch):
     monkeypatch.delenv("WORLD_SIZE", raising=False)
     with pytest.raises(SystemExit, match="CUDA device"):
         bench.maybe_spawn(args)          # no GPU in the build container
+
+
+def test_kernel_flop_model_sums_to_the_step():
+    """bench.py's per-kernel tensor flops (the level plan split by kernel)
+    add up to the whole network's flops (net_stats), for the default
+    4-plane net, the 5-plane net and a 4-level variant."""
+    from paper_2301_05262_b200 import network
+    for cfg in (network.NetworkConfig(), network.NetworkConfig(in_channels=5),
+                network.NetworkConfig(layers=4)):
+        hp, wp = 1088, 1920
+        fl = bench.kernel_flops(cfg, hp, wp, 8)
+        fl.pop("enc0_s2d")                       # the 5-plane twin of enc0_fused
+        total = 2.0 * 8 * hp * wp * sum(s["flops_per_pixel"] for s in network.net_stats(cfg, (hp, wp)))
+        assert sum(fl.values()) == pytest.approx(total, rel=1e-12)
+    prof = {"lv1_enc": (10, 0.4), "dec0_fused": (10, 0.5), "dec0_ring": (10, 0.1)}
+    rows = bench.kernel_rooflines(prof, bench.kernel_flops(network.NetworkConfig(), hp, wp, 8), 10, 1000.0)
+    assert set(rows) == {"lv1_enc", "dec0_fused+dec0_ring"}
+    assert rows["dec0_fused+dec0_ring"]["ms"] == pytest.approx(0.06)
