@@ -2806,25 +2806,25 @@ nsm_status pack_f16(Plan& p, std::vector<char>& blob, size_t& offset_out) {
     const bool bf = p.act == NSM_BF16;
     if (!f16_supported(p)) {
         // generic layer-by-layer path (net_gen16.cu): every conv as mma.sync
-        // B fragments in reference channel order
+        // B fragments in reference channel order.  Everything is packed
+        // before `blob` grows: the fp32 sources (c->w32) point into it
+        std::vector<std::pair<ConvW*, std::vector<uint32_t>>> items;
+        auto pack = [&](ConvW* c) {
+            std::vector<uint32_t> v;
+            if (bf) pack_frag<__nv_bfloat16>(c->w32, c->cout, c->cin, c->k, false, v);
+            else pack_frag<__half>(c->w32, c->cout, c->cin, c->k, false, v);
+            items.emplace_back(c, std::move(v));
+        };
         for (int j = 0; j < p.nlev; ++j)
-            for (ConvW* c : {&p.lev[j].enc3, &p.lev[j].enc1, &p.lev[j].dec3, &p.lev[j].dec1}) {
-                if (!c->present()) continue;
-                std::vector<uint32_t> v;
-                if (bf) pack_frag<__nv_bfloat16>(c->w32, c->cout, c->cin, c->k, false, v);
-                else pack_frag<__half>(c->w32, c->cout, c->cin, c->k, false, v);
-                const size_t off = (blob.size() + 255) / 256 * 256;
-                blob.resize(off + v.size() * 4);
-                memcpy(blob.data() + off, v.data(), v.size() * 4);
-                c->wpk = (const void*)(uintptr_t)off;
-            }
-        std::vector<uint32_t> v;
-        if (bf) pack_frag<__nv_bfloat16>(p.head.w32, p.head.cout, p.head.cin, p.head.k, false, v);
-        else pack_frag<__half>(p.head.w32, p.head.cout, p.head.cin, p.head.k, false, v);
-        const size_t off = (blob.size() + 255) / 256 * 256;
-        blob.resize(off + v.size() * 4);
-        memcpy(blob.data() + off, v.data(), v.size() * 4);
-        p.head.wpk = (const void*)(uintptr_t)off;
+            for (ConvW* c : {&p.lev[j].enc3, &p.lev[j].enc1, &p.lev[j].dec3, &p.lev[j].dec1})
+                if (c->present()) pack(c);
+        pack(&p.head);
+        for (auto& it : items) {
+            const size_t off = (blob.size() + 255) / 256 * 256;
+            blob.resize(off + it.second.size() * 4);
+            memcpy(blob.data() + off, it.second.data(), it.second.size() * 4);
+            it.first->wpk = (const void*)(uintptr_t)off;
+        }
         offset_out = blob.size();
         return NSM_OK;
     }

@@ -90,3 +90,31 @@ def test_five_plane_window_two_chunks():
         one = {k: v[i:i + 1].contiguous() for k, v in inp.items()}
         y1 = ShadowInference(plan, [frames[i]], out_dtype="fp16")(one).cpu()
         torch.testing.assert_close(y1[0], yb[i], rtol=0, atol=0)
+
+
+@pytest.mark.parametrize("dtype", ["fp16", "bf16"])
+def test_generic16_plan_packing_is_deterministic(dtype):
+    """Plans of the generic path built over and over, with host-heap churn in
+    between, give bitwise the same output.  (Regression: the generic packer
+    once read each conv's fp32 source through a pointer into the weight blob
+    it was growing, i.e. freed memory after the first reallocation: rare,
+    heap-dependent wrong outputs.)"""
+    import torch
+    from paper_2301_05262_b200 import network
+    c = NETS["l4_plain_in1"]
+    layers, base, inc, s2d, cap = (int(v) for v in c["cfg"])
+    cfg = network.NetworkConfig(layers, base, inc, bool(s2d), cap)
+    x = torch.from_numpy(np.ascontiguousarray(c["x"][None])).cuda()
+    first = None
+    junk = []
+    for i in range(24):
+        junk.append(bytearray(4096 * (i % 7 + 1)))       # move the host allocator around
+        plan = network.Plan(c["w"], cfg, dtype)
+        y = plan.forward(x).cpu().numpy()
+        if first is None:
+            first = y
+        np.testing.assert_array_equal(y, first)
+        if i % 3 == 2:
+            junk.clear()
+    d = np.asarray(first[0], np.float64) - c["y"]
+    assert float(np.mean(d * d)) <= 1e-4
